@@ -1,0 +1,249 @@
+/*
+ * sst_gpu.h -- C ABI of the B200 (sm_100a) sphere-tracing subsurface renderer.
+ *
+ * This is the drop-in boundary for the reference's hot path (reference =
+ * /root/reference, "sstrace", C++20, namespace sst). The reference has no FFI
+ * layer; its path sits behind plain C++ functions. Each entry point below
+ * names the reference interface it replaces (file:line under
+ * /root/reference/proj/core/). A header-only C++ mirror that rethrows the
+ * reference's std:: exception types lives in include/sst_b200.hpp.
+ *
+ * Conventions
+ *  - extern "C", plain pointers and sizes, no exceptions cross the boundary.
+ *  - Return codes mirror the reference's exception classes:
+ *      SST_OK                 0
+ *      SST_E_INVALID_ARGUMENT 1  std::invalid_argument (bad shapes/config)
+ *      SST_E_RUNTIME          2  std::runtime_error (I/O, bad magic, wrong kind,
+ *                                decoder non-finite twice: scatter.cpp:44-58)
+ *      SST_E_DOMAIN           3  std::domain_error (out-of-range physics,
+ *                                optics.cpp:16-25, scatter.cpp:34-38)
+ *      SST_E_CUDA             4  CUDA failure / no device (there is NO CPU
+ *                                fallback: the library fails loudly)
+ *    The message of the last failure on the calling thread is returned by
+ *    sst_gpu_last_error().
+ *  - One context per device. Calls on one context are serialised on the
+ *    context's CUDA stream. Host buffers are caller-owned and copied; device
+ *    buffers passed with SST_PTR_DEVICE must live on the context's device.
+ *  - Films are returned as SUMS (sum of radiance and of radiance^2 per pixel and
+ *    channel) so that sample-slab shards add up across GPUs.
+ */
+#ifndef SST_GPU_H
+#define SST_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SST_GPU_ABI_VERSION 1
+
+enum {
+    SST_OK = 0,
+    SST_E_INVALID_ARGUMENT = 1,
+    SST_E_RUNTIME = 2,
+    SST_E_DOMAIN = 3,
+    SST_E_CUDA = 4
+};
+
+/* Arithmetic of the device path. F32 is the production path; F64 is the
+ * parity mode (same kernels instantiated in double). */
+enum { SST_PREC_F32 = 0, SST_PREC_F64 = 1 };
+
+/* Integrators: brute-force delta tracking (reference mode)
+ * and learned sphere tracing. */
+enum { SST_INTEGRATOR_PT = 0, SST_INTEGRATOR_ST = 1 };
+
+/* Where the pointers of a batch call live. */
+enum { SST_PTR_HOST = 0, SST_PTR_DEVICE = 1 };
+
+/* Reference model kinds (cvae.hpp:16-20, ModelKind). */
+enum { SST_MODEL_LENGTH = 0, SST_MODEL_PATH = 1, SST_MODEL_EVENT = 2 };
+
+/* Stream salts (rng.hpp:53-63, namespace stream_salt). */
+#define SST_SALT_DATASET 0x01u
+#define SST_SALT_RENDER_PIXEL 0x06u
+#define SST_SALT_RENDER_CHANNEL 0x07u
+
+typedef struct sst_gpu_ctx sst_gpu_ctx;
+
+/* ------------------------------------------------------------------------ */
+/* Context                                                                   */
+/* ------------------------------------------------------------------------ */
+
+int sst_gpu_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* sst_gpu_last_error(void);
+
+/* Creates a context on `device` (CUDA ordinal). Fails with SST_E_CUDA when no
+ * device is present -- there is no CPU fallback. */
+int sst_gpu_create(int device, sst_gpu_ctx** out);
+void sst_gpu_destroy(sst_gpu_ctx* ctx);
+/* SST_PREC_F32 (default) or SST_PREC_F64. */
+int sst_gpu_set_precision(sst_gpu_ctx* ctx, int precision);
+int sst_gpu_get_device(const sst_gpu_ctx* ctx);
+/* The context's cudaStream_t (as void*), for callers that enqueue their own
+ * work (e.g. a torch/NCCL film reduce) behind ours. */
+void* sst_gpu_stream(sst_gpu_ctx* ctx);
+int sst_gpu_synchronize(sst_gpu_ctx* ctx);
+
+/* ------------------------------------------------------------------------ */
+/* CVAE-weight interface: replaces ScatterModels / CvaeModel / load_model     */
+/* (scatter.hpp:28-39, scatter.cpp:22-32, cvae.hpp:52-60, cvae.cpp:379-425)   */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    uint32_t out_dim;
+    uint32_t in_dim;
+    const float* weights; /* row-major [out_dim x in_dim] (mlp.hpp:18-23) */
+    const float* bias;    /* [out_dim] */
+} sst_layer_desc;
+
+typedef struct {
+    uint32_t kind; /* SST_MODEL_* ; checked like scatter.cpp:15-27 */
+    uint32_t p_in, p_out, depth, width, latent; /* CvaeSpec (cvae.hpp:29-38) */
+    double sigma_ref, n_ref;                    /* NormConstants (cvae.hpp:43-50) */
+    uint32_t n_layers;
+    const sst_layer_desc* layers; /* decoder only: input latent+p_in -> 2*p_out */
+} sst_model_desc;
+
+/* Uploads the three decoders (LengthGen, PathGen, EventGen), kind-checked.
+ * Only the production architectures of Table 1 (CvaeSpec::production_default,
+ * cvae.cpp:51-58) have compiled device evaluators; other shapes return
+ * SST_E_INVALID_ARGUMENT. */
+int sst_gpu_upload_models(sst_gpu_ctx* ctx, const sst_model_desc models[3]);
+/* Parses dir/{lengthgen,pathgen,eventgen}.ssnn (SSNN v1, cvae.cpp:349-425) and
+ * uploads them: the equivalent of ScatterModels::load_dir (scatter.cpp:29-32). */
+int sst_gpu_load_models_dir(sst_gpu_ctx* ctx, const char* dir);
+
+/* ------------------------------------------------------------------------ */
+/* RandomStream helpers (rng.hpp:15-50). The stream state after construction */
+/* is one u64; draw k is mix(state + k * 0x9E3779B97F4A7C15).                */
+/* ------------------------------------------------------------------------ */
+
+uint64_t sst_rng_init(uint64_t seed, uint64_t s1, uint64_t s2, uint64_t s3);
+
+/* ------------------------------------------------------------------------ */
+/* Per-step operator: replaces sample_sphere_step (scatter.hpp:119-122,       */
+/* scatter.cpp:152-177). n independent steps; vectors are xyz-interleaved.   */
+/* rng_state[i] is the RandomStream state on entry and is advanced in place   */
+/* by exactly the draws the reference consumes (7 / 24 / 46 per absorbed /   */
+/* survived / survived+event outcome, plus retries).                          */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    const double* sigma_t;   /* [n] world extinction */
+    const double* g;         /* [n] */
+    const double* phi;       /* [n] */
+    const double* w_in;      /* [3n] unit incoming direction */
+    const double* center;    /* [3n] */
+    const double* r_sphere;  /* [n] */
+    const uint8_t* with_event; /* [n] 0/1, or NULL = all with_event_default */
+    uint64_t* rng_state;     /* [n] in/out */
+} sst_step_in;
+
+typedef struct {
+    uint8_t* absorbed;       /* [n] */
+    uint32_t* n_events;      /* [n] */
+    double* exit_position;   /* [3n] */
+    double* exit_direction;  /* [3n] */
+    uint8_t* has_representative; /* [n] */
+    double* rep_position;    /* [3n] */
+    double* rep_direction;   /* [3n] */
+    double* lambda_weight;   /* [n] */
+} sst_step_out;
+
+typedef struct {
+    uint64_t length, path, event; /* DecodeCounters (scatter.hpp:18-25) */
+} sst_decode_counters;
+
+int sst_gpu_sphere_step_batch(sst_gpu_ctx* ctx, uint64_t n, const sst_step_in* in,
+                              int with_event_default, sst_step_out* out, int ptr_kind,
+                              sst_decode_counters* counters /* may be NULL; accumulated */);
+
+/* ------------------------------------------------------------------------ */
+/* Scene: mesh + medium + SDF per object, point light, camera, background.   */
+/* SPEC.md:526-529 (Scene), mesh.hpp:15-30, sdf.hpp:19-33, optics.hpp:16-26. */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    double sigma_t, g, phi; /* MediumParams; validated like optics.cpp:21-25 */
+} sst_medium;
+
+typedef struct {
+    const double* positions;  /* [3 * n_vertices] */
+    uint32_t n_vertices;
+    const uint32_t* triangles; /* [3 * n_triangles], outward CCW winding */
+    uint32_t n_triangles;
+    sst_medium media[3];      /* per RGB channel */
+    /* Conservative SDF grid of THIS object (SdfGrid, sdf.hpp:19-33):
+     * values z-major (z*dy + y)*dx + x, negative inside, already reduced by
+     * half the voxel diagonal. values == NULL asks the library to build it on
+     * the GPU at `sdf_resolution` voxels along the largest axis (build_sdf,
+     * sdf.cpp:20-58; bit-identical to the reference's FP64 build). */
+    double sdf_origin[3];
+    double sdf_voxel;
+    uint32_t sdf_dims[3];
+    const float* sdf_values;
+    uint32_t sdf_resolution;
+} sst_object_desc;
+
+typedef struct {
+    uint32_t n_objects;
+    const sst_object_desc* objects;
+    double light_position[3]; /* point light */
+    double light_power[3];    /* Phi per channel; inverse-square falloff */
+    double background[3];     /* radiance added when a path escapes */
+    double cam_position[3];
+    double cam_look_at[3];
+    double cam_up[3];
+    double cam_vfov_deg;
+    uint32_t width, height;
+    double r_min;             /* <= 0: max(2/sigma_t, 1.5 voxel) */
+    uint32_t max_pt_events;   /* 0: 1e6 */
+    uint32_t max_st_steps;    /* 0: 1e5 */
+} sst_scene_desc;
+
+/* Uploads the scene: builds the BVH on the host, builds missing SDFs on the
+ * GPU, copies everything to device memory owned by the context. */
+int sst_gpu_upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* scene);
+/* Copies back the SDF grid of object `obj` (values may be NULL to query the
+ * dims/origin/voxel only). */
+int sst_gpu_get_sdf(sst_gpu_ctx* ctx, uint32_t obj, double origin[3], double* voxel,
+                    uint32_t dims[3], float* values);
+
+/* PathStats plus bookkeeping. */
+typedef struct {
+    uint64_t paths;          /* traced (pixel, sample, channel) paths */
+    uint64_t segments;       /* sphere_steps + pt_events */
+    uint64_t sphere_steps;
+    uint64_t pt_events;      /* delta-tracking collisions (PT, or ST fallback) */
+    uint64_t decodes_length, decodes_path, decodes_event;
+    uint64_t absorbed, escaped, capped, errors;
+    uint64_t shadow_rays;
+    double device_ms;        /* kernel time of the render call */
+} sst_path_stats;
+
+/* Renders samples [sample_begin, sample_end) of an spp_total frame and ADDS
+ * into film_sum / film_sumsq ([3 * width * height], row 0 on top, RGB
+ * interleaved; Image layout of image.hpp:13-29). Pointers are host or device
+ * per ptr_kind (device: double, must be zeroed by the caller before the first
+ * slab). RNG keys: camera jitter RandomStream(seed, kRenderPixel, pixel,
+ * sample); path RandomStream(seed, kRenderChannel, pixel, 3*sample+channel).
+ * stats is accumulated (may be NULL). */
+int sst_gpu_render(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total,
+                   uint32_t sample_begin, uint32_t sample_end, uint64_t seed, double* film_sum,
+                   double* film_sumsq, int ptr_kind, sst_path_stats* stats);
+
+/* Per-path parity entry: traces n explicit (pixel, sample, channel) paths and
+ * returns their radiance and segment counts (host pointers). */
+int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
+                        const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                        double* radiance, uint32_t* segments, sst_path_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SST_GPU_H */
