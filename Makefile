@@ -1,0 +1,43 @@
+# Builds the B200 library (sm_100a only) and the CPU oracle.
+#   make            -> paper_2011_03082_b200/libsst_gpu.so + oracle/liboracle.so (+ oracle/_ref if the
+#                      reference sources are present)
+#   make lib        -> only the product library
+NVCC ?= nvcc
+ARCH = -gencode arch=compute_100a,code=sm_100a
+NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall
+CSRC = paper_2011_03082_b200/csrc
+BUILD = build
+LIB = paper_2011_03082_b200/libsst_gpu.so
+HDRS = $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/sst_gpu.h include/sst_host.h
+
+.PHONY: all lib oracle clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(BUILD)/kernels_f32.o: $(CSRC)/kernels_f32.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_f32.log || (cat $(BUILD)/ptxas_f32.log; false)
+
+# FP64 parity instantiation: no FMA contraction (matches the reference's rounding).
+$(BUILD)/kernels_f64.o: $(CSRC)/kernels_f64.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -fmad=false -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_f64.log || (cat $(BUILD)/ptxas_f64.log; false)
+
+$(BUILD)/api.o: $(CSRC)/api.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/host.o: $(CSRC)/host.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(BUILD)/kernels_f32.o $(BUILD)/kernels_f64.o $(BUILD)/api.o $(BUILD)/host.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
+
+oracle:
+	$(MAKE) -C oracle all
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+	$(MAKE) -C oracle clean

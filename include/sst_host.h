@@ -1,0 +1,43 @@
+/*
+ * sst_host.h -- host-side utilities of libsst_gpu.so (no device work): meshes,
+ * SDF cache files and PFM output, C ABI mirrors of the reference's host
+ * functions so that callers can build scenes without the reference library.
+ * Return codes as in sst_gpu.h; messages via sst_gpu_last_error().
+ */
+#ifndef SST_HOST_H
+#define SST_HOST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* make_icosphere (mesh.hpp:46-48, mesh.cpp:154-185): identical vertex/face
+ * order. Buffers are allocated by the library; free with sst_mesh_free. */
+int sst_mesh_icosphere(int subdivisions, double radius, double** positions, uint32_t* n_vertices,
+                       uint32_t** triangles, uint32_t* n_triangles);
+/* make_bumpy_sphere (mesh.hpp:50-53, mesh.cpp:187-197). */
+int sst_mesh_bumpy_sphere(int subdivisions, double radius, double amplitude, double frequency,
+                          double** positions, uint32_t* n_vertices, uint32_t** triangles,
+                          uint32_t* n_triangles);
+/* load_obj (mesh.hpp:37-43, mesh.cpp:77-122): v/f records, fan triangulation,
+ * negative indices, degenerate faces dropped and counted. */
+int sst_mesh_load_obj(const char* path, double scale, double** positions, uint32_t* n_vertices,
+                      uint32_t** triangles, uint32_t* n_triangles, uint64_t* dropped_degenerate);
+void sst_mesh_free(double* positions, uint32_t* triangles);
+
+/* SSDF cache files (sdf.cpp:71-101). */
+int sst_sdf_save(const char* path, const double origin[3], double voxel, const uint32_t dims[3],
+                 const float* values, uint64_t mesh_fingerprint);
+int sst_sdf_load(const char* path, double origin[3], double* voxel, uint32_t dims[3],
+                 float** values, uint64_t* mesh_fingerprint);
+void sst_sdf_free(float* values);
+
+/* save_pfm (image.cpp:32-41): little-endian "PF", bottom row first. */
+int sst_image_save_pfm(const char* path, uint32_t width, uint32_t height, const float* rgb);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,241 @@
+"""Python host API over the C ABI (include/sst_gpu.h) -- mirrors the reference's
+C++ interfaces for this path (namespace sst, /root/reference/proj/core):
+
+  ScatterModels::load_dir (scatter.cpp:29-32)   -> Renderer.load_models_dir
+  sample_sphere_step      (scatter.cpp:152-177) -> Renderer.sample_sphere_step_batch
+  make_icosphere / make_bumpy_sphere / load_obj (mesh.cpp) -> make_icosphere / ...
+  render(scene, integrator, spp, seed, nee) -> Renderer.render
+  Image / image_metrics   (image.hpp:13-29, image.cpp:16-30) -> Image / image_metrics
+
+Errors raise the reference's exception classes (abi.InvalidArgument ~
+std::invalid_argument, abi.DomainError ~ std::domain_error, abi.SstError ~
+std::runtime_error). Everything runs on the GPU; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import abi
+from .scene import Scene
+
+PT = abi.SST_INTEGRATOR_PT
+ST = abi.SST_INTEGRATOR_ST
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def rng_init(seed, s1=0, s2=0, s3=0) -> int:
+    """RandomStream(seed, s1, s2, s3) state (rng.hpp:17-23)."""
+    return abi.lib().sst_rng_init(seed, s1, s2, s3)
+
+
+def _mesh_out(fn, *args):
+    L = abi.lib()
+    pos = C.POINTER(C.c_double)()
+    tri = C.POINTER(C.c_uint32)()
+    nv, nt = C.c_uint32(), C.c_uint32()
+    extra = list(args)
+    abi.check(fn(*extra, C.byref(pos), C.byref(nv), C.byref(tri), C.byref(nt)))
+    try:
+        P = np.ctypeslib.as_array(pos, shape=(nv.value * 3,)).reshape(-1, 3).copy()
+        T = np.ctypeslib.as_array(tri, shape=(nt.value * 3,)).reshape(-1, 3).copy()
+    finally:
+        L.sst_mesh_free(C.cast(pos, C.c_void_p), C.cast(tri, C.c_void_p))
+    return P, T
+
+
+def make_icosphere(subdivisions: int = 3, radius: float = 1.0):
+    return _mesh_out(abi.lib().sst_mesh_icosphere, subdivisions, radius)
+
+
+def make_bumpy_sphere(subdivisions=4, radius=1.0, amplitude=0.2, frequency=3.0):
+    return _mesh_out(abi.lib().sst_mesh_bumpy_sphere, subdivisions, radius, amplitude, frequency)
+
+
+def load_obj(path: str, scale: float = 1.0):
+    L = abi.lib()
+    pos = C.POINTER(C.c_double)()
+    tri = C.POINTER(C.c_uint32)()
+    nv, nt = C.c_uint32(), C.c_uint32()
+    dropped = C.c_uint64()
+    abi.check(L.sst_mesh_load_obj(path.encode(), scale, C.byref(pos), C.byref(nv), C.byref(tri),
+                                  C.byref(nt), C.byref(dropped)))
+    try:
+        P = np.ctypeslib.as_array(pos, shape=(nv.value * 3,)).reshape(-1, 3).copy()
+        T = np.ctypeslib.as_array(tri, shape=(nt.value * 3,)).reshape(-1, 3).copy()
+    finally:
+        L.sst_mesh_free(C.cast(pos, C.c_void_p), C.cast(tri, C.c_void_p))
+    return P, T, dropped.value
+
+
+@dataclass
+class Image:
+    """Linear-RGB float framebuffer, row 0 on top (image.hpp:13-29)."""
+    width: int
+    height: int
+    pixels: np.ndarray  # (height, width, 3) float32
+    sample_count: int = 0
+
+    def save_pfm(self, path: str):
+        px = np.ascontiguousarray(self.pixels, dtype=np.float32)
+        abi.check(abi.lib().sst_image_save_pfm(path.encode(), self.width, self.height, _p(px)))
+
+
+def image_metrics(a: Image, b: Image) -> Tuple[float, float]:
+    """Channel-pooled (RMSE, MAE) over linear values (image.cpp:16-30)."""
+    if a.width != b.width or a.height != b.height:
+        raise abi.InvalidArgument(abi.SST_E_INVALID_ARGUMENT, "image_metrics: dimension mismatch")
+    d = a.pixels.astype(np.float64) - b.pixels.astype(np.float64)
+    return float(np.sqrt(np.mean(d * d))), float(np.mean(np.abs(d)))
+
+
+@dataclass
+class Film:
+    """Accumulated per-pixel sums (what shards add up): sum and sum of squares."""
+    width: int
+    height: int
+    sum: np.ndarray    # (H*W*3,) float64
+    sumsq: np.ndarray  # (H*W*3,) float64
+    spp: int
+
+    def image(self) -> Image:
+        mean = (self.sum / max(self.spp, 1)).astype(np.float32).reshape(self.height, self.width, 3)
+        return Image(self.width, self.height, mean, self.spp)
+
+    def variance_of_mean(self) -> np.ndarray:
+        n = max(self.spp, 1)
+        m = self.sum / n
+        var = np.maximum(self.sumsq / n - m * m, 0.0)
+        return (var / max(n - 1, 1)).reshape(self.height, self.width, 3)
+
+
+class Renderer:
+    """One B200 context (sst_gpu_ctx): models, scene and launches."""
+
+    def __init__(self, device: int = 0, precision: str = "f32"):
+        L = abi.lib()
+        h = C.c_void_p()
+        abi.check(L.sst_gpu_create(device, C.byref(h)))
+        self.h = h
+        self.set_precision(precision)
+
+    def close(self):
+        if getattr(self, "h", None):
+            abi.lib().sst_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_precision(self, precision: str):
+        code = {"f32": abi.SST_PREC_F32, "f64": abi.SST_PREC_F64}[precision]
+        abi.check(abi.lib().sst_gpu_set_precision(self.h, code))
+        self.precision = precision
+
+    @property
+    def stream(self) -> int:
+        return abi.lib().sst_gpu_stream(self.h) or 0
+
+    def synchronize(self):
+        abi.check(abi.lib().sst_gpu_synchronize(self.h))
+
+    # -- CVAE-weight interface
+    def load_models_dir(self, directory: str):
+        abi.check(abi.lib().sst_gpu_load_models_dir(self.h, directory.encode()))
+
+    # -- per-step operator
+    def sample_sphere_step_batch(self, batch: dict, with_event_default: int = 1,
+                                 counters: Optional[abi.DecodeCounters] = None) -> dict:
+        """Batch of sample_sphere_step; batch['rng_state'] (uint64) is advanced in place."""
+        n = len(batch["sigma_t"])
+        f = lambda k: np.ascontiguousarray(batch[k], dtype=np.float64)
+        ins = {k: f(k) for k in ("sigma_t", "g", "phi", "w_in", "center", "r_sphere")}
+        we = batch.get("with_event")
+        ins["with_event"] = None if we is None else np.ascontiguousarray(we, dtype=np.uint8)
+        rs = batch["rng_state"]
+        if rs.dtype != np.uint64 or not rs.flags.c_contiguous:
+            raise abi.InvalidArgument(abi.SST_E_INVALID_ARGUMENT, "rng_state must be contiguous uint64")
+        out = dict(absorbed=np.zeros(n, np.uint8), n_events=np.zeros(n, np.uint32),
+                   exit_position=np.zeros((n, 3)), exit_direction=np.zeros((n, 3)),
+                   has_representative=np.zeros(n, np.uint8), rep_position=np.zeros((n, 3)),
+                   rep_direction=np.zeros((n, 3)), lambda_weight=np.zeros(n))
+        sin = abi.StepIn(_p(ins["sigma_t"]), _p(ins["g"]), _p(ins["phi"]), _p(ins["w_in"]),
+                         _p(ins["center"]), _p(ins["r_sphere"]), _p(ins["with_event"]), _p(rs))
+        sout = abi.StepOut(*(_p(out[k]) for k in ("absorbed", "n_events", "exit_position",
+                                                   "exit_direction", "has_representative",
+                                                   "rep_position", "rep_direction", "lambda_weight")))
+        abi.check(abi.lib().sst_gpu_sphere_step_batch(
+            self.h, n, C.byref(sin), with_event_default, C.byref(sout), abi.SST_PTR_HOST,
+            C.byref(counters) if counters is not None else None))
+        return out
+
+    # -- scene / render
+    def upload_scene(self, scene: Scene):
+        d = scene.to_desc()
+        abi.check(abi.lib().sst_gpu_upload_scene(self.h, C.byref(d)))
+        self.scene = scene
+
+    def get_sdf(self, obj: int = 0):
+        origin = np.zeros(3)
+        voxel = C.c_double()
+        dims = np.zeros(3, np.uint32)
+        abi.check(abi.lib().sst_gpu_get_sdf(self.h, obj, _p(origin), C.byref(voxel), _p(dims), None))
+        vals = np.empty(int(np.prod(dims.astype(np.int64))), np.float32)
+        abi.check(abi.lib().sst_gpu_get_sdf(self.h, obj, _p(origin), C.byref(voxel), _p(dims), _p(vals)))
+        return origin, voxel.value, dims, vals
+
+    def render_film(self, integrator: int, spp: int, seed: int = 1, nee: bool = True,
+                    sample_begin: int = 0, sample_end: Optional[int] = None,
+                    film: Optional[Film] = None,
+                    stats: Optional[abi.PathStats] = None) -> Tuple[Film, abi.PathStats]:
+        sc = self.scene
+        n = sc.width * sc.height * 3
+        if film is None:
+            film = Film(sc.width, sc.height, np.zeros(n), np.zeros(n), 0)
+        stats = stats if stats is not None else abi.PathStats()
+        end = spp if sample_end is None else sample_end
+        abi.check(abi.lib().sst_gpu_render(self.h, integrator, int(nee), spp, sample_begin, end, seed,
+                                           _p(film.sum), _p(film.sumsq), abi.SST_PTR_HOST,
+                                           C.byref(stats)))
+        film.spp += end - sample_begin
+        return film, stats
+
+    def render(self, integrator: int, spp: int, seed: int = 1, nee: bool = True):
+        """render(scene, integrator, spp, seed, nee) -> (Image, PathStats)."""
+        film, stats = self.render_film(integrator, spp, seed, nee)
+        return film.image(), stats
+
+    def render_device(self, integrator, spp_total, sample_begin, sample_end, seed, nee, sum_ptr,
+                      sumsq_ptr, stats=None):
+        """Accumulates into caller-owned DEVICE film buffers (e.g. torch tensors)."""
+        stats = stats if stats is not None else abi.PathStats()
+        abi.check(abi.lib().sst_gpu_render(self.h, integrator, int(nee), spp_total, sample_begin,
+                                           sample_end, seed, C.c_void_p(sum_ptr),
+                                           C.c_void_p(sumsq_ptr), abi.SST_PTR_DEVICE,
+                                           C.byref(stats)))
+        return stats
+
+    def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None):
+        pixel = np.ascontiguousarray(pixel, dtype=np.uint32)
+        sample = np.ascontiguousarray(sample, dtype=np.uint32)
+        channel = np.ascontiguousarray(channel, dtype=np.uint8)
+        n = len(pixel)
+        rad = np.empty(n)
+        seg = np.empty(n, np.uint32)
+        stats = stats if stats is not None else abi.PathStats()
+        abi.check(abi.lib().sst_gpu_trace_paths(self.h, integrator, int(nee), seed, n, _p(pixel),
+                                                _p(sample), _p(channel), _p(rad), _p(seg),
+                                                C.byref(stats)))
+        return rad, seg

@@ -1,0 +1,899 @@
+// api.cu -- implementation of the C ABI (include/sst_gpu.h, include/sst_host.h).
+//
+// Host C++ around the kernels: contexts, uploads (models -> __constant__, scene ->
+// BVH/SDF/medium tables in HBM), launches, error mapping. No exception crosses the
+// boundary; there is no CPU fallback -- without a CUDA device every compute entry
+// fails with SST_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sst_gpu.h"
+#include "../../include/sst_host.h"
+#include "host.h"
+#include "launch.h"
+#include "rng.cuh"
+#include "types.cuh"
+
+using namespace sstg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+#define CK(expr)                                                                                \
+    do {                                                                                        \
+        const cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                                  \
+            throw CudaFailure(std::string(#expr) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return SST_OK;
+    } catch (const InvalidArgument& e) {
+        g_last_error = e.what();
+        return SST_E_INVALID_ARGUMENT;
+    } catch (const DomainError& e) {
+        g_last_error = e.what();
+        return SST_E_DOMAIN;
+    } catch (const CudaFailure& e) {
+        g_last_error = e.what();
+        return SST_E_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return SST_E_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SST_E_RUNTIME;
+    }
+}
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n) {
+        if (n <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        CK(cudaMalloc(&p, n));
+        bytes = n;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct ObjectHost {
+    double sdf_origin[3];
+    double sdf_voxel;
+    uint32_t dims[3];
+    std::vector<float> sdf;
+    sst_medium media[3];
+};
+
+}  // namespace
+
+struct sst_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int precision = SST_PREC_F32;
+    uint64_t serial = 0;
+
+    bool models = false;
+    std::vector<double> weights;
+    double norms[6] = {};
+    uint64_t model_gen = 0;
+
+    bool scene = false;
+    std::vector<ObjectHost> objects;
+    sst_scene_desc desc{};
+    DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64;
+    std::vector<DevBuf> sdf_dev;
+    DevScene<float> sc32{};
+    DevScene<double> sc64{};
+
+    DevBuf radiance, segments, work, stats, error, film_sum, film_sq, keys_pix, keys_smp, keys_ch;
+    DevBuf step_in, step_out;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+std::mutex g_const_mu;
+std::map<int, std::pair<const sst_gpu_ctx*, uint64_t>> g_const_owner;  // device -> (ctx, gen)
+uint64_t g_serial = 0;
+
+void require_device(sst_gpu_ctx* ctx) {
+    if (!ctx) throw InvalidArgument("null context");
+    CK(cudaSetDevice(ctx->device));
+}
+
+// __constant__ memory is per device: re-upload when another context owns it.
+void ensure_constants(sst_gpu_ctx* ctx) {
+    if (!ctx->models) throw InvalidArgument("no models uploaded (sst_gpu_upload_models / sst_gpu_load_models_dir)");
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    auto it = g_const_owner.find(ctx->device);
+    if (it != g_const_owner.end() && it->second.first == ctx && it->second.second == ctx->model_gen) return;
+    CK(f32::upload_constants(ctx->weights.data(), ctx->norms, ctx->stream));
+    CK(f64::upload_constants(ctx->weights.data(), ctx->norms, ctx->stream));
+    g_const_owner[ctx->device] = {ctx, ctx->model_gen};
+}
+
+void set_models(sst_gpu_ctx* ctx, const HostModel (&m)[3]) {
+    std::vector<double> w;
+    double norms[6];
+    pack_models(m, w, norms);
+    ctx->weights = std::move(w);
+    std::memcpy(ctx->norms, norms, sizeof norms);
+    ctx->models = true;
+    ctx->model_gen = ++g_serial;
+}
+
+void validate_medium(const sst_medium& m) {  // MediumParams::validate (optics.cpp:21-25)
+    if (!(m.sigma_t >= 0.0)) throw DomainError("sigma_t must be >= 0");
+    if (!(m.g > -1.0 && m.g < 1.0)) throw DomainError("HG anisotropy g must lie in (-1, 1)");
+    if (!(m.phi >= 0.0 && m.phi <= 1.0)) throw DomainError("albedo phi must lie in [0, 1]");
+}
+
+template <class R>
+MediumK<R> medium_constants(const sst_medium& m, double r_min) {
+    MediumK<R> k{};
+    k.sigma_t = static_cast<R>(m.sigma_t);
+    k.g = static_cast<R>(m.g);
+    k.phi = static_cast<R>(m.phi);
+    k.log_phi = (m.phi > 0.0 && m.phi < 1.0) ? static_cast<R>(std::log(m.phi)) : R(0);
+    k.one_minus_phi = static_cast<R>(1.0 - m.phi);
+    k.r_min = static_cast<R>(r_min > 3e38 && !std::is_same<R, double>::value ? 3e38 : r_min);
+    // u < phi with u = (x >> 11) * 2^-53  <=>  (x >> 11) < ceil(phi * 2^53)
+    k.survive_below = static_cast<uint64_t>(std::ceil(m.phi * 9007199254740992.0));
+    k.phi_is_one = m.phi >= 1.0;
+    k.phi_is_zero = m.phi <= 0.0;
+    return k;
+}
+
+double r_min_of(const sst_scene_desc& d, const ObjectHost& o, int c) {
+    if (d.r_min > 0.0) return d.r_min;
+    const double s = o.media[c].sigma_t;
+    if (!(s > 0.0)) return 1e300;
+    return std::fmax(2.0 / s, 1.5 * o.sdf_voxel);
+}
+
+// build_sdf geometry (sdf.cpp:20-38) + exact FP64 GPU evaluation.
+void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, bool watertight) {
+    const uint32_t res = od.sdf_resolution ? od.sdf_resolution : 64;
+    if (res < 8) throw InvalidArgument("build_sdf: resolution must be >= 8");
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (uint32_t i = 0; i < od.n_vertices; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::fmin(lo[a], od.positions[3 * i + a]);
+            hi[a] = std::fmax(hi[a], od.positions[3 * i + a]);
+        }
+    const double ext[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+    const double me = std::fmax(ext[0], std::fmax(ext[1], ext[2]));
+    if (!(me > 0.0)) throw InvalidArgument("build_sdf: empty mesh bounds");
+    SdfBuildArgs a{};
+    a.voxel = me / res;
+    for (int k = 0; k < 3; ++k) {
+        a.origin[k] = lo[k] - a.voxel;
+        a.dims[k] = static_cast<uint32_t>(std::ceil(ext[k] / a.voxel - 1e-9)) + 2;
+    }
+    a.half_diagonal = 0.5 * std::sqrt(3.0) * a.voxel;
+    const double raw[3][3] = {{0.5380, 0.1123, 0.8354}, {-0.8312, 0.3052, 0.4643}, {0.1710, -0.9364, 0.3063}};
+    for (int k = 0; k < 3; ++k) {
+        const double len = std::sqrt(raw[k][0] * raw[k][0] + raw[k][1] * raw[k][1] + raw[k][2] * raw[k][2]);
+        for (int j = 0; j < 3; ++j) a.dirs[3 * k + j] = raw[k][j] / len;
+    }
+    a.watertight = watertight ? 1 : 0;
+    a.n_tris = od.n_triangles;
+    std::vector<double> tv(9ull * od.n_triangles);
+    for (uint32_t t = 0; t < od.n_triangles; ++t)
+        for (int c = 0; c < 3; ++c)
+            for (int k = 0; k < 3; ++k) tv[9ull * t + 3 * c + k] = od.positions[3ull * od.triangles[3 * t + c] + k];
+    const size_t nvox = static_cast<size_t>(a.dims[0]) * a.dims[1] * a.dims[2];
+    DevBuf dtv, dval;
+    dtv.reserve(tv.size() * sizeof(double));
+    dval.reserve(nvox * sizeof(float));
+    CK(cudaMemcpyAsync(dtv.p, tv.data(), tv.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    a.tri_vertices = dtv.as<double>();
+    a.values = dval.as<float>();
+    CK(launch_sdf_build(a, ctx->stream));
+    oh.sdf.resize(nvox);
+    CK(cudaMemcpyAsync(oh.sdf.data(), dval.p, nvox * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    dtv.release();
+    dval.release();
+    for (int k = 0; k < 3; ++k) {
+        oh.sdf_origin[k] = a.origin[k];
+        oh.dims[k] = a.dims[k];
+    }
+    oh.sdf_voxel = a.voxel;
+}
+
+template <class R>
+void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const DevBuf& tris, DevBuf& objs) {
+    const sst_scene_desc& d = ctx->desc;
+    std::vector<ObjK<R>> ok(ctx->objects.size());
+    for (size_t o = 0; o < ctx->objects.size(); ++o) {
+        const ObjectHost& oh = ctx->objects[o];
+        for (int c = 0; c < 3; ++c) ok[o].med[c] = medium_constants<R>(oh.media[c], r_min_of(d, oh, c));
+        for (int a = 0; a < 3; ++a) {
+            ok[o].sdf_origin[a] = static_cast<R>(oh.sdf_origin[a]);
+            ok[o].dims[a] = oh.dims[a];
+        }
+        ok[o].sdf_voxel = static_cast<R>(oh.sdf_voxel);
+        ok[o].sdf_inv_voxel = static_cast<R>(1.0 / oh.sdf_voxel);
+        ok[o].sdf = ctx->sdf_dev[o].as<float>();
+    }
+    objs.reserve(ok.size() * sizeof(ObjK<R>));
+    CK(cudaMemcpyAsync(objs.p, ok.data(), ok.size() * sizeof(ObjK<R>), cudaMemcpyHostToDevice, ctx->stream));
+    sc.nodes = nodes.p;
+    sc.tris = tris.p;
+    sc.objs = objs.as<ObjK<R>>();
+    sc.n_objects = static_cast<uint32_t>(ok.size());
+    // Camera basis in double (DESIGN.md camera model), then rounded.
+    auto v = [](const double* p) { return std::array<double, 3>{p[0], p[1], p[2]}; };
+    auto sub = [](std::array<double, 3> a, std::array<double, 3> b) {
+        return std::array<double, 3>{a[0] - b[0], a[1] - b[1], a[2] - b[2]};
+    };
+    auto cross = [](std::array<double, 3> a, std::array<double, 3> b) {
+        return std::array<double, 3>{a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    };
+    auto norm = [](std::array<double, 3> a) {
+        const double l = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+        return std::array<double, 3>{a[0] / l, a[1] / l, a[2] / l};
+    };
+    const auto fwd = norm(sub(v(d.cam_look_at), v(d.cam_position)));
+    const auto right = norm(cross(fwd, v(d.cam_up)));
+    const auto up = cross(right, fwd);
+    auto tor = [](std::array<double, 3> a) { return mk<R>(R(a[0]), R(a[1]), R(a[2])); };
+    sc.cam_pos = tor(v(d.cam_position));
+    sc.cam_fwd = tor(fwd);
+    sc.cam_right = tor(right);
+    sc.cam_up = tor(up);
+    sc.tan_half = static_cast<R>(std::tan(d.cam_vfov_deg * 3.14159265358979323846 / 360.0));
+    sc.aspect = static_cast<R>(static_cast<double>(d.width) / static_cast<double>(d.height));
+    sc.width = d.width;
+    sc.height = d.height;
+    sc.light = tor(v(d.light_position));
+    for (int c = 0; c < 3; ++c) {
+        sc.power[c] = static_cast<R>(d.light_power[c]);
+        sc.bg[c] = static_cast<R>(d.background[c]);
+    }
+    // Surface self-intersection guard for FP32 (relative to the scene extent).
+    double ext = 1.0;
+    for (const auto& oh : ctx->objects)
+        for (int a = 0; a < 3; ++a) ext = std::fmax(ext, std::fabs(oh.sdf_origin[a]) + oh.dims[a] * oh.sdf_voxel);
+    sc.t_min = static_cast<R>(1e-9);
+    sc.surf_eps = std::is_same<R, double>::value ? static_cast<R>(1e-9) : static_cast<R>(2e-6 * ext);
+    sc.cap_pt = d.max_pt_events ? d.max_pt_events : 1000000u;
+    sc.cap_st = d.max_st_steps ? d.max_st_steps : 100000u;
+}
+
+void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
+    if (!d || d->n_objects == 0 || !d->objects) throw InvalidArgument("scene has no objects");
+    if (d->width == 0 || d->height == 0) throw InvalidArgument("camera resolution must be >= 1x1");
+    if (!(d->cam_vfov_deg > 0.0 && d->cam_vfov_deg < 180.0)) throw InvalidArgument("camera fov out of range");
+    std::vector<ObjectHost> objs(d->n_objects);
+    std::vector<std::array<std::array<double, 3>, 3>> tv;
+    std::vector<uint32_t> tobj;
+    for (uint32_t o = 0; o < d->n_objects; ++o) {
+        const sst_object_desc& od = d->objects[o];
+        if (!od.positions || !od.triangles || od.n_triangles == 0) throw InvalidArgument("object has no geometry");
+        for (int c = 0; c < 3; ++c) {
+            validate_medium(od.media[c]);
+            objs[o].media[c] = od.media[c];
+        }
+        std::vector<std::array<uint32_t, 3>> tri(od.n_triangles);
+        for (uint32_t t = 0; t < od.n_triangles; ++t)
+            for (int c = 0; c < 3; ++c) {
+                const uint32_t vi = od.triangles[3 * t + c];
+                if (vi >= od.n_vertices) throw InvalidArgument("triangle index out of range");
+                tri[t][c] = vi;
+            }
+        // Orientation: the order-free optical depth needs outward winding; flip an
+        // inward-wound (negative signed volume) mesh.
+        double vol = 0.0;
+        for (const auto& t : tri) {
+            const double* a = od.positions + 3 * t[0];
+            const double* b = od.positions + 3 * t[1];
+            const double* c = od.positions + 3 * t[2];
+            vol += a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) +
+                   a[2] * (b[0] * c[1] - b[1] * c[0]);
+        }
+        const bool flip = vol < 0.0;
+        for (const auto& t : tri) {
+            std::array<std::array<double, 3>, 3> corners;
+            for (int c = 0; c < 3; ++c)
+                for (int k = 0; k < 3; ++k) corners[c][k] = od.positions[3 * t[c] + k];
+            if (flip) std::swap(corners[1], corners[2]);
+            tv.push_back(corners);
+            tobj.push_back(o);
+        }
+        if (od.sdf_values) {
+            if (!(od.sdf_voxel > 0.0) || !od.sdf_dims[0] || !od.sdf_dims[1] || !od.sdf_dims[2])
+                throw InvalidArgument("SDF grid has empty dims or voxel size");
+            const size_t n = static_cast<size_t>(od.sdf_dims[0]) * od.sdf_dims[1] * od.sdf_dims[2];
+            objs[o].sdf.assign(od.sdf_values, od.sdf_values + n);
+            for (int a = 0; a < 3; ++a) {
+                objs[o].sdf_origin[a] = od.sdf_origin[a];
+                objs[o].dims[a] = od.sdf_dims[a];
+            }
+            objs[o].sdf_voxel = od.sdf_voxel;
+        } else {
+            build_sdf_gpu(ctx, od, objs[o], is_watertight(tri));
+        }
+    }
+    const FlatBvh bvh = build_bvh(tv, tobj);
+    // upload
+    ctx->objects = std::move(objs);
+    ctx->desc = *d;
+    ctx->desc.objects = nullptr;
+    auto up = [&](DevBuf& b, const std::vector<uint8_t>& src) {
+        b.reserve(src.size());
+        CK(cudaMemcpyAsync(b.p, src.data(), src.size(), cudaMemcpyHostToDevice, ctx->stream));
+    };
+    up(ctx->nodes32, bvh.nodes_f32);
+    up(ctx->tris32, bvh.tris_f32);
+    up(ctx->nodes64, bvh.nodes_f64);
+    up(ctx->tris64, bvh.tris_f64);
+    for (auto& b : ctx->sdf_dev) b.release();
+    ctx->sdf_dev.assign(ctx->objects.size(), DevBuf{});
+    for (size_t o = 0; o < ctx->objects.size(); ++o) {
+        const auto& s = ctx->objects[o].sdf;
+        ctx->sdf_dev[o].reserve(s.size() * sizeof(float));
+        CK(cudaMemcpyAsync(ctx->sdf_dev[o].p, s.data(), s.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
+    fill_devscene<double>(ctx, ctx->sc64, ctx->nodes64, ctx->tris64, ctx->objs64);
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->scene = true;
+}
+
+template <class R>
+const DevScene<R>& scene_of(const sst_gpu_ctx* ctx) {
+    if constexpr (std::is_same<R, float>::value) return ctx->sc32;
+    else return ctx->sc64;
+}
+
+constexpr uint64_t kChunkPaths = 1ull << 24;  // radiance scratch per launch
+
+template <class R>
+void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_keys, int nee,
+               uint64_t seed, uint64_t n_paths, uint32_t n_pix, uint32_t sample_begin,
+               const uint32_t* pix, const uint32_t* smp, const uint8_t* ch, R* radiance,
+               uint32_t* segments) {
+    TraceArgs<R> a{};
+    a.sc = sc;
+    a.nee = nee;
+    a.seed = seed;
+    a.n_paths = n_paths;
+    a.n_pix = n_pix;
+    a.sample_begin = sample_begin;
+    a.pixel = pix;
+    a.sample = smp;
+    a.channel = ch;
+    a.radiance = radiance;
+    a.segments = segments;
+    a.work = ctx->work.as<unsigned long long>();
+    a.stats = ctx->stats.as<unsigned long long>();
+    CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), ctx->stream));
+    if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, ctx->stream));
+    else CK(f64::launch_trace(a, st, explicit_keys, ctx->stream));
+}
+
+void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
+    unsigned long long v[kStCount];
+    CK(cudaMemcpyAsync(v, ctx->stats.p, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (v[kStErrors]) {
+        // the reference throws std::runtime_error (scatter.cpp:56)
+        if (out) {
+            out->errors += v[kStErrors];
+        }
+        throw RuntimeError("decoder produced non-finite output twice (" + std::to_string(v[kStErrors]) + " paths)");
+    }
+    if (!out) return;
+    out->paths += v[kStPaths];
+    out->segments += v[kStSphere] + v[kStEvents];
+    out->sphere_steps += v[kStSphere];
+    out->pt_events += v[kStEvents];
+    out->decodes_length += v[kStDecL];
+    out->decodes_path += v[kStDecP];
+    out->decodes_event += v[kStDecE];
+    out->absorbed += v[kStAbsorbed];
+    out->escaped += v[kStEscaped];
+    out->capped += v[kStCapped];
+    out->shadow_rays += v[kStShadow];
+}
+
+void check_render_ready(sst_gpu_ctx* ctx, int integrator) {
+    if (!ctx->scene) throw InvalidArgument("no scene uploaded (sst_gpu_upload_scene)");
+    if (integrator != SST_INTEGRATOR_PT && integrator != SST_INTEGRATOR_ST) throw InvalidArgument("unknown integrator");
+    if (integrator == SST_INTEGRATOR_ST) ensure_constants(ctx);
+}
+
+template <class R>
+void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, uint32_t s0, uint32_t s1,
+                 uint64_t seed, double* film_sum, double* film_sq, int ptr_kind, sst_path_stats* stats) {
+    const DevScene<R>& sc = scene_of<R>(ctx);
+    const uint32_t n_pix = ctx->desc.width * ctx->desc.height;
+    const uint64_t per_sample = 3ull * n_pix;
+    const uint32_t n_samples = s1 - s0;
+    uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, kChunkPaths / per_sample));
+    if (chunk > n_samples) chunk = n_samples;
+    ctx->radiance.reserve(per_sample * chunk * sizeof(R));
+    ctx->stats.reserve(kStCount * sizeof(unsigned long long));
+    ctx->work.reserve(sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+    double* dsum = film_sum;
+    double* dsq = film_sq;
+    if (ptr_kind == SST_PTR_HOST) {
+        ctx->film_sum.reserve(per_sample * sizeof(double));
+        ctx->film_sq.reserve(per_sample * sizeof(double));
+        dsum = ctx->film_sum.as<double>();
+        dsq = ctx->film_sq.as<double>();
+        CK(cudaMemsetAsync(dsum, 0, per_sample * sizeof(double), ctx->stream));
+        CK(cudaMemsetAsync(dsq, 0, per_sample * sizeof(double), ctx->stream));
+    }
+    if (!ctx->ev0) {
+        CK(cudaEventCreate(&ctx->ev0));
+        CK(cudaEventCreate(&ctx->ev1));
+    }
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    for (uint32_t s = s0; s < s1; s += chunk) {
+        const uint32_t ns = std::min(chunk, s1 - s);
+        run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, false, nee, seed, per_sample * ns, n_pix, s,
+                     nullptr, nullptr, nullptr, ctx->radiance.as<R>(), nullptr);
+        if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(ctx->radiance.as<R>(), per_sample, ns, dsum, dsq, ctx->stream));
+        else CK(f64::launch_film(ctx->radiance.as<R>(), per_sample, ns, dsum, dsq, ctx->stream));
+    }
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    if (ptr_kind == SST_PTR_HOST) {
+        std::vector<double> hs(per_sample), hq(per_sample);
+        CK(cudaMemcpyAsync(hs.data(), dsum, per_sample * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(hq.data(), dsq, per_sample * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (uint64_t i = 0; i < per_sample; ++i) {
+            film_sum[i] += hs[i];
+            film_sq[i] += hq[i];
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (stats) stats->device_ms += ms;
+    read_stats(ctx, stats);
+}
+
+template <class R>
+void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
+                      const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                      double* radiance, uint32_t* segments, sst_path_stats* stats) {
+    const DevScene<R>& sc = scene_of<R>(ctx);
+    const uint32_t n_pix = ctx->desc.width * ctx->desc.height;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (pixel[i] >= n_pix) throw InvalidArgument("pixel index out of range");
+        if (channel[i] > 2) throw InvalidArgument("channel must be 0, 1 or 2");
+    }
+    ctx->keys_pix.reserve(n * 4);
+    ctx->keys_smp.reserve(n * 4);
+    ctx->keys_ch.reserve(n);
+    ctx->radiance.reserve(n * sizeof(R));
+    ctx->segments.reserve(n * 4);
+    ctx->stats.reserve(kStCount * sizeof(unsigned long long));
+    ctx->work.reserve(sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+    CK(cudaMemcpyAsync(ctx->keys_pix.p, pixel, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->keys_smp.p, sample, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->keys_ch.p, channel, n, cudaMemcpyHostToDevice, ctx->stream));
+    run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, true, nee, seed, n, n_pix, 0,
+                 ctx->keys_pix.as<uint32_t>(), ctx->keys_smp.as<uint32_t>(), ctx->keys_ch.as<uint8_t>(),
+                 ctx->radiance.as<R>(), ctx->segments.as<uint32_t>());
+    std::vector<R> rad(n);
+    CK(cudaMemcpyAsync(rad.data(), ctx->radiance.p, n * sizeof(R), cudaMemcpyDeviceToHost, ctx->stream));
+    if (segments) CK(cudaMemcpyAsync(segments, ctx->segments.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint64_t i = 0; i < n; ++i) radiance[i] = static_cast<double>(rad[i]);
+    read_stats(ctx, stats);
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+extern "C" {
+
+int sst_gpu_abi_version(void) { return SST_GPU_ABI_VERSION; }
+
+const char* sst_gpu_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t sst_rng_init(uint64_t seed, uint64_t s1, uint64_t s2, uint64_t s3) {
+    return rng_key(seed, s1, s2, s3);
+}
+
+int sst_gpu_create(int device, sst_gpu_ctx** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArgument("null output pointer");
+        *out = nullptr;
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0)
+            throw CudaFailure(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                              "); this library has no CPU fallback");
+        if (device < 0 || device >= n) throw InvalidArgument("device ordinal out of range");
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw CudaFailure(std::string("device ") + prop.name + " is not sm_100 (B200); kernels are built for sm_100a only");
+        auto ctx = std::make_unique<sst_gpu_ctx>();
+        ctx->device = device;
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->serial = ++g_serial;
+        *out = ctx.release();
+    });
+}
+
+void sst_gpu_destroy(sst_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    {
+        std::lock_guard<std::mutex> lk(g_const_mu);
+        auto it = g_const_owner.find(ctx->device);
+        if (it != g_const_owner.end() && it->second.first == ctx) g_const_owner.erase(it);
+    }
+    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64,
+                      &ctx->radiance, &ctx->segments, &ctx->work, &ctx->stats, &ctx->error, &ctx->film_sum,
+                      &ctx->film_sq, &ctx->keys_pix, &ctx->keys_smp, &ctx->keys_ch, &ctx->step_in, &ctx->step_out})
+        b->release();
+    for (auto& b : ctx->sdf_dev) b.release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int sst_gpu_set_precision(sst_gpu_ctx* ctx, int precision) {
+    return guarded([&] {
+        if (!ctx) throw InvalidArgument("null context");
+        if (precision != SST_PREC_F32 && precision != SST_PREC_F64) throw InvalidArgument("precision must be SST_PREC_F32 or SST_PREC_F64");
+        ctx->precision = precision;
+    });
+}
+
+int sst_gpu_get_device(const sst_gpu_ctx* ctx) { return ctx ? ctx->device : -1; }
+
+void* sst_gpu_stream(sst_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int sst_gpu_synchronize(sst_gpu_ctx* ctx) {
+    return guarded([&] {
+        require_device(ctx);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sst_gpu_upload_models(sst_gpu_ctx* ctx, const sst_model_desc models[3]) {
+    return guarded([&] {
+        require_device(ctx);
+        if (!models) throw InvalidArgument("null model descriptors");
+        HostModel m[3];
+        for (int k = 0; k < 3; ++k) {
+            const sst_model_desc& d = models[k];
+            m[k].kind = d.kind;
+            m[k].p_in = d.p_in;
+            m[k].p_out = d.p_out;
+            m[k].depth = d.depth;
+            m[k].width = d.width;
+            m[k].latent = d.latent;
+            m[k].sigma_ref = d.sigma_ref;
+            m[k].n_ref = d.n_ref;
+            if (!d.layers || d.n_layers == 0) throw InvalidArgument("model has no layers");
+            for (uint32_t i = 0; i < d.n_layers; ++i) {
+                const sst_layer_desc& l = d.layers[i];
+                if (!l.weights || !l.bias || !l.out_dim || !l.in_dim) throw InvalidArgument("empty layer");
+                HostLayer hl;
+                hl.out_dim = l.out_dim;
+                hl.in_dim = l.in_dim;
+                hl.w.assign(l.weights, l.weights + static_cast<size_t>(l.out_dim) * l.in_dim);
+                hl.b.assign(l.bias, l.bias + l.out_dim);
+                m[k].layers.push_back(std::move(hl));
+            }
+        }
+        set_models(ctx, m);
+        ensure_constants(ctx);
+    });
+}
+
+int sst_gpu_load_models_dir(sst_gpu_ctx* ctx, const char* dir) {
+    return guarded([&] {
+        require_device(ctx);
+        if (!dir) throw InvalidArgument("null directory");
+        const std::string d(dir);
+        HostModel m[3] = {load_ssnn(d + "/lengthgen.ssnn"), load_ssnn(d + "/pathgen.ssnn"),
+                          load_ssnn(d + "/eventgen.ssnn")};
+        set_models(ctx, m);
+        ensure_constants(ctx);
+    });
+}
+
+int sst_gpu_sphere_step_batch(sst_gpu_ctx* ctx, uint64_t n, const sst_step_in* in, int with_event_default,
+                              sst_step_out* out, int ptr_kind, sst_decode_counters* counters) {
+    return guarded([&] {
+        require_device(ctx);
+        if (!in || !out) throw InvalidArgument("null batch descriptors");
+        if (ptr_kind != SST_PTR_HOST && ptr_kind != SST_PTR_DEVICE) throw InvalidArgument("bad ptr_kind");
+        ensure_constants(ctx);
+        if (n == 0) return;
+        if (ptr_kind == SST_PTR_HOST) {
+            for (uint64_t i = 0; i < n; ++i) {
+                if (!(in->sigma_t[i] >= 0.0 && in->r_sphere[i] >= 0.0)) throw DomainError("rescale_sigma: negative input");
+                if (!(in->r_sphere[i] > 0.0)) throw DomainError("to_world: r_sphere must be > 0");
+            }
+        }
+        ctx->error.reserve(sizeof(int) + 3 * sizeof(unsigned long long));
+        int* derr = ctx->error.as<int>();
+        unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(ctx->error.as<char>() + 8);
+        CK(cudaMemsetAsync(ctx->error.p, 0, 8 + 3 * sizeof(unsigned long long), ctx->stream));
+        StepBatchArgs a{};
+        a.n = n;
+        a.with_event_default = with_event_default;
+        a.error = derr;
+        a.counters = dcnt;
+        if (ptr_kind == SST_PTR_DEVICE) {
+            a.sigma_t = in->sigma_t; a.g = in->g; a.phi = in->phi; a.w_in = in->w_in; a.center = in->center;
+            a.r = in->r_sphere; a.with_event = in->with_event; a.rng_state = in->rng_state;
+            a.absorbed = out->absorbed; a.n_events = out->n_events; a.exit_pos = out->exit_position;
+            a.exit_dir = out->exit_direction; a.has_rep = out->has_representative; a.rep_pos = out->rep_position;
+            a.rep_dir = out->rep_direction; a.lambda = out->lambda_weight;
+            CK(ctx->precision == SST_PREC_F64 ? f64::launch_step_batch(a, ctx->stream)
+                                              : f32::launch_step_batch(a, ctx->stream));
+        } else {
+            // staging: inputs 8+8+8+24+24+8+1+8 B, outputs 1+4+4*24+1+8 B per step, 16-B aligned segments
+            const size_t in_b = n * 89 + 8 * 16, out_b = n * 110 + 8 * 16;
+            ctx->step_in.reserve(in_b);
+            ctx->step_out.reserve(out_b);
+            char* pi = ctx->step_in.as<char>();
+            char* po = ctx->step_out.as<char>();
+            auto h2d = [&](const void* src, size_t bytes) {
+                char* dst = pi;
+                CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+                pi += (bytes + 15) / 16 * 16;
+                return dst;
+            };
+            auto dal = [&](size_t bytes) {
+                char* dst = po;
+                po += (bytes + 15) / 16 * 16;
+                return dst;
+            };
+            a.sigma_t = reinterpret_cast<const double*>(h2d(in->sigma_t, 8 * n));
+            a.g = reinterpret_cast<const double*>(h2d(in->g, 8 * n));
+            a.phi = reinterpret_cast<const double*>(h2d(in->phi, 8 * n));
+            a.w_in = reinterpret_cast<const double*>(h2d(in->w_in, 24 * n));
+            a.center = reinterpret_cast<const double*>(h2d(in->center, 24 * n));
+            a.r = reinterpret_cast<const double*>(h2d(in->r_sphere, 8 * n));
+            a.with_event = in->with_event ? reinterpret_cast<const uint8_t*>(h2d(in->with_event, n)) : nullptr;
+            a.rng_state = reinterpret_cast<uint64_t*>(h2d(in->rng_state, 8 * n));
+            a.absorbed = reinterpret_cast<uint8_t*>(dal(n));
+            a.n_events = reinterpret_cast<uint32_t*>(dal(4 * n));
+            a.exit_pos = reinterpret_cast<double*>(dal(24 * n));
+            a.exit_dir = reinterpret_cast<double*>(dal(24 * n));
+            a.has_rep = reinterpret_cast<uint8_t*>(dal(n));
+            a.rep_pos = reinterpret_cast<double*>(dal(24 * n));
+            a.rep_dir = reinterpret_cast<double*>(dal(24 * n));
+            a.lambda = reinterpret_cast<double*>(dal(8 * n));
+            CK(ctx->precision == SST_PREC_F64 ? f64::launch_step_batch(a, ctx->stream) : f32::launch_step_batch(a, ctx->stream));
+            auto d2h = [&](void* dst, const void* src, size_t bytes) {
+                CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            };
+            d2h(in->rng_state, a.rng_state, 8 * n);
+            d2h(out->absorbed, a.absorbed, n);
+            d2h(out->n_events, a.n_events, 4 * n);
+            d2h(out->exit_position, a.exit_pos, 24 * n);
+            d2h(out->exit_direction, a.exit_dir, 24 * n);
+            d2h(out->has_representative, a.has_rep, n);
+            d2h(out->rep_position, a.rep_pos, 24 * n);
+            d2h(out->rep_direction, a.rep_dir, 24 * n);
+            d2h(out->lambda_weight, a.lambda, 8 * n);
+        }
+        int herr = 0;
+        unsigned long long hc[3];
+        CK(cudaMemcpyAsync(&herr, derr, sizeof herr, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(hc, dcnt, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (counters) {
+            counters->length += hc[0];
+            counters->path += hc[1];
+            counters->event += hc[2];
+        }
+        if (herr) throw RuntimeError("decoder produced non-finite output twice");
+    });
+}
+
+int sst_gpu_upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* scene) {
+    return guarded([&] {
+        require_device(ctx);
+        upload_scene(ctx, scene);
+    });
+}
+
+int sst_gpu_get_sdf(sst_gpu_ctx* ctx, uint32_t obj, double origin[3], double* voxel, uint32_t dims[3],
+                    float* values) {
+    return guarded([&] {
+        if (!ctx || !ctx->scene) throw InvalidArgument("no scene uploaded");
+        if (obj >= ctx->objects.size()) throw InvalidArgument("object index out of range");
+        const ObjectHost& o = ctx->objects[obj];
+        for (int a = 0; a < 3; ++a) {
+            if (origin) origin[a] = o.sdf_origin[a];
+            if (dims) dims[a] = o.dims[a];
+        }
+        if (voxel) *voxel = o.sdf_voxel;
+        if (values) std::memcpy(values, o.sdf.data(), o.sdf.size() * sizeof(float));
+    });
+}
+
+int sst_gpu_render(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, uint32_t sample_begin,
+                   uint32_t sample_end, uint64_t seed, double* film_sum, double* film_sumsq, int ptr_kind,
+                   sst_path_stats* stats) {
+    return guarded([&] {
+        require_device(ctx);
+        check_render_ready(ctx, integrator);
+        if (spp_total == 0) throw InvalidArgument("spp must be >= 1");
+        if (sample_begin >= sample_end || sample_end > spp_total) throw InvalidArgument("bad sample range");
+        if (!film_sum || !film_sumsq) throw InvalidArgument("null film buffers");
+        if (ptr_kind != SST_PTR_HOST && ptr_kind != SST_PTR_DEVICE) throw InvalidArgument("bad ptr_kind");
+        if (ctx->precision == SST_PREC_F64)
+            render_impl<double>(ctx, integrator, nee, spp_total, sample_begin, sample_end, seed, film_sum,
+                                film_sumsq, ptr_kind, stats);
+        else
+            render_impl<float>(ctx, integrator, nee, spp_total, sample_begin, sample_end, seed, film_sum,
+                               film_sumsq, ptr_kind, stats);
+    });
+}
+
+int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
+                        const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel, double* radiance,
+                        uint32_t* segments, sst_path_stats* stats) {
+    return guarded([&] {
+        require_device(ctx);
+        check_render_ready(ctx, integrator);
+        if (n == 0) return;
+        if (!pixel || !sample || !channel || !radiance) throw InvalidArgument("null path key buffers");
+        if (ctx->precision == SST_PREC_F64)
+            trace_paths_impl<double>(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments, stats);
+        else
+            trace_paths_impl<float>(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments, stats);
+    });
+}
+
+// ---------------------------------------------------------------- host utilities
+namespace {
+void export_mesh(const HostMesh& m, double** pos, uint32_t* nv, uint32_t** tris, uint32_t* nt) {
+    if (!pos || !nv || !tris || !nt) throw InvalidArgument("null output pointer");
+    *pos = static_cast<double*>(std::malloc(m.pos.size() * 3 * sizeof(double)));
+    *tris = static_cast<uint32_t*>(std::malloc(m.tri.size() * 3 * sizeof(uint32_t)));
+    if (!*pos || !*tris) throw std::bad_alloc();
+    for (size_t i = 0; i < m.pos.size(); ++i)
+        for (int a = 0; a < 3; ++a) (*pos)[3 * i + a] = m.pos[i][a];
+    for (size_t i = 0; i < m.tri.size(); ++i)
+        for (int a = 0; a < 3; ++a) (*tris)[3 * i + a] = m.tri[i][a];
+    *nv = static_cast<uint32_t>(m.pos.size());
+    *nt = static_cast<uint32_t>(m.tri.size());
+}
+}  // namespace
+
+int sst_mesh_icosphere(int subdivisions, double radius, double** positions, uint32_t* n_vertices,
+                       uint32_t** triangles, uint32_t* n_triangles) {
+    return guarded([&] { export_mesh(make_icosphere(subdivisions, radius), positions, n_vertices, triangles, n_triangles); });
+}
+
+int sst_mesh_bumpy_sphere(int subdivisions, double radius, double amplitude, double frequency, double** positions,
+                          uint32_t* n_vertices, uint32_t** triangles, uint32_t* n_triangles) {
+    return guarded([&] {
+        export_mesh(make_bumpy_sphere(subdivisions, radius, amplitude, frequency), positions, n_vertices, triangles,
+                    n_triangles);
+    });
+}
+
+int sst_mesh_load_obj(const char* path, double scale, double** positions, uint32_t* n_vertices,
+                      uint32_t** triangles, uint32_t* n_triangles, uint64_t* dropped) {
+    return guarded([&] {
+        if (!path) throw InvalidArgument("null path");
+        const HostMesh m = load_obj(path, scale);
+        export_mesh(m, positions, n_vertices, triangles, n_triangles);
+        if (dropped) *dropped = m.dropped;
+    });
+}
+
+void sst_mesh_free(double* positions, uint32_t* triangles) {
+    std::free(positions);
+    std::free(triangles);
+}
+
+int sst_sdf_save(const char* path, const double origin[3], double voxel, const uint32_t dims[3], const float* values,
+                 uint64_t fp) {
+    return guarded([&] {
+        if (!path || !origin || !dims || !values) throw InvalidArgument("null argument");
+        std::ofstream f(path, std::ios::binary | std::ios::trunc);
+        if (!f) throw RuntimeError(std::string("cannot open for writing: ") + path);
+        auto put = [&](const void* p, size_t n) { f.write(static_cast<const char*>(p), static_cast<std::streamsize>(n)); };
+        const uint32_t version = 1;
+        put("SSDF", 4);
+        put(&version, 4);
+        put(&fp, 8);
+        put(dims, 12);
+        const float o[4] = {static_cast<float>(origin[0]), static_cast<float>(origin[1]), static_cast<float>(origin[2]),
+                            static_cast<float>(voxel)};
+        put(o, 16);
+        put(values, static_cast<size_t>(dims[0]) * dims[1] * dims[2] * sizeof(float));
+        f.close();
+        if (!f) throw RuntimeError("write failure on close");
+    });
+}
+
+int sst_sdf_load(const char* path, double origin[3], double* voxel, uint32_t dims[3], float** values, uint64_t* fp) {
+    return guarded([&] {
+        if (!path || !origin || !voxel || !dims || !values) throw InvalidArgument("null argument");
+        std::ifstream f(path, std::ios::binary);
+        if (!f) throw RuntimeError(std::string("cannot open for reading: ") + path);
+        const std::string what = std::string("sdf ") + path;
+        char magic[4];
+        f.read(magic, 4);
+        if (!f || std::memcmp(magic, "SSDF", 4) != 0) throw RuntimeError(what + ": bad magic bytes");
+        uint32_t version = 0;
+        f.read(reinterpret_cast<char*>(&version), 4);
+        if (version != 1) throw RuntimeError(what + ": unsupported version");
+        uint64_t fpv = 0;
+        f.read(reinterpret_cast<char*>(&fpv), 8);
+        f.read(reinterpret_cast<char*>(dims), 12);
+        float o[4];
+        f.read(reinterpret_cast<char*>(o), 16);
+        const size_t n = static_cast<size_t>(dims[0]) * dims[1] * dims[2];
+        if (!f || n == 0 || n > (1ull << 32)) throw RuntimeError(what + ": implausible dims");
+        float* v = static_cast<float*>(std::malloc(n * sizeof(float)));
+        if (!v) throw std::bad_alloc();
+        f.read(reinterpret_cast<char*>(v), static_cast<std::streamsize>(n * sizeof(float)));
+        if (!f) {
+            std::free(v);
+            throw RuntimeError(what + ": truncated or corrupt file");
+        }
+        for (int a = 0; a < 3; ++a) origin[a] = o[a];
+        *voxel = o[3];
+        *values = v;
+        if (fp) *fp = fpv;
+    });
+}
+
+void sst_sdf_free(float* values) { std::free(values); }
+
+int sst_image_save_pfm(const char* path, uint32_t w, uint32_t h, const float* rgb) {
+    return guarded([&] {
+        if (!path || !rgb) throw InvalidArgument("null argument");
+        std::ofstream out(path, std::ios::binary | std::ios::trunc);
+        if (!out) throw RuntimeError(std::string("cannot open for writing: ") + path);
+        out << "PF\n" << w << " " << h << "\n-1.0\n";
+        for (uint32_t y = h; y-- > 0;)
+            out.write(reinterpret_cast<const char*>(rgb + static_cast<size_t>(y) * w * 3),
+                      static_cast<std::streamsize>(w) * 3 * sizeof(float));
+        if (!out) throw RuntimeError(std::string("write failure: ") + path);
+    });
+}
+
+}  // extern "C"

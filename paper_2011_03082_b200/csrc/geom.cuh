@@ -1,0 +1,270 @@
+// geom.cuh -- software ray traversal (B200 has no RT cores) and the SDF lookup.
+//
+//   BVH2 with both child boxes stored in the parent (64 B FP32 node = 4 x LDG.128),
+//   near-child-first traversal, per-ray inverse direction.
+//   Triangle test: Moller-Trumbore with the operation order of bvh.cpp:11-27.
+//   intersect_nearest  ~ Bvh::intersect      (bvh.cpp:115-148)
+//   optical_depth      ~ Bvh::intersect_all + in-medium toggling (bvh.cpp:150-179,
+//                        SPEC.md:597), restated order-free: for closed outward-oriented
+//                        meshes the in-medium length of object j on [0, d] from a
+//                        start inside j is sum_hits(j) sign * t with sign = +1 when the
+//                        ray leaves (det < 0 in Moller-Trumbore) and -1 when it enters.
+//                        No hit list, no sort.
+//   sdf_radius         ~ query_safe_radius   (sdf.cpp:60-69)
+#pragma once
+
+#include "common.cuh"
+#include "step.cuh"
+#include "types.cuh"
+
+namespace sstg {
+
+
+// --------------------------------------------------------------- SDF lookup
+template <class R>
+SST_D R sdf_raw(const ObjK<R>& o, V3<R> p, bool* inside_grid) {
+    R rx, ry, rz;
+    if (Real<R>::kIsDouble) {  // (point - origin) / voxel_size, sdf.cpp:61
+        rx = (p.x - o.sdf_origin[0]) / o.sdf_voxel;
+        ry = (p.y - o.sdf_origin[1]) / o.sdf_voxel;
+        rz = (p.z - o.sdf_origin[2]) / o.sdf_voxel;
+    } else {
+        rx = (p.x - o.sdf_origin[0]) * o.sdf_inv_voxel;
+        ry = (p.y - o.sdf_origin[1]) * o.sdf_inv_voxel;
+        rz = (p.z - o.sdf_origin[2]) * o.sdf_inv_voxel;
+    }
+    *inside_grid = false;
+    if (rx < R(0) || ry < R(0) || rz < R(0)) return R(0);
+    const uint32_t x = static_cast<uint32_t>(rx), y = static_cast<uint32_t>(ry),
+                   z = static_cast<uint32_t>(rz);
+    if (x >= o.dims[0] || y >= o.dims[1] || z >= o.dims[2]) return R(0);
+    *inside_grid = true;
+    return static_cast<R>(__ldg(o.sdf + (static_cast<size_t>(z) * o.dims[1] + y) * o.dims[0] + x));
+}
+
+// query_safe_radius: -v inside (v < 0), else 0; 0 outside the grid.
+template <class R>
+SST_D R sdf_radius(const ObjK<R>& o, V3<R> p) {
+    bool in;
+    const R v = sdf_raw(o, p, &in);
+    return v < R(0) ? -v : R(0);
+}
+
+// --------------------------------------------------------------- ray setup
+template <class R>
+struct RayK {
+    V3<R> o, d, inv;
+};
+
+template <class R>
+SST_D RayK<R> make_ray(V3<R> o, V3<R> d) {
+    RayK<R> r;
+    r.o = o;
+    r.d = d;
+    if (Real<R>::kIsDouble) {  // bvh.cpp:91 computes 1/dir per axis (inf allowed)
+        r.inv = mk<R>(R(1) / d.x, R(1) / d.y, R(1) / d.z);
+    } else {
+        const float e = 1e-20f;
+        r.inv = mk<R>(1.0f / (fabsf(d.x) > e ? d.x : copysignf(e, d.x)),
+                      1.0f / (fabsf(d.y) > e ? d.y : copysignf(e, d.y)),
+                      1.0f / (fabsf(d.z) > e ? d.z : copysignf(e, d.z)));
+    }
+    return r;
+}
+
+// slab_hit (bvh.cpp:88-101) returning the entry distance.
+template <class R>
+SST_D bool slab(const RayK<R>& r, R lox, R hix, R loy, R hiy, R loz, R hiz, R t_min, R t_max,
+                R* t_enter) {
+    R t0 = t_min, t1 = t_max;
+    R n = (lox - r.o.x) * r.inv.x, f = (hix - r.o.x) * r.inv.x;
+    if (n > f) { const R t = n; n = f; f = t; }
+    t0 = Real<R>::fmax_(t0, n);
+    t1 = Real<R>::fmin_(t1, f);
+    n = (loy - r.o.y) * r.inv.y;
+    f = (hiy - r.o.y) * r.inv.y;
+    if (n > f) { const R t = n; n = f; f = t; }
+    t0 = Real<R>::fmax_(t0, n);
+    t1 = Real<R>::fmin_(t1, f);
+    n = (loz - r.o.z) * r.inv.z;
+    f = (hiz - r.o.z) * r.inv.z;
+    if (n > f) { const R t = n; n = f; f = t; }
+    t0 = Real<R>::fmax_(t0, n);
+    t1 = Real<R>::fmin_(t1, f);
+    *t_enter = t0;
+    return t0 <= t1;
+}
+
+// Moller-Trumbore (bvh.cpp:11-27). Returns t (> t_min, < t_max) or a negative
+// value on a miss; *det_out receives det (sign = crossing direction).
+template <class R>
+SST_D R ray_tri(const RayK<R>& r, V3<R> v0, V3<R> e1, V3<R> e2, R t_min, R t_max, R* det_out) {
+    const V3<R> pvec = cross(r.d, e2);
+    const R det = dot(e1, pvec);
+    *det_out = det;
+    if (Real<R>::fabs_(det) < R(1e-14)) return R(-1);
+    const R inv_det = R(1) / det;
+    const V3<R> tvec = r.o - v0;
+    const R u = dot(tvec, pvec) * inv_det;
+    if (u < R(0) || u > R(1)) return R(-1);
+    const V3<R> qvec = cross(tvec, e1);
+    const R v = dot(r.d, qvec) * inv_det;
+    if (v < R(0) || u + v > R(1)) return R(-1);
+    const R t = dot(e2, qvec) * inv_det;
+    if (t <= t_min || t >= t_max) return R(-1);
+    return t;
+}
+
+template <class R>
+SST_D void load_node(const void* nodes, int i, R (&b)[12], int& c0, int& c1);
+template <>
+SST_D void load_node<float>(const void* nodes, int i, float (&b)[12], int& c0, int& c1) {
+    const NodeF* n = static_cast<const NodeF*>(nodes) + i;
+    const float4 a = __ldg(&n->a), bb = __ldg(&n->b), c = __ldg(&n->c);
+    const int4 d = __ldg(&n->d);
+    // b = lo0x hi0x lo0y hi0y lo0z hi0z | lo1x hi1x lo1y hi1y lo1z hi1z
+    b[0] = a.x; b[1] = a.y; b[2] = a.z; b[3] = a.w; b[4] = c.x; b[5] = c.y;
+    b[6] = bb.x; b[7] = bb.y; b[8] = bb.z; b[9] = bb.w; b[10] = c.z; b[11] = c.w;
+    c0 = d.x;
+    c1 = d.y;
+}
+template <>
+SST_D void load_node<double>(const void* nodes, int i, double (&b)[12], int& c0, int& c1) {
+    const NodeD* n = static_cast<const NodeD*>(nodes) + i;
+    b[0] = n->lo0[0]; b[1] = n->hi0[0]; b[2] = n->lo0[1]; b[3] = n->hi0[1]; b[4] = n->lo0[2]; b[5] = n->hi0[2];
+    b[6] = n->lo1[0]; b[7] = n->hi1[0]; b[8] = n->lo1[1]; b[9] = n->hi1[1]; b[10] = n->lo1[2]; b[11] = n->hi1[2];
+    c0 = n->c0;
+    c1 = n->c1;
+}
+
+template <class R>
+SST_D void load_tri(const void* tris, uint32_t i, V3<R>& v0, V3<R>& e1, V3<R>& e2, uint32_t& obj,
+                    uint32_t& id);
+template <>
+SST_D void load_tri<float>(const void* tris, uint32_t i, V3<float>& v0, V3<float>& e1,
+                           V3<float>& e2, uint32_t& obj, uint32_t& id) {
+    const TriF* t = static_cast<const TriF*>(tris) + i;
+    const float4 a = __ldg(&t->v0o), b = __ldg(&t->e1i), c = __ldg(&t->e2);
+    v0 = mk(a.x, a.y, a.z);
+    e1 = mk(b.x, b.y, b.z);
+    e2 = mk(c.x, c.y, c.z);
+    obj = __float_as_uint(a.w);
+    id = __float_as_uint(b.w);
+}
+template <>
+SST_D void load_tri<double>(const void* tris, uint32_t i, V3<double>& v0, V3<double>& e1,
+                            V3<double>& e2, uint32_t& obj, uint32_t& id) {
+    const TriD* t = static_cast<const TriD*>(tris) + i;
+    v0 = mk(t->v0[0], t->v0[1], t->v0[2]);
+    e1 = mk(t->e1[0], t->e1[1], t->e1[2]);
+    e2 = mk(t->e2[0], t->e2[1], t->e2[2]);
+    obj = t->obj;
+    id = t->id;
+}
+
+constexpr int kStack = 48;
+
+// Nearest hit with t in (t_min, t_max), ignoring triangle `skip` (FP32
+// self-intersection guard for rays leaving a surface; -1 = none).
+template <class R>
+SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
+                             R* t_hit, Hit* hit) {
+    int stack_n[kStack];
+    R stack_t[kStack];
+    int sp = 0;
+    int cur = 0;
+    R t_best = t_max;
+    bool found = false;
+    for (;;) {
+        if (cur >= 0) {
+            R b[12];
+            int c0, c1;
+            load_node<R>(sc.nodes, cur, b, c0, c1);
+            R t0, t1;
+            const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_best, &t0);
+            const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_best, &t1);
+            if (h0 && h1) {
+                const bool first0 = t0 <= t1;
+                stack_n[sp] = first0 ? c1 : c0;
+                stack_t[sp] = first0 ? t1 : t0;
+                ++sp;
+                cur = first0 ? c0 : c1;
+                continue;
+            }
+            if (h0) { cur = c0; continue; }
+            if (h1) { cur = c1; continue; }
+        } else {
+            const uint32_t leaf = static_cast<uint32_t>(~cur);
+            const uint32_t first = leaf >> 3, count = leaf & 7u;
+            for (uint32_t i = first; i < first + count; ++i) {
+                V3<R> v0, e1, e2;
+                uint32_t obj, id;
+                load_tri<R>(sc.tris, i, v0, e1, e2, obj, id);
+                if (static_cast<int>(id) == skip) continue;
+                R det;
+                const R t = ray_tri(ray, v0, e1, e2, t_min, t_best, &det);
+                if (t >= R(0)) {
+                    t_best = t;
+                    hit->tri = id;
+                    hit->obj = obj;
+                    found = true;
+                }
+            }
+        }
+        // pop the next node still in front of the best hit
+        for (;;) {
+            if (sp == 0) {
+                *t_hit = t_best;
+                return found;
+            }
+            --sp;
+            if (stack_t[sp] <= t_best) break;
+        }
+        cur = stack_n[sp];
+    }
+}
+
+// Optical depth along [0, t_max] from a point inside a medium (order-free signed sum;
+// see header). sigma(obj) = objs[obj].med[c].sigma_t.
+template <class R>
+SST_D R optical_depth(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int c) {
+    int stack_n[kStack];
+    int sp = 0;
+    int cur = 0;
+    R tau = R(0);
+    for (;;) {
+        if (cur >= 0) {
+            R b[12];
+            int c0, c1;
+            load_node<R>(sc.nodes, cur, b, c0, c1);
+            R t0, t1;
+            const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_max, &t0);
+            const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_max, &t1);
+            if (h0 && h1) {
+                stack_n[sp++] = c1;
+                cur = c0;
+                continue;
+            }
+            if (h0) { cur = c0; continue; }
+            if (h1) { cur = c1; continue; }
+        } else {
+            const uint32_t leaf = static_cast<uint32_t>(~cur);
+            const uint32_t first = leaf >> 3, count = leaf & 7u;
+            for (uint32_t i = first; i < first + count; ++i) {
+                V3<R> v0, e1, e2;
+                uint32_t obj, id;
+                load_tri<R>(sc.tris, i, v0, e1, e2, obj, id);
+                R det;
+                const R t = ray_tri(ray, v0, e1, e2, t_min, t_max, &det);
+                if (t >= R(0)) {
+                    const R sig = sc.objs[obj].med[c].sigma_t;
+                    tau += det < R(0) ? sig * t : -(sig * t);
+                }
+            }
+        }
+        if (sp == 0) return tau;
+        cur = stack_n[--sp];
+    }
+}
+
+}  // namespace sstg

@@ -1,0 +1,261 @@
+// integrator.cuh -- the per-path loop of the two integrators as a
+// persistent megakernel body. DESIGN.md "Integrator semantics" fixes the loop; the
+// CPU oracle (oracle/sst_oracle.c trace_one, oracle/ref_shim.cpp trace_one) follows
+// the same draw order, so FP64 paths reproduce the oracle draw for draw.
+//
+// Path state lives in registers for the whole path (no HBM round trips); a lane
+// whose path ends fetches the next path id with one warp-aggregated atomic.
+#pragma once
+
+#include "common.cuh"
+#include "geom.cuh"
+#include "rng.cuh"
+#include "step.cuh"
+#include "types.cuh"
+
+namespace sstg {
+
+
+// hg_sample_cos (optics.cpp:33-39)
+template <class R>
+SST_D R hg_cos(R g, R u) {
+    if (Real<R>::fabs_(g) < R(1e-4)) return R(1) - R(2) * u;
+    const R s = (R(1) - g * g) / (R(1) + g - R(2) * g * u);
+    const R c = (R(1) + g * g - s * s) / (R(2) * g);
+    return c < R(-1) ? R(-1) : (c > R(1) ? R(1) : c);
+}
+
+// hg_sample (optics.cpp:41-48)
+template <class R>
+SST_D V3<R> hg_sample(R g, V3<R> w_in, R u1, R u2) {
+    const R ct = hg_cos(g, u1);
+    const R st = Real<R>::sqrt_(Real<R>::fmax_(R(0), R(1) - ct * ct));
+    R cp, sp;
+    rot_angle<R>(u2, &cp, &sp);
+    V3<R> b1, b2;
+    onb(w_in, &b1, &b2);
+    return b1 * (st * cp) + b2 * (st * sp) + w_in * ct;
+}
+
+// hg_eval (optics.cpp:27-31)
+template <class R>
+SST_D R hg_eval(R g, R c) {
+    const R denom = R(1) + g * g - R(2) * g * c;
+    return R(kInv4PiD) * (R(1) - g * g) / (denom * Real<R>::sqrt_(denom));
+}
+
+// NEE toward the point light from p (in object obj, channel c) with incoming w:
+// weight * Phi * hg(g, w.wl) * exp(-tau) / d^2.
+template <class R>
+SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<R> w, R weight) {
+    const V3<R> to_l = sc.light - p;
+    const R d2 = dot(to_l, to_l);
+    const R d = Real<R>::sqrt_(d2);
+    const V3<R> wl = to_l / d;
+    const RayK<R> ray = make_ray(p, wl);
+    const R tau = optical_depth(sc, ray, sc.t_min, d, c);
+    const R phase = hg_eval(m.g, dot(w, wl));
+    return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) / d2;
+}
+
+template <class R>
+struct PathLocal {
+    V3<R> x, w;
+    Rng rng;
+    R L;
+    R r_here;       // SDF radius at x (valid iff r_valid)
+    uint64_t id;
+    uint32_t seg, pixel;
+    int obj;        // -1 outside every medium
+    int skip;       // triangle to ignore on the next traversal (FP32 surface start)
+    uint8_t c;
+    bool r_valid;
+};
+
+struct LaneStats {
+    uint32_t paths = 0, absorbed = 0, escaped = 0, capped = 0, errors = 0;
+    uint64_t seg = 0, sphere = 0, events = 0, shadow = 0;
+    DecodeCount dc;
+};
+
+template <class R, bool EXPLICIT>
+SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
+    uint32_t pixel, sample, c;
+    if (EXPLICIT) {
+        pixel = a.pixel[id];
+        sample = a.sample[id];
+        c = a.channel[id];
+    } else {  // id = (s_local * n_pix + pixel) * 3 + c
+        c = static_cast<uint32_t>(id % 3);
+        const uint64_t rest = id / 3;
+        pixel = static_cast<uint32_t>(rest % a.n_pix);
+        sample = a.sample_begin + static_cast<uint32_t>(rest / a.n_pix);
+    }
+    const DevScene<R>& sc = a.sc;
+    Rng cam{rng_key(a.seed, 0x06, pixel, sample)};  // kRenderPixel
+    const R jx = cam.uniform<R>();
+    const R jy = cam.uniform<R>();
+    const uint32_t px = pixel % sc.width, py = pixel / sc.width;
+    const R sx = (R(2) * (static_cast<R>(px) + jx) / static_cast<R>(sc.width) - R(1)) * sc.tan_half * sc.aspect;
+    const R sy = (R(1) - R(2) * (static_cast<R>(py) + jy) / static_cast<R>(sc.height)) * sc.tan_half;
+    p.x = sc.cam_pos;
+    p.w = normalize(sc.cam_fwd + sc.cam_right * sx + sc.cam_up * sy);
+    p.rng.s = rng_key(a.seed, 0x07, pixel, 3ull * sample + c);  // kRenderChannel
+    p.L = R(0);
+    p.id = id;
+    p.seg = 0;
+    p.pixel = pixel;
+    p.obj = -1;
+    p.skip = -1;
+    p.c = static_cast<uint8_t>(c);
+    p.r_valid = false;
+}
+
+// One state transition. Returns -1 while the path lives, else its end code.
+template <class R, bool ST>
+SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st) {
+    const DevScene<R>& sc = a.sc;
+    if (p.obj < 0) {  // outside all media: find the next boundary (medium entry)
+        const RayK<R> ray = make_ray(p.x, p.w);
+        R t;
+        Hit h;
+        const R tmin = p.skip >= 0 ? sc.surf_eps : sc.t_min;
+        if (!intersect_nearest(sc, ray, tmin, Real<R>::kInf, p.skip, &t, &h)) {
+            p.L += sc.bg[p.c];
+            return kEndEscaped;
+        }
+        p.x = p.x + p.w * t;
+        p.obj = static_cast<int>(h.obj);
+        p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
+        p.r_valid = false;
+    }
+    const ObjK<R>& ob = sc.objs[p.obj];
+    const MediumK<R>& m = ob.med[p.c];
+    // free flight (sample_free_path, optics.cpp:55-60)
+    R t_free;
+    if (m.sigma_t > R(0)) {
+        const R u = p.rng.template uniform<R>();
+        if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
+        else t_free = -Real<R>::log_(R(1) - u) / m.sigma_t;
+    } else {
+        t_free = Real<R>::kInf;
+    }
+    // A conservative SDF ball around x is surface-free: a flight shorter than its
+    // radius cannot reach the boundary, so the traversal is skipped (exact).
+    if (!p.r_valid) {
+        p.r_here = sdf_radius(ob, p.x);
+        p.r_valid = true;
+    }
+    bool left = false;
+    if (!(t_free < p.r_here)) {
+        const RayK<R> ray = make_ray(p.x, p.w);
+        R t;
+        Hit h;
+        const R tmin = p.skip >= 0 ? sc.surf_eps : sc.t_min;
+        if (intersect_nearest(sc, ray, tmin, t_free, p.skip, &t, &h)) {
+            p.x = p.x + p.w * t;
+            p.obj = -1;
+            p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
+            left = true;
+        }
+    }
+    if (left) return -1;
+    p.skip = -1;
+    p.x = p.x + p.w * t_free;  // collision
+    p.r_valid = false;
+    const uint32_t cap = ST ? sc.cap_st : sc.cap_pt;
+    if (p.seg >= cap) {
+        p.L = R(0);  // dropped
+        return kEndCapped;
+    }
+    ++p.seg;
+    if (ST) {
+        p.r_here = sdf_radius(ob, p.x);
+        p.r_valid = true;
+        if (p.r_here > m.r_min) {
+            ++st.sphere;
+            StepOut<R> o;
+            if (!sphere_step(m, p.w, p.x, p.r_here, a.nee != 0, p.rng, o, st.dc)) {
+                p.L = R(0);
+                return kEndError;
+            }
+            if (o.absorbed) return kEndAbsorbed;
+            if (a.nee) {
+                p.L += nee_term(sc, m, p.c, o.rep_pos, o.rep_dir, o.lambda);
+                ++st.shadow;
+            }
+            p.x = o.exit_pos;
+            p.w = o.exit_dir;
+            p.r_valid = false;
+            return -1;
+        }
+    }
+    // one delta-tracking event: Russian roulette by albedo, NEE, HG scatter
+    ++st.events;
+    if (!((p.rng.next() >> 11) < m.survive_below)) return kEndAbsorbed;  // u < phi, bit-exact
+    if (a.nee) {
+        p.L += nee_term(sc, m, p.c, p.x, p.w, R(1));
+        ++st.shadow;
+    }
+    const R u1 = p.rng.template uniform<R>();
+    const R u2 = p.rng.template uniform<R>();
+    p.w = hg_sample(m.g, p.w, u1, u2);
+    return -1;
+}
+
+template <class T>
+SST_D T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <class R, bool ST, bool EXPLICIT>
+SST_D void trace_persistent(const TraceArgs<R>& a) {
+    const unsigned lane = threadIdx.x & 31u;
+    PathLocal<R> p;
+    bool alive = false, exhausted = false;
+    LaneStats st;
+    for (;;) {
+        const unsigned need = __ballot_sync(0xffffffffu, !alive && !exhausted);
+        if (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (static_cast<int>(lane) == leader) base = atomicAdd(a.work, static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (!alive && !exhausted) {
+                const uint64_t my = base + __popc(need & ((1u << lane) - 1u));
+                if (my < a.n_paths) {
+                    path_init<R, EXPLICIT>(a, my, p);
+                    alive = true;
+                } else {
+                    exhausted = true;
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, alive)) break;
+        if (alive) {
+            const int end = path_advance<R, ST>(a, p, st);
+            if (end >= 0) {
+                a.radiance[p.id] = p.L;
+                if (a.segments) a.segments[p.id] = p.seg;
+                ++st.paths;
+                st.seg += p.seg;
+                st.escaped += end == kEndEscaped;
+                st.absorbed += end == kEndAbsorbed;
+                st.capped += end == kEndCapped;
+                st.errors += end == kEndError;
+                alive = false;
+            }
+        }
+    }
+    unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
+                                      st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow};
+#pragma unroll
+    for (int k = 0; k < kStCount; ++k) {
+        const unsigned long long s = warp_sum(v[k]);
+        if (lane == 0 && s) atomicAdd(a.stats + k, s);
+    }
+}
+
+}  // namespace sstg

@@ -1,0 +1,145 @@
+// kernels_f64.cu -- FP64 parity instantiation (compiled with -fmad=false so every
+// product/sum rounds like the reference's x86-64 FP64 code), plus the exact SDF
+// build kernel.
+#include <cstdint>
+
+#define SST_REAL double
+#define SST_NS f64
+
+__constant__ double c_weights[1332];
+__constant__ double c_norm[6];
+
+#include "kernels_impl.cuh"
+
+namespace sstg {
+
+namespace {
+
+struct D3 {
+    double x, y, z;
+};
+__device__ __forceinline__ D3 d3(double x, double y, double z) { return D3{x, y, z}; }
+__device__ __forceinline__ D3 sub(D3 a, D3 b) { return d3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ D3 add(D3 a, D3 b) { return d3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ D3 mul(D3 a, double s) { return d3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ double dt(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ D3 cr(D3 a, D3 b) {
+    return d3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+
+// point_triangle_distance_squared (mesh.cpp:199-233), same operation order.
+__device__ double pt_tri_d2(D3 p, D3 a, D3 b, D3 c) {
+    const D3 ab = sub(b, a), ac = sub(c, a), ap = sub(p, a);
+    const double d1 = dt(ab, ap), d2 = dt(ac, ap);
+    if (d1 <= 0.0 && d2 <= 0.0) { const D3 q = sub(p, a); return dt(q, q); }
+    const D3 bp = sub(p, b);
+    const double d3v = dt(ab, bp), d4 = dt(ac, bp);
+    if (d3v >= 0.0 && d4 <= d3v) { const D3 q = sub(p, b); return dt(q, q); }
+    const double vc = d1 * d4 - d3v * d2;
+    if (vc <= 0.0 && d1 >= 0.0 && d3v <= 0.0) {
+        const double v = d1 / (d1 - d3v);
+        const D3 q = sub(p, add(a, mul(ab, v)));
+        return dt(q, q);
+    }
+    const D3 cp = sub(p, c);
+    const double d5 = dt(ab, cp), d6 = dt(ac, cp);
+    if (d6 >= 0.0 && d5 <= d6) { const D3 q = sub(p, c); return dt(q, q); }
+    const double vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        const double w = d2 / (d2 - d6);
+        const D3 q = sub(p, add(a, mul(ac, w)));
+        return dt(q, q);
+    }
+    const double va = d3v * d6 - d5 * d4;
+    if (va <= 0.0 && (d4 - d3v) >= 0.0 && (d5 - d6) >= 0.0) {
+        const double w = (d4 - d3v) / ((d4 - d3v) + (d5 - d6));
+        const D3 q = sub(p, add(b, mul(sub(c, b), w)));
+        return dt(q, q);
+    }
+    const double denom = 1.0 / (va + vb + vc);
+    const double v = vb * denom, w = vc * denom;
+    const D3 q = sub(p, add(add(a, mul(ab, v)), mul(ac, w)));
+    return dt(q, q);
+}
+
+// ray_triangle (bvh.cpp:11-27) with t_min 1e-9, t_max 1e300 (Bvh::inside).
+__device__ bool mt_hit(D3 o, D3 d, D3 a, D3 b, D3 c) {
+    const D3 e1 = sub(b, a), e2 = sub(c, a);
+    const D3 pvec = cr(d, e2);
+    const double det = dt(e1, pvec);
+    if (fabs(det) < 1e-14) return false;
+    const double inv_det = 1.0 / det;
+    const D3 tvec = sub(o, a);
+    const double u = dt(tvec, pvec) * inv_det;
+    if (u < 0.0 || u > 1.0) return false;
+    const D3 qvec = cr(tvec, e1);
+    const double v = dt(d, qvec) * inv_det;
+    if (v < 0.0 || u + v > 1.0) return false;
+    const double t = dt(e2, qvec) * inv_det;
+    return !(t <= 1e-9 || t >= 1e300);
+}
+
+constexpr int kSdfTile = 128;
+
+// One voxel per thread; triangles staged through shared memory in tiles. The min
+// distance and the hit parity do not depend on traversal order, so brute force
+// over all triangles reproduces the reference's BVH-pruned build bit for bit.
+__global__ void __launch_bounds__(128) k_sdf_build(SdfBuildArgs a) {
+    __shared__ double tile[kSdfTile * 9];
+    const uint64_t nvox = static_cast<uint64_t>(a.dims[0]) * a.dims[1] * a.dims[2];
+    const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const bool active = v < nvox;
+    const uint32_t x = active ? static_cast<uint32_t>(v % a.dims[0]) : 0;
+    const uint32_t y = active ? static_cast<uint32_t>((v / a.dims[0]) % a.dims[1]) : 0;
+    const uint32_t z = active ? static_cast<uint32_t>(v / (static_cast<uint64_t>(a.dims[0]) * a.dims[1])) : 0;
+    // voxel_center (sdf.hpp:29-32)
+    const D3 c = add(d3(a.origin[0], a.origin[1], a.origin[2]),
+                     d3((x + 0.5) * a.voxel, (y + 0.5) * a.voxel, (z + 0.5) * a.voxel));
+    const D3 dirs[3] = {d3(a.dirs[0], a.dirs[1], a.dirs[2]), d3(a.dirs[3], a.dirs[4], a.dirs[5]),
+                        d3(a.dirs[6], a.dirs[7], a.dirs[8])};
+    double best = 1e300, wind = 0.0;
+    uint32_t hits[3] = {0, 0, 0};
+    for (uint32_t base = 0; base < a.n_tris; base += kSdfTile) {
+        const uint32_t n = min(static_cast<uint32_t>(kSdfTile), a.n_tris - base);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < n * 9; k += blockDim.x) tile[k] = a.tri_vertices[base * 9ull + k];
+        __syncthreads();
+        if (!active) continue;
+        for (uint32_t t = 0; t < n; ++t) {
+            const double* q = tile + 9 * t;
+            const D3 A = d3(q[0], q[1], q[2]), B = d3(q[3], q[4], q[5]), C = d3(q[6], q[7], q[8]);
+            best = fmin(best, pt_tri_d2(c, A, B, C));
+            if (a.watertight) {
+                for (int k = 0; k < 3; ++k) hits[k] += mt_hit(c, dirs[k], A, B, C);
+            } else {  // winding_number (bvh.cpp:219-232)
+                const D3 pa = sub(A, c), pb = sub(B, c), pc = sub(C, c);
+                const double la = sqrt(dt(pa, pa)), lb = sqrt(dt(pb, pb)), lc = sqrt(dt(pc, pc));
+                const double num = dt(pa, cr(pb, pc));
+                const double den = la * lb * lc + dt(pa, pb) * lc + dt(pb, pc) * la + dt(pc, pa) * lb;
+                wind += 2.0 * atan2(num, den);
+            }
+        }
+    }
+    if (!active) return;
+    bool inside;
+    if (a.watertight) {
+        const int votes = (hits[0] & 1) + (hits[1] & 1) + (hits[2] & 1);
+        inside = votes >= 2;
+    } else {
+        inside = wind / (4.0 * 3.14159265358979323846) > 0.5;
+    }
+    const double d = sqrt(best);
+    const double cons = fmax(0.0, d - a.half_diagonal);
+    a.values[v] = static_cast<float>(inside ? -cons : cons);
+}
+
+}  // namespace
+
+cudaError_t launch_sdf_build(const SdfBuildArgs& a, cudaStream_t s) {
+    const uint64_t nvox = static_cast<uint64_t>(a.dims[0]) * a.dims[1] * a.dims[2];
+    const unsigned grid = static_cast<unsigned>((nvox + 127) / 128);
+    k_sdf_build<<<grid, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace sstg

@@ -1,0 +1,153 @@
+// kernels_impl.cuh -- kernel bodies instantiated once per precision.
+// Included by kernels_f32.cu (SST_REAL=float, SST_NS=f32) and kernels_f64.cu
+// (SST_REAL=double, SST_NS=f64, compiled with -fmad=false).
+#pragma once
+
+#include "integrator.cuh"
+#include "launch.h"
+
+namespace sstg {
+namespace SST_NS {
+
+using R = SST_REAL;
+
+// ---------------------------------------------------------------------------
+// Batch of independent sphere steps (the parity unit; C ABI
+// sst_gpu_sphere_step_batch). One thread per step.
+__global__ void __launch_bounds__(128) k_step_batch(StepBatchArgs a) {
+    DecodeCount dc;
+    bool err = false;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < a.n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double phi = a.phi[i];
+        MediumK<R> m;
+        m.sigma_t = static_cast<R>(a.sigma_t[i]);
+        m.g = static_cast<R>(a.g[i]);
+        m.phi = static_cast<R>(phi);
+        m.phi_is_one = phi >= 1.0;
+        m.phi_is_zero = phi <= 0.0;
+        m.one_minus_phi = static_cast<R>(1.0 - phi);
+        m.log_phi = (phi > 0.0 && phi < 1.0) ? static_cast<R>(log(phi)) : R(0);
+        const V3<R> w = mk<R>(a.w_in[3 * i], a.w_in[3 * i + 1], a.w_in[3 * i + 2]);
+        const V3<R> c = mk<R>(a.center[3 * i], a.center[3 * i + 1], a.center[3 * i + 2]);
+        const bool we = a.with_event ? a.with_event[i] != 0 : a.with_event_default != 0;
+        Rng rng{a.rng_state[i]};
+        StepOut<R> o;
+        o.n = 1;
+        const bool ok = sphere_step(m, w, c, static_cast<R>(a.r[i]), we, rng, o, dc);
+        err |= !ok;
+        a.rng_state[i] = rng.s;
+        a.absorbed[i] = o.absorbed;
+        a.n_events[i] = o.n;
+        const bool ex = ok && !o.absorbed;
+        const bool rep = ex && we;
+        const V3<R> z = mk<R>(R(0), R(0), R(0));
+        const V3<R> ep = ex ? o.exit_pos : z, ed = ex ? o.exit_dir : z;
+        const V3<R> rp = rep ? o.rep_pos : z, rd = rep ? o.rep_dir : z;
+        a.exit_pos[3 * i] = ep.x; a.exit_pos[3 * i + 1] = ep.y; a.exit_pos[3 * i + 2] = ep.z;
+        a.exit_dir[3 * i] = ed.x; a.exit_dir[3 * i + 1] = ed.y; a.exit_dir[3 * i + 2] = ed.z;
+        a.rep_pos[3 * i] = rp.x; a.rep_pos[3 * i + 1] = rp.y; a.rep_pos[3 * i + 2] = rp.z;
+        a.rep_dir[3 * i] = rd.x; a.rep_dir[3 * i + 1] = rd.y; a.rep_dir[3 * i + 2] = rd.z;
+        a.has_rep[i] = rep;
+        a.lambda[i] = rep ? static_cast<double>(o.lambda) : 0.0;
+    }
+    const unsigned long long l = warp_sum<unsigned long long>(dc.l);
+    const unsigned long long p = warp_sum<unsigned long long>(dc.p);
+    const unsigned long long e = warp_sum<unsigned long long>(dc.e);
+    if ((threadIdx.x & 31) == 0) {
+        if (l) atomicAdd(a.counters + 0, l);
+        if (p) atomicAdd(a.counters + 1, p);
+        if (e) atomicAdd(a.counters + 2, e);
+    }
+    if (err) atomicOr(a.error, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent path-tracing megakernel (PT or ST; render ids or explicit keys).
+template <bool ST, bool EXPLICIT>
+__global__ void __launch_bounds__(kTraceBlock) k_trace(TraceArgs<R> a) {
+    trace_persistent<R, ST, EXPLICIT>(a);
+}
+
+// ---------------------------------------------------------------------------
+// Film accumulation: deterministic fixed-order FP64 sums over the slab's samples.
+// radiance[s * stride + k], k = pixel * 3 + channel (Image layout, image.hpp:13-29).
+__global__ void k_film(const R* __restrict__ radiance, uint64_t stride, uint32_t n_samples,
+                       double* __restrict__ sum, double* __restrict__ sumsq) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < stride;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0, q = 0.0;
+        for (uint32_t j = 0; j < n_samples; ++j) {
+            const double v = static_cast<double>(radiance[j * stride + k]);
+            s += v;
+            q += v * v;
+        }
+        sum[k] += s;
+        sumsq[k] += q;
+    }
+}
+
+static int g_sms = 0;
+static int sm_count() {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return g_sms;
+}
+
+cudaError_t upload_constants(const double* weights1332, const double* norms6, cudaStream_t s) {
+    R w[kTotalWeights];
+    R n[6];
+    for (int i = 0; i < kTotalWeights; ++i) w[i] = static_cast<R>(weights1332[i]);
+    for (int i = 0; i < 6; ++i) n[i] = static_cast<R>(norms6[i]);
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_weights, w, sizeof w, 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyToSymbolAsync(c_norm, n, sizeof n, 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(s);  // the host staging arrays live on this stack
+}
+
+cudaError_t launch_step_batch(const StepBatchArgs& a, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    const int block = 128;
+    const uint64_t need = (a.n + block - 1) / block;
+    const int grid = static_cast<int>(need < 1u << 20 ? need : 1u << 20);
+    k_step_batch<<<grid, block, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <bool ST, bool EX>
+static cudaError_t launch_trace_t(const TraceArgs<R>& a, cudaStream_t s) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace<ST, EX>, kTraceBlock, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    uint64_t grid = static_cast<uint64_t>(sm_count()) * blocks_per_sm;
+    const uint64_t warps_needed = (a.n_paths + 31) / 32;
+    const uint64_t max_grid = (warps_needed * 32 + kTraceBlock - 1) / kTraceBlock;
+    if (grid > max_grid) grid = max_grid;
+    if (grid < 1) grid = 1;
+    k_trace<ST, EX><<<static_cast<unsigned>(grid), kTraceBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {
+    if (a.n_paths == 0) return cudaSuccess;
+    if (st) return explicit_keys ? launch_trace_t<true, true>(a, s) : launch_trace_t<true, false>(a, s);
+    return explicit_keys ? launch_trace_t<false, true>(a, s) : launch_trace_t<false, false>(a, s);
+}
+
+cudaError_t launch_film(const R* radiance, uint64_t stride, uint32_t n_samples, double* sum,
+                        double* sumsq, cudaStream_t s) {
+    const int block = 256;
+    uint64_t grid = (stride + block - 1) / block;
+    if (grid > 65535u * 16u) grid = 65535u * 16u;
+    k_film<<<static_cast<unsigned>(grid), block, 0, s>>>(radiance, stride, n_samples, sum, sumsq);
+    return cudaGetLastError();
+}
+
+}  // namespace SST_NS
+}  // namespace sstg

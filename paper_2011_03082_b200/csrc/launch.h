@@ -1,0 +1,40 @@
+// launch.h -- host-side entry points of the two kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "types.cuh"
+
+namespace sstg {
+
+constexpr int kTraceBlock = 256;
+
+#define SST_DECLARE_LAUNCHERS(NS, REAL)                                                          \
+    namespace NS {                                                                              \
+    cudaError_t upload_constants(const double* weights1332, const double* norms6, cudaStream_t); \
+    cudaError_t launch_step_batch(const StepBatchArgs& a, cudaStream_t s);                      \
+    cudaError_t launch_trace(const TraceArgs<REAL>& a, bool st, bool explicit_keys,             \
+                             cudaStream_t s);                                                   \
+    cudaError_t launch_film(const REAL* radiance, uint64_t stride, uint32_t n_samples,          \
+                            double* sum, double* sumsq, cudaStream_t s);                        \
+    }
+
+SST_DECLARE_LAUNCHERS(f32, float)
+SST_DECLARE_LAUNCHERS(f64, double)
+#undef SST_DECLARE_LAUNCHERS
+
+// Exact FP64 SDF build (kernels_f64.cu): build_sdf semantics of sdf.cpp:20-58.
+struct SdfBuildArgs {
+    const double* tri_vertices;  // [9 * n_tris] (a, b, c) per triangle
+    uint32_t n_tris;
+    double origin[3];
+    double voxel;
+    uint32_t dims[3];
+    double half_diagonal;
+    double dirs[9];    // normalised inside-test directions (bvh.cpp:206-208)
+    int watertight;    // parity vote if 1, generalized winding number if 0
+    float* values;
+};
+cudaError_t launch_sdf_build(const SdfBuildArgs& a, cudaStream_t s);
+
+}  // namespace sstg

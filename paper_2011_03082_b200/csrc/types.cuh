@@ -1,0 +1,122 @@
+// types.cuh -- plain data shared by the host API (api.cu) and the kernel TUs.
+#pragma once
+
+#include "common.cuh"
+
+namespace sstg {
+
+// Per-medium constants, precomputed on the host in double (so FP32 kernels see
+// correctly rounded log(phi) and 1-phi, not their float cancellations).
+template <class R>
+struct MediumK {
+    R sigma_t, g, phi;
+    R log_phi;        // log(phi)   (0 < phi < 1)
+    R one_minus_phi;  // 1 - phi
+    R r_min;          // sphere-step threshold
+    uint64_t survive_below;  // roulette: survive iff (draw >> 11) < ceil(phi * 2^53): bit-exact u < phi
+    uint32_t phi_is_one, phi_is_zero;
+};
+
+template <class R>
+struct StepOut {
+    bool absorbed;
+    uint32_t n;
+    V3<R> exit_pos, exit_dir, rep_pos, rep_dir;
+    R lambda;
+};
+
+struct DecodeCount {
+    uint32_t l = 0, p = 0, e = 0;
+};
+
+// FP32 node: a = (lo0.x, hi0.x, lo0.y, hi0.y), b = (lo1.x, hi1.x, lo1.y, hi1.y),
+//            c = (lo0.z, hi0.z, lo1.z, hi1.z), d = (child0, child1, -, -)
+// child >= 0: interior node index; child < 0: leaf, ~child = (first << 3) | count.
+struct alignas(16) NodeF {
+    float4 a, b, c;
+    int4 d;
+};
+struct alignas(16) NodeD {
+    double lo0[3], hi0[3], lo1[3], hi1[3];
+    int32_t c0, c1, pad0, pad1;
+};
+// Triangles in leaf order. FP32: v0.xyz + object id, e1.xyz + triangle id, e2.xyz.
+struct alignas(16) TriF {
+    float4 v0o, e1i, e2;
+};
+struct alignas(16) TriD {
+    double v0[3], e1[3], e2[3];
+    uint32_t obj, id;
+};
+
+template <class R>
+struct ObjK {
+    MediumK<R> med[3];
+    R sdf_origin[3];
+    R sdf_voxel;
+    R sdf_inv_voxel;
+    uint32_t dims[3];
+    const float* sdf;
+};
+
+template <class R>
+struct DevScene {
+    const void* nodes;
+    const void* tris;
+    const ObjK<R>* objs;
+    uint32_t n_objects;
+    V3<R> light;
+    R power[3], bg[3];
+    V3<R> cam_pos, cam_fwd, cam_right, cam_up;
+    R tan_half, aspect;
+    uint32_t width, height;
+    R t_min, surf_eps;
+    uint32_t cap_pt, cap_st;
+};
+
+struct Hit {
+    uint32_t tri, obj;
+};
+
+enum : int { kEndEscaped = 0, kEndAbsorbed = 1, kEndCapped = 2, kEndError = 3 };
+
+// Stats slots (device u64 array).
+enum : int {
+    kStPaths = 0, kStSegments, kStSphere, kStEvents, kStDecL, kStDecP, kStDecE, kStAbsorbed,
+    kStEscaped, kStCapped, kStErrors, kStShadow, kStCount
+};
+
+template <class R>
+struct TraceArgs {
+    DevScene<R> sc;
+    int nee;
+    uint64_t seed;
+    uint64_t n_paths;
+    uint32_t n_pix;
+    uint32_t sample_begin;
+    const uint32_t* pixel;   // explicit-key mode (trace_paths); null for render
+    const uint32_t* sample;
+    const uint8_t* channel;
+    R* radiance;             // [n_paths]
+    uint32_t* segments;      // [n_paths] or null
+    unsigned long long* work;   // path-id counter
+    unsigned long long* stats;  // [kStCount]
+};
+
+// Arguments of the sphere-step batch kernel (C ABI sst_gpu_sphere_step_batch).
+struct StepBatchArgs {
+    uint64_t n;
+    const double *sigma_t, *g, *phi, *w_in, *center, *r;
+    const uint8_t* with_event;
+    int with_event_default;
+    uint64_t* rng_state;
+    uint8_t* absorbed;
+    uint32_t* n_events;
+    double *exit_pos, *exit_dir;
+    uint8_t* has_rep;
+    double *rep_pos, *rep_dir, *lambda;
+    unsigned long long* counters;  // [3] length, path, event
+    int* error;
+};
+
+}  // namespace sstg

@@ -1,0 +1,62 @@
+"""Live pinning of the C oracle against the reference library built from
+/root/reference (oracle/_ref). Skipped where the reference is absent (GPU box)."""
+import ctypes as C
+
+import numpy as np
+
+from util import random_step_batch
+
+
+def test_steps_live(ref, oracle, models_dir):
+    b = random_step_batch(3000, 123, oracle)
+    keys = np.stack([np.full(3000, 123), np.full(3000, 6), np.arange(3000), np.zeros(3000)], 1).astype(np.uint64)
+    ro = ref.Models(models_dir).sphere_step_batch(b["sigma_t"], b["g"], b["phi"], b["w_in"], b["center"],
+                                                 b["r_sphere"], b["with_event"], keys)
+    oo = oracle.Models(models_dir).sphere_step_batch(b)
+    for k in oo:
+        assert (oo[k] == ro[k]).all(), k
+
+
+def test_bvh_live(ref, oracle):
+    from paper_2011_03082_b200 import make_bumpy_sphere
+    from paper_2011_03082_b200.scene import SdfGrid, c1_scene
+    P, T = make_bumpy_sphere(3, 1.0, 0.2, 3.0)
+    rng = np.random.default_rng(9)
+    o = rng.normal(size=(2000, 3)) * 0.7
+    d = rng.normal(size=(2000, 3))
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    t, tid = ref.bvh_intersect(P, T, o, d)
+    sc = oracle.Scene(c1_scene((P, T), 4, 4, sdf=SdfGrid(np.zeros(3), 1.0, np.array([1, 1, 1]),
+                                                          np.zeros(1, np.float32))).to_desc())
+    for i in range(len(o)):
+        tt, _ = sc.intersect(o[i], d[i])
+        assert tt == t[i]
+
+
+def test_sdf_live(ref, oracle):
+    from paper_2011_03082_b200 import make_icosphere
+    P, T = make_icosphere(2, 0.7)
+    a = ref.build_sdf(P, T, 20)
+    b = oracle.build_sdf(P, T, 20)
+    assert (a[0] == b[0]).all() and a[1] == b[1] and (a[2] == b[2]).all() and (a[3] == b[3]).all()
+
+
+def test_integrator_live_res64(ref, oracle, models_dir):
+    """Reference-composed vs C-restated integrator on the full C1 scene (res-64 SDF)."""
+    from paper_2011_03082_b200 import abi, make_icosphere
+    from paper_2011_03082_b200.scene import SdfGrid, c1_scene
+    P, T = make_icosphere(3, 1.0)
+    sdf = SdfGrid(*ref.build_sdf(P, T, 64))
+    desc = c1_scene((P, T), 256, 256, sdf=sdf).to_desc()
+    rs = ref.Scene(C.byref(desc))
+    os_ = oracle.Scene(desc)
+    rng = np.random.default_rng(4)
+    n = 1500
+    pix = rng.integers(0, 256 * 256, n)
+    smp = rng.integers(0, 64, n)
+    ch = rng.integers(0, 3, n)
+    rm, om = ref.Models(models_dir), oracle.Models(models_dir)
+    for integ in (0, 1):
+        r1, s1 = rs.trace_paths(rm, integ, 1, 7, pix, smp, ch, abi.PathStats())
+        r2, s2 = os_.trace_paths(om, integ, 1, 7, pix, smp, ch, abi.PathStats())
+        assert (r1 == r2).all() and (s1 == s2).all()
