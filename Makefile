@@ -8,12 +8,16 @@ NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall
 CSRC = paper_2011_03082_b200/csrc
 BUILD = build
 LIB = paper_2011_03082_b200/libsst_gpu.so
+PEAKLIB = paper_2011_03082_b200/libsst_peak.so
 HDRS = $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/sst_gpu.h include/sst_host.h
 
 .PHONY: all lib oracle clean
 all: lib oracle
 
-lib: $(LIB)
+lib: $(LIB) $(PEAKLIB)
+
+$(PEAKLIB): $(CSRC)/peak.cu
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $<
 
 $(BUILD)/kernels_f32.o: $(CSRC)/kernels_f32.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -39,5 +43,5 @@ oracle:
 	$(MAKE) -C oracle all
 
 clean:
-	rm -rf $(BUILD) $(LIB)
+	rm -rf $(BUILD) $(LIB) $(PEAKLIB)
 	$(MAKE) -C oracle clean

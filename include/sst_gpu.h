@@ -208,6 +208,10 @@ typedef struct {
 /* Uploads the scene: builds the BVH on the host, builds missing SDFs on the
  * GPU, copies everything to device memory owned by the context. */
 int sst_gpu_upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* scene);
+/* Device footprint of the uploaded scene: bytes copied host->device by the last
+ * sst_gpu_upload_scene (BVH nodes + triangles in both precisions, SDF grids,
+ * medium tables), BVH node and triangle counts. */
+int sst_gpu_scene_info(sst_gpu_ctx* ctx, uint64_t* h2d_bytes, uint32_t* n_nodes, uint32_t* n_triangles);
 /* Copies back the SDF grid of object `obj` (values may be NULL to query the
  * dims/origin/voxel only). */
 int sst_gpu_get_sdf(sst_gpu_ctx* ctx, uint32_t obj, double origin[3], double* voxel,

@@ -187,6 +187,11 @@ class Renderer:
         abi.check(abi.lib().sst_gpu_upload_scene(self.h, C.byref(d)))
         self.scene = scene
 
+    def scene_info(self):
+        b, nn, nt = C.c_uint64(), C.c_uint32(), C.c_uint32()
+        abi.check(abi.lib().sst_gpu_scene_info(self.h, C.byref(b), C.byref(nn), C.byref(nt)))
+        return {"h2d_bytes": b.value, "bvh_nodes": nn.value, "triangles": nt.value}
+
     def get_sdf(self, obj: int = 0):
         origin = np.zeros(3)
         voxel = C.c_double()

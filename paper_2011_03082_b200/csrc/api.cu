@@ -103,6 +103,8 @@ struct sst_gpu_ctx {
     uint64_t model_gen = 0;
 
     bool scene = false;
+    uint64_t scene_bytes = 0;
+    uint32_t n_nodes = 0, n_tris = 0;
     std::vector<ObjectHost> objects;
     sst_scene_desc desc{};
     DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64;
@@ -361,6 +363,12 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         ctx->sdf_dev[o].reserve(s.size() * sizeof(float));
         CK(cudaMemcpyAsync(ctx->sdf_dev[o].p, s.data(), s.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
     }
+    uint64_t bytes = bvh.nodes_f32.size() + bvh.tris_f32.size() + bvh.nodes_f64.size() + bvh.tris_f64.size();
+    for (const auto& o : ctx->objects) bytes += o.sdf.size() * sizeof(float);
+    bytes += ctx->objects.size() * (sizeof(ObjK<float>) + sizeof(ObjK<double>));
+    ctx->scene_bytes = bytes;
+    ctx->n_nodes = bvh.n_nodes;
+    ctx->n_tris = bvh.n_tris;
     fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
     fill_devscene<double>(ctx, ctx->sc64, ctx->nodes64, ctx->tris64, ctx->objs64);
     CK(cudaStreamSynchronize(ctx->stream));
@@ -648,7 +656,7 @@ int sst_gpu_sphere_step_batch(sst_gpu_ctx* ctx, uint64_t n, const sst_step_in* i
                 if (!(in->r_sphere[i] > 0.0)) throw DomainError("to_world: r_sphere must be > 0");
             }
         }
-        ctx->error.reserve(sizeof(int) + 3 * sizeof(unsigned long long));
+        ctx->error.reserve(8 + 3 * sizeof(unsigned long long));
         int* derr = ctx->error.as<int>();
         unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(ctx->error.as<char>() + 8);
         CK(cudaMemsetAsync(ctx->error.p, 0, 8 + 3 * sizeof(unsigned long long), ctx->stream));
@@ -731,6 +739,15 @@ int sst_gpu_upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* scene) {
     return guarded([&] {
         require_device(ctx);
         upload_scene(ctx, scene);
+    });
+}
+
+int sst_gpu_scene_info(sst_gpu_ctx* ctx, uint64_t* h2d_bytes, uint32_t* n_nodes, uint32_t* n_triangles) {
+    return guarded([&] {
+        if (!ctx || !ctx->scene) throw InvalidArgument("no scene uploaded");
+        if (h2d_bytes) *h2d_bytes = ctx->scene_bytes;
+        if (n_nodes) *n_nodes = ctx->n_nodes;
+        if (n_triangles) *n_triangles = ctx->n_tris;
     });
 }
 

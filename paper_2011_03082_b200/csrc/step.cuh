@@ -95,6 +95,7 @@ SST_D bool sphere_step(const MediumK<R>& m, V3<R> w_in, V3<R> center, R r, bool 
     }
     const R nf = static_cast<R>(o.n);
     R ct, al, be;
+    bool projected = false;
     {  // sample_exit
         R cond[3] = {Real<R>::div_(l1, c_norm[2]), m.g,
                      Real<R>::div_(Real<R>::log_(Real<R>::fmax_(R(1), nf)), c_norm[3])};
@@ -108,6 +109,7 @@ SST_D bool sphere_step(const MediumK<R>& m, V3<R> w_in, V3<R> center, R r, bool 
             const R inv = R(1) / Real<R>::sqrt_(r2);
             al *= inv;
             be *= inv;
+            projected = true;
         }
     }
     R cp, sp;
@@ -121,7 +123,13 @@ SST_D bool sphere_step(const MediumK<R>& m, V3<R> w_in, V3<R> center, R r, bool 
         if (st < R(1e-9)) onb(e_n, &e_b, &b2);
         else e_b = normalize(cross(mk<R>(R(0), R(0), R(1)), e_n));
         const V3<R> e_t = cross(e_b, e_n);
-        const R nc = Real<R>::sqrt_(Real<R>::fmax_(R(0), R(1) - al * al - be * be));
+        // Normal component sqrt(1 - a^2 - b^2) (scatter.cpp:124). After the unit-disk
+        // projection it is 0 mathematically; FP64 keeps the reference's expression
+        // (whose rounding leaves up to ~1.5e-8), FP32 uses the exact 0 because
+        // sqrt(FP32 rounding) would inject ~3e-4 into grazing exits.
+        R nc;
+        if (Real<R>::kIsDouble) nc = Real<R>::sqrt_(Real<R>::fmax_(R(0), R(1) - al * al - be * be));
+        else nc = projected ? R(0) : Real<R>::sqrt_(Real<R>::fmax_(R(0), R(1) - al * al - be * be));
         const V3<R> d = normalize(e_b * al + e_t * be + e_n * nc);
         o.exit_dir = rot * d;
     }
