@@ -235,10 +235,18 @@ typedef struct {
  * per ptr_kind (device: double, must be zeroed by the caller before the first
  * slab). RNG keys: camera jitter RandomStream(seed, kRenderPixel, pixel,
  * sample); path RandomStream(seed, kRenderChannel, pixel, 3*sample+channel).
- * stats is accumulated (may be NULL). */
+ * Host pointers or a non-NULL stats make the call synchronous (stats accumulated,
+ * including counters of earlier unread asynchronous calls). Device pointers with
+ * stats == NULL return after enqueueing: consecutive calls pipeline on the
+ * context's internal streams (long-path tails overlap the next slab); collect with
+ * sst_gpu_read_stats, and only read the film after it or sst_gpu_synchronize. */
 int sst_gpu_render(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total,
                    uint32_t sample_begin, uint32_t sample_end, uint64_t seed, double* film_sum,
                    double* film_sumsq, int ptr_kind, sst_path_stats* stats);
+
+/* Waits for all enqueued work, adds the counters accumulated since the last read
+ * (and their device time) into *stats and resets them. */
+int sst_gpu_read_stats(sst_gpu_ctx* ctx, sst_path_stats* stats);
 
 /* Per-path parity entry: traces n explicit (pixel, sample, channel) paths and
  * returns their radiance and segment counts (host pointers). */

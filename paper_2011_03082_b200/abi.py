@@ -95,7 +95,7 @@ EXPORTED = [
     "sst_gpu_set_precision", "sst_gpu_get_device", "sst_gpu_stream", "sst_gpu_synchronize",
     "sst_gpu_upload_models", "sst_gpu_load_models_dir", "sst_rng_init",
     "sst_gpu_sphere_step_batch", "sst_gpu_upload_scene", "sst_gpu_scene_info", "sst_gpu_get_sdf", "sst_gpu_render",
-    "sst_gpu_trace_paths",
+    "sst_gpu_trace_paths", "sst_gpu_read_stats",
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
     "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm",
@@ -138,6 +138,7 @@ def _declare(L):
     L.sst_gpu_get_sdf.argtypes = [P, U32, P, P, P, P]
     L.sst_gpu_scene_info.argtypes = [P, P, P, P]
     L.sst_gpu_render.argtypes = [P, I, I, U32, U32, U32, U64, P, P, I, C.POINTER(PathStats)]
+    L.sst_gpu_read_stats.argtypes = [P, C.POINTER(PathStats)]
     L.sst_gpu_trace_paths.argtypes = [P, I, I, U64, U64, P, P, P, P, P, C.POINTER(PathStats)]
     L.sst_mesh_icosphere.argtypes = [I, D, P, P, P, P]
     L.sst_mesh_bumpy_sphere.argtypes = [I, D, D, D, P, P, P, P]

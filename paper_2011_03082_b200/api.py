@@ -223,13 +223,23 @@ class Renderer:
         return film.image(), stats
 
     def render_device(self, integrator, spp_total, sample_begin, sample_end, seed, nee, sum_ptr,
-                      sumsq_ptr, stats=None):
-        """Accumulates into caller-owned DEVICE film buffers (e.g. torch tensors)."""
-        stats = stats if stats is not None else abi.PathStats()
+                      sumsq_ptr, stats=None, asynchronous=False):
+        """Accumulates into caller-owned DEVICE film buffers (e.g. torch tensors).
+        asynchronous=True enqueues and returns (collect with read_stats())."""
+        if asynchronous:
+            sp = None
+        else:
+            stats = stats if stats is not None else abi.PathStats()
+            sp = C.byref(stats)
         abi.check(abi.lib().sst_gpu_render(self.h, integrator, int(nee), spp_total, sample_begin,
                                            sample_end, seed, C.c_void_p(sum_ptr),
-                                           C.c_void_p(sumsq_ptr), abi.SST_PTR_DEVICE,
-                                           C.byref(stats)))
+                                           C.c_void_p(sumsq_ptr), abi.SST_PTR_DEVICE, sp))
+        return stats
+
+    def read_stats(self, stats=None):
+        """Waits for enqueued work and returns the counters accumulated since the last read."""
+        stats = stats if stats is not None else abi.PathStats()
+        abi.check(abi.lib().sst_gpu_read_stats(self.h, C.byref(stats)))
         return stats
 
     def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None):

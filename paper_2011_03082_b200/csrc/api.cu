@@ -115,6 +115,19 @@ struct sst_gpu_ctx {
     DevBuf radiance, segments, work, stats, error, film_sum, film_sq, keys_pix, keys_smp, keys_ch;
     DevBuf step_in, step_out;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    // Render pipeline: chunks of a render call rotate over kSlots streams so the
+    // long-path tail of one persistent launch overlaps the next launch's bulk.
+    // Film accumulations stay in chunk order (event chain) -> deterministic sums.
+    static constexpr int kSlots = 3;
+    struct Slot {
+        cudaStream_t s = nullptr;
+        DevBuf rad, work;
+        cudaEvent_t film_done = nullptr;
+    } slots[kSlots];
+    int next_slot = 0;
+    cudaEvent_t ev_start = nullptr, last_film = nullptr;
+    bool timing_open = false;
 };
 
 namespace {
@@ -387,7 +400,7 @@ template <class R>
 void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_keys, int nee,
                uint64_t seed, uint64_t n_paths, uint32_t n_pix, uint32_t sample_begin,
                const uint32_t* pix, const uint32_t* smp, const uint8_t* ch, R* radiance,
-               uint32_t* segments) {
+               uint32_t* segments, unsigned long long* work, cudaStream_t stream) {
     TraceArgs<R> a{};
     a.sc = sc;
     a.nee = nee;
@@ -400,11 +413,11 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.channel = ch;
     a.radiance = radiance;
     a.segments = segments;
-    a.work = ctx->work.as<unsigned long long>();
+    a.work = work;
     a.stats = ctx->stats.as<unsigned long long>();
-    CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), ctx->stream));
-    if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, ctx->stream));
-    else CK(f64::launch_trace(a, st, explicit_keys, ctx->stream));
+    CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
+    if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
+    else CK(f64::launch_trace(a, st, explicit_keys, stream));
 }
 
 void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
@@ -412,6 +425,7 @@ void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
     CK(cudaMemcpyAsync(v, ctx->stats.p, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (v[kStErrors]) {
+        CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
         // the reference throws std::runtime_error (scatter.cpp:56)
         if (out) {
             out->errors += v[kStErrors];
@@ -438,19 +452,55 @@ void check_render_ready(sst_gpu_ctx* ctx, int integrator) {
     if (integrator == SST_INTEGRATOR_ST) ensure_constants(ctx);
 }
 
+void ensure_pipeline(sst_gpu_ctx* ctx) {
+    if (ctx->ev_start) return;
+    for (auto& sl : ctx->slots) {
+        CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&sl.film_done, cudaEventDisableTiming));
+        sl.work.reserve(sizeof(unsigned long long));
+    }
+    CK(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    ctx->stats.reserve(kStCount * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+}
+
+// Makes ctx->stream wait for every render slot (no host synchronisation).
+void join_slots(sst_gpu_ctx* ctx) {
+    if (!ctx->ev_start) return;
+    for (auto& sl : ctx->slots) CK(cudaStreamWaitEvent(ctx->stream, sl.film_done, 0));
+}
+
+// Joins, synchronises and moves the accumulated device counters (and the device
+// time since the first unread call) into *out; resets the accumulators.
+void collect_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
+    ensure_pipeline(ctx);
+    join_slots(ctx);
+    float ms = 0.0f;
+    if (ctx->timing_open) CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->timing_open) {
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->timing_open = false;
+    }
+    if (out) out->device_ms += ms;
+    read_stats(ctx, out);
+    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+}
+
 template <class R>
 void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, uint32_t s0, uint32_t s1,
                  uint64_t seed, double* film_sum, double* film_sq, int ptr_kind, sst_path_stats* stats) {
+    (void)spp_total;
     const DevScene<R>& sc = scene_of<R>(ctx);
     const uint32_t n_pix = ctx->desc.width * ctx->desc.height;
     const uint64_t per_sample = 3ull * n_pix;
     const uint32_t n_samples = s1 - s0;
     uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, kChunkPaths / per_sample));
     if (chunk > n_samples) chunk = n_samples;
-    ctx->radiance.reserve(per_sample * chunk * sizeof(R));
-    ctx->stats.reserve(kStCount * sizeof(unsigned long long));
-    ctx->work.reserve(sizeof(unsigned long long));
-    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+    ensure_pipeline(ctx);
+    const bool sync = ptr_kind == SST_PTR_HOST || stats != nullptr;
     double* dsum = film_sum;
     double* dsq = film_sq;
     if (ptr_kind == SST_PTR_HOST) {
@@ -461,19 +511,27 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         CK(cudaMemsetAsync(dsum, 0, per_sample * sizeof(double), ctx->stream));
         CK(cudaMemsetAsync(dsq, 0, per_sample * sizeof(double), ctx->stream));
     }
-    if (!ctx->ev0) {
-        CK(cudaEventCreate(&ctx->ev0));
-        CK(cudaEventCreate(&ctx->ev1));
+    if (!ctx->timing_open) {
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        ctx->timing_open = true;
     }
-    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    CK(cudaEventRecord(ctx->ev_start, ctx->stream));
     for (uint32_t s = s0; s < s1; s += chunk) {
         const uint32_t ns = std::min(chunk, s1 - s);
+        auto& sl = ctx->slots[ctx->next_slot];
+        ctx->next_slot = (ctx->next_slot + 1) % sst_gpu_ctx::kSlots;
+        sl.rad.reserve(per_sample * chunk * sizeof(R));
+        CK(cudaStreamWaitEvent(sl.s, ctx->ev_start, 0));
         run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, false, nee, seed, per_sample * ns, n_pix, s,
-                     nullptr, nullptr, nullptr, ctx->radiance.as<R>(), nullptr);
-        if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(ctx->radiance.as<R>(), per_sample, ns, dsum, dsq, ctx->stream));
-        else CK(f64::launch_film(ctx->radiance.as<R>(), per_sample, ns, dsum, dsq, ctx->stream));
+                     nullptr, nullptr, nullptr, sl.rad.as<R>(), nullptr, sl.work.as<unsigned long long>(), sl.s);
+        if (ctx->last_film) CK(cudaStreamWaitEvent(sl.s, ctx->last_film, 0));
+        if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
+        else CK(f64::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
+        CK(cudaEventRecord(sl.film_done, sl.s));
+        ctx->last_film = sl.film_done;
     }
-    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    if (!sync) return;  // asynchronous device-pointer call: sst_gpu_read_stats collects
+    join_slots(ctx);
     if (ptr_kind == SST_PTR_HOST) {
         std::vector<double> hs(per_sample), hq(per_sample);
         CK(cudaMemcpyAsync(hs.data(), dsum, per_sample * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -484,11 +542,7 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
             film_sq[i] += hq[i];
         }
     }
-    CK(cudaStreamSynchronize(ctx->stream));
-    float ms = 0.0f;
-    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    if (stats) stats->device_ms += ms;
-    read_stats(ctx, stats);
+    collect_stats(ctx, stats);
 }
 
 template <class R>
@@ -501,26 +555,29 @@ void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, 
         if (pixel[i] >= n_pix) throw InvalidArgument("pixel index out of range");
         if (channel[i] > 2) throw InvalidArgument("channel must be 0, 1 or 2");
     }
+    ensure_pipeline(ctx);
+    collect_stats(ctx, nullptr);  // drain (and discard) counters of earlier asynchronous calls
     ctx->keys_pix.reserve(n * 4);
     ctx->keys_smp.reserve(n * 4);
     ctx->keys_ch.reserve(n);
     ctx->radiance.reserve(n * sizeof(R));
     ctx->segments.reserve(n * 4);
-    ctx->stats.reserve(kStCount * sizeof(unsigned long long));
     ctx->work.reserve(sizeof(unsigned long long));
-    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    ctx->timing_open = true;
     CK(cudaMemcpyAsync(ctx->keys_pix.p, pixel, n * 4, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->keys_smp.p, sample, n * 4, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->keys_ch.p, channel, n, cudaMemcpyHostToDevice, ctx->stream));
     run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, true, nee, seed, n, n_pix, 0,
                  ctx->keys_pix.as<uint32_t>(), ctx->keys_smp.as<uint32_t>(), ctx->keys_ch.as<uint8_t>(),
-                 ctx->radiance.as<R>(), ctx->segments.as<uint32_t>());
+                 ctx->radiance.as<R>(), ctx->segments.as<uint32_t>(), ctx->work.as<unsigned long long>(),
+                 ctx->stream);
     std::vector<R> rad(n);
     CK(cudaMemcpyAsync(rad.data(), ctx->radiance.p, n * sizeof(R), cudaMemcpyDeviceToHost, ctx->stream));
     if (segments) CK(cudaMemcpyAsync(segments, ctx->segments.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     for (uint64_t i = 0; i < n; ++i) radiance[i] = static_cast<double>(rad[i]);
-    read_stats(ctx, stats);
+    collect_stats(ctx, stats);
 }
 
 }  // namespace
@@ -575,6 +632,14 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
     for (auto& b : ctx->sdf_dev) b.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+    for (auto& sl : ctx->slots) {
+        if (sl.s) cudaStreamSynchronize(sl.s);
+        sl.rad.release();
+        sl.work.release();
+        if (sl.film_done) cudaEventDestroy(sl.film_done);
+        if (sl.s) cudaStreamDestroy(sl.s);
+    }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -594,7 +659,15 @@ void* sst_gpu_stream(sst_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st
 int sst_gpu_synchronize(sst_gpu_ctx* ctx) {
     return guarded([&] {
         require_device(ctx);
+        join_slots(ctx);
         CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sst_gpu_read_stats(sst_gpu_ctx* ctx, sst_path_stats* stats) {
+    return guarded([&] {
+        require_device(ctx);
+        collect_stats(ctx, stats);
     });
 }
 

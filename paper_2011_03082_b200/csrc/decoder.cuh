@@ -79,11 +79,10 @@ SST_D bool decode_sample(const R (&cond)[S::P_IN], Rng& rng, R (&x)[S::P_OUT], u
 #pragma unroll 1
     for (int attempt = 0; attempt < 2; ++attempt) {
         R in[S::IN];
-        R eps[S::P_OUT];
+        R nz[S::LATENT + S::P_OUT];  // z then eps, the reference's draw order
+        rng.s = draw_normals<R>(rng.s, nz, S::LATENT + S::P_OUT);
 #pragma unroll
-        for (int i = 0; i < S::LATENT; ++i) in[i] = rng.normal<R>();
-#pragma unroll
-        for (int i = 0; i < S::P_OUT; ++i) eps[i] = rng.normal<R>();
+        for (int i = 0; i < S::LATENT; ++i) in[i] = nz[i];
 #pragma unroll
         for (int i = 0; i < S::P_IN; ++i) in[S::LATENT + i] = cond[i];
         ++count;
@@ -92,7 +91,7 @@ SST_D bool decode_sample(const R (&cond)[S::P_IN], Rng& rng, R (&x)[S::P_OUT], u
         bool finite = true;
 #pragma unroll
         for (int i = 0; i < S::P_OUT; ++i) {
-            x[i] = mu[i] + Real<R>::exp_(R(0.5) * lv[i]) * eps[i];
+            x[i] = mu[i] + Real<R>::exp_(R(0.5) * lv[i]) * nz[S::LATENT + i];
             finite = finite && Real<R>::isfinite_(x[i]);
         }
         if (finite) return true;

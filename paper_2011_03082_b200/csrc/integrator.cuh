@@ -111,96 +111,132 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
     p.r_valid = false;
 }
 
-// One state transition. Returns -1 while the path lives, else its end code.
+// One iteration of the path loop, written as a fixed sequence of phases in which
+// every expensive operation (BVH traversal, sphere step, NEE shadow traversal)
+// has exactly ONE call site: the kernel is instruction-cache bound, and lanes of a
+// warp that reached the same operation by different routes (e.g. NEE after a
+// sphere step and NEE after a delta-tracking event) execute it together.
+//   1. traversal : medium entry (outside) or free flight (inside, unless the
+//                  conservative SDF ball already contains the whole flight)
+//   2. resolve   : escape / enter / leave / collide
+//   3. collision : sphere step (ST and r > r_min) or one delta-tracking event
+//   4. NEE       : shadow ray toward the point light
+// Returns -1 while the path lives, else its end code. `active` lanes only.
 template <class R, bool ST>
-SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st) {
+SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bool active) {
     const DevScene<R>& sc = a.sc;
-    if (p.obj < 0) {  // outside all media: find the next boundary (medium entry)
-        const RayK<R> ray = make_ray(p.x, p.w);
-        R t;
-        Hit h;
-        const R tmin = p.skip >= 0 ? sc.surf_eps : sc.t_min;
-        if (!intersect_nearest(sc, ray, tmin, Real<R>::kInf, p.skip, &t, &h)) {
-            p.L += sc.bg[p.c];
-            return kEndEscaped;
+    int end = -1;
+    // ---- 1. traversal
+    bool trace = false, inside = false;
+    R t_max = Real<R>::kInf, t_free = Real<R>::kInf;
+    const ObjK<R>* ob = nullptr;
+    if (active) {
+        inside = p.obj >= 0;
+        if (inside) {
+            ob = &sc.objs[p.obj];
+            const MediumK<R>& m = ob->med[p.c];
+            if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
+                const R u = p.rng.template uniform<R>();
+                if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
+                else t_free = -Real<R>::log_(R(1) - u) / m.sigma_t;
+            }
+            if (!p.r_valid) {
+                p.r_here = sdf_radius(*ob, p.x);
+                p.r_valid = true;
+            }
+            // A flight shorter than the conservative SDF radius cannot reach the
+            // boundary: skip the traversal (exact).
+            trace = !(t_free < p.r_here);
+            t_max = t_free;
+        } else {
+            trace = true;
         }
-        p.x = p.x + p.w * t;
-        p.obj = static_cast<int>(h.obj);
-        p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
-        p.r_valid = false;
     }
-    const ObjK<R>& ob = sc.objs[p.obj];
-    const MediumK<R>& m = ob.med[p.c];
-    // free flight (sample_free_path, optics.cpp:55-60)
-    R t_free;
-    if (m.sigma_t > R(0)) {
-        const R u = p.rng.template uniform<R>();
-        if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
-        else t_free = -Real<R>::log_(R(1) - u) / m.sigma_t;
-    } else {
-        t_free = Real<R>::kInf;
-    }
-    // A conservative SDF ball around x is surface-free: a flight shorter than its
-    // radius cannot reach the boundary, so the traversal is skipped (exact).
-    if (!p.r_valid) {
-        p.r_here = sdf_radius(ob, p.x);
-        p.r_valid = true;
-    }
-    bool left = false;
-    if (!(t_free < p.r_here)) {
+    bool hit = false;
+    R t_hit = R(0);
+    Hit h{0, 0};
+    if (trace) {
         const RayK<R> ray = make_ray(p.x, p.w);
-        R t;
-        Hit h;
-        const R tmin = p.skip >= 0 ? sc.surf_eps : sc.t_min;
-        if (intersect_nearest(sc, ray, tmin, t_free, p.skip, &t, &h)) {
-            p.x = p.x + p.w * t;
+        hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, &t_hit, &h);
+    }
+    // ---- 2. resolve
+    bool collide = false;
+    if (active) {
+        if (!inside) {
+            if (!hit) {
+                p.L += sc.bg[p.c];
+                end = kEndEscaped;
+            } else {  // medium entry (index-matched boundary)
+                p.x = p.x + p.w * t_hit;
+                p.obj = static_cast<int>(h.obj);
+                p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
+                p.r_valid = false;
+            }
+        } else if (hit) {  // leaves the medium
+            p.x = p.x + p.w * t_hit;
             p.obj = -1;
             p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
-            left = true;
+        } else {  // collision
+            p.skip = -1;
+            p.x = p.x + p.w * t_free;
+            p.r_valid = false;
+            if (p.seg >= (ST ? sc.cap_st : sc.cap_pt)) {
+                p.L = R(0);  // dropped
+                end = kEndCapped;
+            } else {
+                ++p.seg;
+                collide = true;
+            }
         }
     }
-    if (left) return -1;
-    p.skip = -1;
-    p.x = p.x + p.w * t_free;  // collision
-    p.r_valid = false;
-    const uint32_t cap = ST ? sc.cap_st : sc.cap_pt;
-    if (p.seg >= cap) {
-        p.L = R(0);  // dropped
-        return kEndCapped;
-    }
-    ++p.seg;
-    if (ST) {
-        p.r_here = sdf_radius(ob, p.x);
+    // ---- 3. collision
+    bool sphere = false, nee = false;
+    V3<R> nee_p, nee_w;
+    R nee_wt = R(1);
+    if (ST && collide) {
+        p.r_here = sdf_radius(*ob, p.x);
         p.r_valid = true;
-        if (p.r_here > m.r_min) {
-            ++st.sphere;
-            StepOut<R> o;
-            if (!sphere_step(m, p.w, p.x, p.r_here, a.nee != 0, p.rng, o, st.dc)) {
-                p.L = R(0);
-                return kEndError;
-            }
-            if (o.absorbed) return kEndAbsorbed;
-            if (a.nee) {
-                p.L += nee_term(sc, m, p.c, o.rep_pos, o.rep_dir, o.lambda);
-                ++st.shadow;
-            }
+        sphere = p.r_here > ob->med[p.c].r_min;
+    }
+    if (ST && sphere) {
+        ++st.sphere;
+        StepOut<R> o;
+        const MediumK<R>& m = ob->med[p.c];
+        if (!sphere_step(m, p.w, p.x, p.r_here, a.nee != 0, p.rng, o, st.dc)) {
+            p.L = R(0);
+            end = kEndError;
+        } else if (o.absorbed) {
+            end = kEndAbsorbed;
+        } else {
+            nee = a.nee != 0;
+            nee_p = o.rep_pos;
+            nee_w = o.rep_dir;
+            nee_wt = o.lambda;
             p.x = o.exit_pos;
             p.w = o.exit_dir;
             p.r_valid = false;
-            return -1;
         }
     }
-    // one delta-tracking event: Russian roulette by albedo, NEE, HG scatter
-    ++st.events;
-    if (!((p.rng.next() >> 11) < m.survive_below)) return kEndAbsorbed;  // u < phi, bit-exact
-    if (a.nee) {
-        p.L += nee_term(sc, m, p.c, p.x, p.w, R(1));
+    if (collide && !sphere) {  // delta-tracking event: roulette, NEE, HG scatter
+        ++st.events;
+        const MediumK<R>& m = ob->med[p.c];
+        if (!((p.rng.next() >> 11) < m.survive_below)) {  // u < phi, bit-exact
+            end = kEndAbsorbed;
+        } else {
+            nee = a.nee != 0;
+            nee_p = p.x;
+            nee_w = p.w;  // incoming direction (NEE draws no random numbers)
+            const R u1 = p.rng.template uniform<R>();
+            const R u2 = p.rng.template uniform<R>();
+            p.w = hg_sample(m.g, p.w, u1, u2);
+        }
+    }
+    // ---- 4. NEE
+    if (nee) {
+        p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt);
         ++st.shadow;
     }
-    const R u1 = p.rng.template uniform<R>();
-    const R u2 = p.rng.template uniform<R>();
-    p.w = hg_sample(m.g, p.w, u1, u2);
-    return -1;
+    return end;
 }
 
 template <class T>
@@ -234,19 +270,17 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
             }
         }
         if (!__any_sync(0xffffffffu, alive)) break;
-        if (alive) {
-            const int end = path_advance<R, ST>(a, p, st);
-            if (end >= 0) {
-                a.radiance[p.id] = p.L;
-                if (a.segments) a.segments[p.id] = p.seg;
-                ++st.paths;
-                st.seg += p.seg;
-                st.escaped += end == kEndEscaped;
-                st.absorbed += end == kEndAbsorbed;
-                st.capped += end == kEndCapped;
-                st.errors += end == kEndError;
-                alive = false;
-            }
+        const int end = path_advance<R, ST>(a, p, st, alive);
+        if (alive && end >= 0) {
+            a.radiance[p.id] = p.L;
+            if (a.segments) a.segments[p.id] = p.seg;
+            ++st.paths;
+            st.seg += p.seg;
+            st.escaped += end == kEndEscaped;
+            st.absorbed += end == kEndAbsorbed;
+            st.capped += end == kEndCapped;
+            st.errors += end == kEndError;
+            alive = false;
         }
     }
     unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,

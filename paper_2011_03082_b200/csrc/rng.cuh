@@ -58,4 +58,14 @@ SST_D float Rng::normal<float>() {
     return sqrtf(-2.0f * __logf(u1)) * c;
 }
 
+// n consecutive normal() draws (one out-of-line copy of Box-Muller for every
+// decoder instead of 22 inlined copies: the render kernel is I-cache bound).
+template <class R>
+__device__ __noinline__ uint64_t draw_normals(uint64_t s, R* out, int n) {
+    Rng r{s};
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) out[i] = r.normal<R>();
+    return r.s;
+}
+
 }  // namespace sstg

@@ -159,3 +159,21 @@ def test_image_matches_oracle_statistically(renderer, oracle, models_dir, ico3):
     assert (z > 3).mean() <= 0.015, (z > 3).mean()
     rmse = np.sqrt(np.mean((gm - om_) ** 2))
     assert rmse <= 1.5 * np.sqrt(np.mean(se ** 2)), rmse
+
+
+def test_async_pipelined_render_equals_sync(renderer, ico3):
+    """Asynchronous device-pointer calls (pipelined slots) give the same film and stats."""
+    torch = pytest.importorskip("torch")
+    from paper_2011_03082_b200 import ST
+    from paper_2011_03082_b200.scene import c1_scene
+    renderer.upload_scene(c1_scene(ico3, 40, 32))
+    ref, rst = renderer.render_film(ST, 12, seed=5)
+    n = 40 * 32 * 3
+    s = torch.zeros(n, dtype=torch.float64, device="cuda")
+    q = torch.zeros(n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    for a in range(0, 12, 3):
+        renderer.render_device(ST, 12, a, a + 3, 5, True, s.data_ptr(), q.data_ptr(), asynchronous=True)
+    st = renderer.read_stats()
+    assert st.paths == rst.paths and st.segments == rst.segments
+    assert np.allclose(s.cpu().numpy(), ref.sum, rtol=1e-12, atol=1e-15)

@@ -4,7 +4,7 @@ and the C oracle.
 
 Tolerances (written here, per the north star):
   FP64 parity mode: discrete outcomes and RNG consumption identical on every step;
-      continuous outputs within 1e-6 relative (+1e-9 absolute). CUDA libm and glibc
+      continuous outputs within 1e-6 relative (+5e-8 absolute). CUDA libm and glibc
       differ by ulps; the reference's exit-direction normal component
       sqrt(1 - a^2 - b^2) (scatter.cpp:124) is ill-conditioned after the unit-disk
       projection (1e-16 in -> 1e-8 out), everything else agrees to ~1e-15.
@@ -41,7 +41,7 @@ def test_f64_step_matches_reference_golden(renderer, golden, oracle):
     for k in ("absorbed", "n_events", "has_representative"):
         assert (out[k] == golden["step_out_" + k]).all(), k
     for k in CONT:
-        ok = rel_close(out[k], golden["step_out_" + k], 1e-6, 1e-9)
+        ok = rel_close(out[k], golden["step_out_" + k], 1e-6, 5e-8)
         assert ok.all(), (k, np.abs(out[k] - golden["step_out_" + k]).max())
     # identical RNG consumption (7 / 24 / 46 draws)
     for i in range(0, len(s0), 53):
@@ -83,7 +83,7 @@ def test_f32_and_f64_vs_oracle_on_fresh_inputs(renderer, oracle, models_dir):
     assert (b64["rng_state"] == ob["rng_state"]).all()
     assert (g64["n_events"] == oo["n_events"]).all() and (g64["absorbed"] == oo["absorbed"]).all()
     for k in CONT:
-        assert rel_close(g64[k], oo[k], 1e-6, 1e-9).all(), k
+        assert rel_close(g64[k], oo[k], 1e-6, 5e-8).all(), k
     b32 = copy_batch(b)
     g32 = _run(renderer, b32, "f32")
     agree = (g32["absorbed"] == oo["absorbed"])
