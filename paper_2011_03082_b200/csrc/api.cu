@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -103,11 +104,12 @@ struct sst_gpu_ctx {
     uint64_t model_gen = 0;
 
     bool scene = false;
-    uint64_t scene_bytes = 0;
+    uint64_t scene_bytes = 0, scene_bytes_grid = 0;
     uint32_t n_nodes = 0, n_tris = 0;
     std::vector<ObjectHost> objects;
     sst_scene_desc desc{};
-    DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64;
+    DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri;
+    uint32_t grid_res = 0;
     std::vector<DevBuf> sdf_dev;
     DevScene<float> sc32{};
     DevScene<double> sc64{};
@@ -119,7 +121,7 @@ struct sst_gpu_ctx {
     // Render pipeline: chunks of a render call rotate over kSlots streams so the
     // long-path tail of one persistent launch overlaps the next launch's bulk.
     // Film accumulations stay in chunk order (event chain) -> deterministic sums.
-    static constexpr int kSlots = 3;
+    static constexpr int kSlots = 5;
     struct Slot {
         cudaStream_t s = nullptr;
         DevBuf rad, work;
@@ -128,6 +130,7 @@ struct sst_gpu_ctx {
     int next_slot = 0;
     cudaEvent_t ev_start = nullptr, last_film = nullptr;
     bool timing_open = false;
+    int sphere_batch = 16;  // SST_SPHERE_BATCH overrides (tuning)
 };
 
 namespace {
@@ -300,6 +303,90 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     sc.surf_eps = std::is_same<R, double>::value ? static_cast<R>(1e-9) : static_cast<R>(2e-6 * ext);
     sc.cap_pt = d.max_pt_events ? d.max_pt_events : 1000000u;
     sc.cap_st = d.max_st_steps ? d.max_st_steps : 100000u;
+    const char* no_grid = std::getenv("SST_NO_LIGHT_GRID");
+    const bool use_grid = ctx->grid_res && !(no_grid && no_grid[0] == '1');
+    sc.grid_off = use_grid ? ctx->grid_off.as<uint32_t>() : nullptr;
+    sc.grid_tri = use_grid ? ctx->grid_tri.as<uint32_t>() : nullptr;
+    sc.grid_res = ctx->grid_res;
+}
+
+// Light-space culling grid for NEE shadow rays (see types.cuh DevScene::grid_*).
+// Per triangle: the cone from the light that contains it (axis = mean vertex
+// direction, half angle = max vertex angle + padding); cells overlap-tested on the
+// GPU in FP64 (count pass, host prefix sum, fill pass).
+void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
+                      const std::vector<std::array<std::array<double, 3>, 3>>& tv, const FlatBvh& bvh) {
+    const uint32_t n = bvh.n_tris;
+    const uint32_t res = n <= 4096 ? 128u : 256u;
+    const double pad = 2e-5;
+    std::vector<double> caps(6ull * n);
+    for (uint32_t k = 0; k < n; ++k) {
+        const auto& t = tv[bvh.order[k]];
+        double dir[3][3], ax[3] = {0, 0, 0};
+        for (int c = 0; c < 3; ++c) {
+            double v[3], l = 0;
+            for (int a = 0; a < 3; ++a) {
+                v[a] = t[c][a] - d->light_position[a];
+                l += v[a] * v[a];
+            }
+            l = std::sqrt(l);
+            for (int a = 0; a < 3; ++a) {
+                dir[c][a] = l > 0 ? v[a] / l : 0.0;
+                ax[a] += dir[c][a];
+            }
+        }
+        const double al = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+        double alpha = 3.14159265358979323846;
+        if (al > 1e-6) {
+            for (int a = 0; a < 3; ++a) ax[a] /= al;
+            double mind = 1.0;
+            for (int c = 0; c < 3; ++c)
+                mind = std::fmin(mind, ax[0] * dir[c][0] + ax[1] * dir[c][1] + ax[2] * dir[c][2]);
+            alpha = std::acos(std::fmax(-1.0, std::fmin(1.0, mind))) + pad;
+            // a cap contains the geodesic triangle only below a hemisphere
+            if (alpha > 1.5) alpha = 3.14159265358979323846;
+        }
+        caps[6ull * k] = ax[0];
+        caps[6ull * k + 1] = ax[1];
+        caps[6ull * k + 2] = ax[2];
+        caps[6ull * k + 3] = alpha;
+        caps[6ull * k + 4] = std::cos(alpha);
+        caps[6ull * k + 5] = std::sin(alpha);
+    }
+    const uint32_t ncell = 6u * res * res;
+    DevBuf dcaps, dcounts;
+    dcaps.reserve(caps.size() * sizeof(double));
+    dcounts.reserve(ncell * sizeof(uint32_t));
+    CK(cudaMemcpyAsync(dcaps.p, caps.data(), caps.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    LightGridArgs a{};
+    a.caps = dcaps.as<double>();
+    a.n_tris = n;
+    a.res = res;
+    a.eps = pad;
+    a.counts = dcounts.as<uint32_t>();
+    a.fill = 0;
+    CK(launch_light_grid(a, ctx->stream));
+    std::vector<uint32_t> counts(ncell), offsets(ncell + 1);
+    CK(cudaMemcpyAsync(counts.data(), dcounts.p, ncell * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    uint64_t total = 0;
+    for (uint32_t c = 0; c < ncell; ++c) {
+        offsets[c] = static_cast<uint32_t>(total);
+        total += counts[c];
+    }
+    offsets[ncell] = static_cast<uint32_t>(total);
+    if (total >= (1ull << 31)) throw InvalidArgument("light grid too large");
+    ctx->grid_off.reserve(offsets.size() * sizeof(uint32_t));
+    ctx->grid_tri.reserve(std::max<uint64_t>(total, 1) * sizeof(uint32_t));
+    CK(cudaMemcpyAsync(ctx->grid_off.p, offsets.data(), offsets.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    a.fill = 1;
+    a.offsets = ctx->grid_off.as<uint32_t>();
+    a.lists = ctx->grid_tri.as<uint32_t>();
+    CK(launch_light_grid(a, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->grid_res = res;
+    ctx->scene_bytes_grid = offsets.size() * sizeof(uint32_t) + total * sizeof(uint32_t);
 }
 
 void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
@@ -357,6 +444,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         }
     }
     const FlatBvh bvh = build_bvh(tv, tobj);
+    build_light_grid(ctx, d, tv, bvh);
     // upload
     ctx->objects = std::move(objs);
     ctx->desc = *d;
@@ -378,6 +466,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     }
     uint64_t bytes = bvh.nodes_f32.size() + bvh.tris_f32.size() + bvh.nodes_f64.size() + bvh.tris_f64.size();
     for (const auto& o : ctx->objects) bytes += o.sdf.size() * sizeof(float);
+    bytes += ctx->scene_bytes_grid;
     bytes += ctx->objects.size() * (sizeof(ObjK<float>) + sizeof(ObjK<double>));
     ctx->scene_bytes = bytes;
     ctx->n_nodes = bvh.n_nodes;
@@ -415,6 +504,7 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.segments = segments;
     a.work = work;
     a.stats = ctx->stats.as<unsigned long long>();
+    a.sphere_batch = ctx->sphere_batch;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
     else CK(f64::launch_trace(a, st, explicit_keys, stream));
@@ -612,6 +702,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         ctx->device = device;
         CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->serial = ++g_serial;
+        if (const char* e = std::getenv("SST_SPHERE_BATCH")) ctx->sphere_batch = std::max(1, std::atoi(e));
         *out = ctx.release();
     });
 }
@@ -625,7 +716,7 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         auto it = g_const_owner.find(ctx->device);
         if (it != g_const_owner.end() && it->second.first == ctx) g_const_owner.erase(it);
     }
-    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64,
+    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri,
                       &ctx->radiance, &ctx->segments, &ctx->work, &ctx->stats, &ctx->error, &ctx->film_sum,
                       &ctx->film_sq, &ctx->keys_pix, &ctx->keys_smp, &ctx->keys_ch, &ctx->step_in, &ctx->step_out})
         b->release();

@@ -267,4 +267,54 @@ SST_D R optical_depth(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_ma
     }
 }
 
+// ---------------------------------------------------------------- light grid
+// Cube-map cell of a direction (faces +x,-x,+y,-y,+z,-z; (s,t) = minor/|major|).
+// Shared by the device lookup and the build kernel (cell centres).
+template <class R>
+SST_HD uint32_t cube_cell(R x, R y, R z, uint32_t res) {
+    const R ax = x < R(0) ? -x : x, ay = y < R(0) ? -y : y, az = z < R(0) ? -z : z;
+    uint32_t face;
+    R s, t, m;
+    if (ax >= ay && ax >= az) {
+        face = x > R(0) ? 0u : 1u;
+        m = ax; s = y; t = z;
+    } else if (ay >= az) {
+        face = y > R(0) ? 2u : 3u;
+        m = ay; s = x; t = z;
+    } else {
+        face = z > R(0) ? 4u : 5u;
+        m = az; s = x; t = y;
+    }
+    const R fs = (s / m + R(1)) * R(0.5) * static_cast<R>(res);
+    const R ft = (t / m + R(1)) * R(0.5) * static_cast<R>(res);
+    int i = static_cast<int>(fs), j = static_cast<int>(ft);
+    i = i < 0 ? 0 : (i >= static_cast<int>(res) ? static_cast<int>(res) - 1 : i);
+    j = j < 0 ? 0 : (j >= static_cast<int>(res) ? static_cast<int>(res) - 1 : j);
+    return (face * res + static_cast<uint32_t>(j)) * res + static_cast<uint32_t>(i);
+}
+
+// Optical depth along [0, t_max] from p toward the point light using the light
+// grid: the same Moller-Trumbore tests as the BVH path on a conservative
+// candidate set (every triangle whose footprint seen from the light overlaps the
+// cell of this direction), so the hit set is identical -- without pointer chasing.
+template <class R>
+SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int c) {
+    const uint32_t cell = cube_cell<R>(-ray.d.x, -ray.d.y, -ray.d.z, sc.grid_res);
+    const uint32_t b = __ldg(sc.grid_off + cell), e = __ldg(sc.grid_off + cell + 1);
+    R tau = R(0);
+    for (uint32_t k = b; k < e; ++k) {
+        const uint32_t i = __ldg(sc.grid_tri + k);
+        V3<R> v0, e1, e2;
+        uint32_t obj, id;
+        load_tri<R>(sc.tris, i, v0, e1, e2, obj, id);
+        R det;
+        const R t = ray_tri(ray, v0, e1, e2, t_min, t_max, &det);
+        if (t >= R(0)) {
+            const R sig = sc.objs[obj].med[c].sigma_t;
+            tau += det < R(0) ? sig * t : -(sig * t);
+        }
+    }
+    return tau;
+}
+
 }  // namespace sstg

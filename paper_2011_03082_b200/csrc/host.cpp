@@ -400,6 +400,7 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
     FlatBvh out;
     out.n_nodes = static_cast<uint32_t>(bld.nodes.size());
     out.n_tris = n;
+    out.order = bld.order;
     std::vector<NodeF> nf(out.n_nodes);
     std::vector<NodeD> nd(out.n_nodes);
     for (uint32_t i = 0; i < out.n_nodes; ++i) {

@@ -53,7 +53,7 @@ SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<
     const R d = Real<R>::sqrt_(d2);
     const V3<R> wl = to_l / d;
     const RayK<R> ray = make_ray(p, wl);
-    const R tau = optical_depth(sc, ray, sc.t_min, d, c);
+    const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c) : optical_depth(sc, ray, sc.t_min, d, c);
     const R phase = hg_eval(m.g, dot(w, wl));
     return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) / d2;
 }
@@ -70,6 +70,8 @@ struct PathLocal {
     int skip;       // triangle to ignore on the next traversal (FP32 surface start)
     uint8_t c;
     bool r_valid;
+    bool pending;   // a sphere step is requested and waits for its warp batch
+    uint16_t waited;
 };
 
 struct LaneStats {
@@ -109,6 +111,8 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
     p.skip = -1;
     p.c = static_cast<uint8_t>(c);
     p.r_valid = false;
+    p.pending = false;
+    p.waited = 0;
 }
 
 // One iteration of the path loop, written as a fixed sequence of phases in which
@@ -119,21 +123,24 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
 //   1. traversal : medium entry (outside) or free flight (inside, unless the
 //                  conservative SDF ball already contains the whole flight)
 //   2. resolve   : escape / enter / leave / collide
-//   3. collision : sphere step (ST and r > r_min) or one delta-tracking event
-//   4. NEE       : shadow ray toward the point light
-// Returns -1 while the path lives, else its end code. `active` lanes only.
+//   3. collision : one delta-tracking event, or a sphere-step REQUEST (ST, r > r_min)
+//   4. sphere    : warp-regrouped: requested sphere steps wait until at least
+//                  `sphere_batch` lanes (or every live lane) want one, so the
+//                  ~3k-instruction CVAE step runs on a mostly full warp
+//   5. NEE       : shadow ray toward the point light
+// Returns -1 while the path lives, else its end code. `alive` lanes only.
 template <class R, bool ST>
-SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bool active) {
+SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bool alive) {
     const DevScene<R>& sc = a.sc;
     int end = -1;
+    const bool active = alive && !p.pending;  // lanes waiting for a sphere batch sit out 1-3
     // ---- 1. traversal
     bool trace = false, inside = false;
     R t_max = Real<R>::kInf, t_free = Real<R>::kInf;
-    const ObjK<R>* ob = nullptr;
+    const ObjK<R>* ob = alive && p.obj >= 0 ? &sc.objs[p.obj] : nullptr;
     if (active) {
         inside = p.obj >= 0;
         if (inside) {
-            ob = &sc.objs[p.obj];
             const MediumK<R>& m = ob->med[p.c];
             if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
                 const R u = p.rng.template uniform<R>();
@@ -190,34 +197,20 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
         }
     }
     // ---- 3. collision
-    bool sphere = false, nee = false;
+    bool nee = false;
     V3<R> nee_p, nee_w;
     R nee_wt = R(1);
+    bool event = collide;
     if (ST && collide) {
         p.r_here = sdf_radius(*ob, p.x);
         p.r_valid = true;
-        sphere = p.r_here > ob->med[p.c].r_min;
-    }
-    if (ST && sphere) {
-        ++st.sphere;
-        StepOut<R> o;
-        const MediumK<R>& m = ob->med[p.c];
-        if (!sphere_step(m, p.w, p.x, p.r_here, a.nee != 0, p.rng, o, st.dc)) {
-            p.L = R(0);
-            end = kEndError;
-        } else if (o.absorbed) {
-            end = kEndAbsorbed;
-        } else {
-            nee = a.nee != 0;
-            nee_p = o.rep_pos;
-            nee_w = o.rep_dir;
-            nee_wt = o.lambda;
-            p.x = o.exit_pos;
-            p.w = o.exit_dir;
-            p.r_valid = false;
+        if (p.r_here > ob->med[p.c].r_min) {
+            p.pending = true;
+            p.waited = 0;
+            event = false;
         }
     }
-    if (collide && !sphere) {  // delta-tracking event: roulette, NEE, HG scatter
+    if (event) {  // delta-tracking event: roulette, NEE, HG scatter
         ++st.events;
         const MediumK<R>& m = ob->med[p.c];
         if (!((p.rng.next() >> 11) < m.survive_below)) {  // u < phi, bit-exact
@@ -231,7 +224,40 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             p.w = hg_sample(m.g, p.w, u1, u2);
         }
     }
-    // ---- 4. NEE
+    // ---- 4. sphere steps, regrouped per warp
+    if (ST) {
+        const unsigned pend = __ballot_sync(0xffffffffu, alive && p.pending);
+        if (pend) {
+            const unsigned live = __ballot_sync(0xffffffffu, alive && end < 0);
+            const bool starving = __any_sync(0xffffffffu, alive && p.pending && p.waited >= 64);
+            const bool go = __popc(pend) >= a.sphere_batch || (live & ~pend) == 0u || starving;
+            if (alive && p.pending) {
+                if (!go) {
+                    ++p.waited;
+                } else {
+                    p.pending = false;
+                    ++st.sphere;
+                    StepOut<R> o;
+                    const MediumK<R>& m = ob->med[p.c];
+                    if (!sphere_step(m, p.w, p.x, p.r_here, a.nee != 0, p.rng, o, st.dc)) {
+                        p.L = R(0);
+                        end = kEndError;
+                    } else if (o.absorbed) {
+                        end = kEndAbsorbed;
+                    } else {
+                        nee = a.nee != 0;
+                        nee_p = o.rep_pos;
+                        nee_w = o.rep_dir;
+                        nee_wt = o.lambda;
+                        p.x = o.exit_pos;
+                        p.w = o.exit_dir;
+                        p.r_valid = false;
+                    }
+                }
+            }
+        }
+    }
+    // ---- 5. NEE
     if (nee) {
         p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt);
         ++st.shadow;

@@ -133,7 +133,76 @@ __global__ void __launch_bounds__(128) k_sdf_build(SdfBuildArgs a) {
     a.values[v] = static_cast<float>(inside ? -cons : cons);
 }
 
+constexpr int kGridTile = 256;
+
+// Light grid build: one cube-map cell per thread; a triangle belongs to the cell
+// when their angular caps overlap: angle(c, a) <= r_cell + alpha_tri, tested as
+// dot(c, a) >= cos(r)cos(alpha) - sin(r)sin(alpha) (alpha already padded).
+__global__ void __launch_bounds__(128) k_light_grid(LightGridArgs a) {
+    __shared__ double tile[kGridTile * 6];
+    const uint32_t ncell = 6u * a.res * a.res;
+    const uint32_t cell = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = cell < ncell;
+    double cx = 0, cy = 0, cz = 1, cr = 1, sr = 0, r = 0;
+    if (active) {
+        const uint32_t face = cell / (a.res * a.res), rem = cell % (a.res * a.res);
+        const uint32_t j = rem / a.res, i = rem % a.res;
+        auto dir = [&](double s, double t, double* o) {
+            double v[3];
+            switch (face) {
+                case 0: v[0] = 1; v[1] = s; v[2] = t; break;
+                case 1: v[0] = -1; v[1] = s; v[2] = t; break;
+                case 2: v[0] = s; v[1] = 1; v[2] = t; break;
+                case 3: v[0] = s; v[1] = -1; v[2] = t; break;
+                case 4: v[0] = s; v[1] = t; v[2] = 1; break;
+                default: v[0] = s; v[1] = t; v[2] = -1; break;
+            }
+            const double l = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            o[0] = v[0] / l; o[1] = v[1] / l; o[2] = v[2] / l;
+        };
+        const double h = 1.0 / a.res;
+        const double sc = (i + 0.5) * 2.0 * h - 1.0, tc = (j + 0.5) * 2.0 * h - 1.0;
+        double c[3];
+        dir(sc, tc, c);
+        double mind = 1.0;
+        for (int k = 0; k < 4; ++k) {
+            double q[3];
+            dir(sc + ((k & 1) ? h : -h), tc + ((k & 2) ? h : -h), q);
+            mind = fmin(mind, c[0] * q[0] + c[1] * q[1] + c[2] * q[2]);
+        }
+        r = acos(fmax(-1.0, fmin(1.0, mind))) + a.eps;
+        cx = c[0]; cy = c[1]; cz = c[2];
+        cr = cos(r); sr = sin(r);
+    }
+    const uint32_t base_out = (a.fill && active) ? a.offsets[cell] : 0;
+    uint32_t count = 0;
+    for (uint32_t base = 0; base < a.n_tris; base += kGridTile) {
+        const uint32_t n = min(static_cast<uint32_t>(kGridTile), a.n_tris - base);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < n * 6; k += blockDim.x) tile[k] = a.caps[base * 6ull + k];
+        __syncthreads();
+        if (!active) continue;
+        for (uint32_t t = 0; t < n; ++t) {
+            const double* q = tile + 6 * t;  // axis xyz, alpha, cos alpha, sin alpha
+            bool hit;
+            if (r + q[3] >= 3.14159265358979323846) hit = true;
+            else hit = cx * q[0] + cy * q[1] + cz * q[2] >= cr * q[4] - sr * q[5];
+            if (hit) {
+                if (a.fill) a.lists[base_out + count] = base + t;
+                ++count;
+            }
+        }
+    }
+    if (active && !a.fill) a.counts[cell] = count;
+}
+
 }  // namespace
+
+cudaError_t launch_light_grid(const LightGridArgs& a, cudaStream_t s) {
+    const uint32_t ncell = 6u * a.res * a.res;
+    k_light_grid<<<(ncell + 127) / 128, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sdf_build(const SdfBuildArgs& a, cudaStream_t s) {
     const uint64_t nvox = static_cast<uint64_t>(a.dims[0]) * a.dims[1] * a.dims[2];

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(128) k_step_batch(StepBatchArgs a) {
 // ---------------------------------------------------------------------------
 // Persistent path-tracing megakernel (PT or ST; render ids or explicit keys).
 template <bool ST, bool EXPLICIT>
-__global__ void __launch_bounds__(kTraceBlock) k_trace(TraceArgs<R> a) {
+__global__ void __launch_bounds__(kTraceBlock, 16) k_trace(TraceArgs<R> a) {
     trace_persistent<R, ST, EXPLICIT>(a);
 }
 

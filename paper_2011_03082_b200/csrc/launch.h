@@ -7,7 +7,7 @@
 
 namespace sstg {
 
-constexpr int kTraceBlock = 256;
+constexpr int kTraceBlock = 32;  // one warp per block: a long-path tail strands one warp, not a block
 
 #define SST_DECLARE_LAUNCHERS(NS, REAL)                                                          \
     namespace NS {                                                                              \
@@ -36,5 +36,19 @@ struct SdfBuildArgs {
     float* values;
 };
 cudaError_t launch_sdf_build(const SdfBuildArgs& a, cudaStream_t s);
+
+// Light-space culling grid build (kernels_f64.cu). caps: per triangle
+// {axis.x, axis.y, axis.z, half_angle} of the cone (from the light) that contains it.
+struct LightGridArgs {
+    const double* caps;
+    uint32_t n_tris;
+    uint32_t res;         // cells per cube face edge
+    double eps;           // angular padding (rad)
+    uint32_t* counts;     // pass 0: [6 res^2] list lengths
+    const uint32_t* offsets;  // pass 1: [6 res^2 + 1]
+    uint32_t* lists;      // pass 1
+    int fill;
+};
+cudaError_t launch_light_grid(const LightGridArgs& a, cudaStream_t s);
 
 }  // namespace sstg

@@ -72,6 +72,12 @@ struct DevScene {
     uint32_t width, height;
     R t_min, surf_eps;
     uint32_t cap_pt, cap_st;
+    // Light-space culling grid for NEE shadow rays: a cube map over directions
+    // from the point light; cell c lists (leaf-order) triangles whose angular
+    // footprint overlaps it: grid_tri[grid_off[c] .. grid_off[c+1]). Null = use the BVH.
+    const uint32_t* grid_off;
+    const uint32_t* grid_tri;
+    uint32_t grid_res;
 };
 
 struct Hit {
@@ -101,6 +107,7 @@ struct TraceArgs {
     uint32_t* segments;      // [n_paths] or null
     unsigned long long* work;   // path-id counter
     unsigned long long* stats;  // [kStCount]
+    int sphere_batch;           // warp regrouping threshold for sphere steps (lanes)
 };
 
 // Arguments of the sphere-step batch kernel (C ABI sst_gpu_sphere_step_batch).
