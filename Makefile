@@ -11,8 +11,13 @@ LIB = paper_2011_03082_b200/libsst_gpu.so
 PEAKLIB = paper_2011_03082_b200/libsst_peak.so
 HDRS = $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/sst_gpu.h include/sst_host.h
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle tools clean
+all: lib oracle tools
+
+tools: tools/sst_render
+
+tools/sst_render: tools/sst_render.cpp include/sst_b200.hpp $(LIB)
+	$(CXX) -O2 -std=c++17 -Wall -Iinclude -o $@ $< -Lpaper_2011_03082_b200 -lsst_gpu -Wl,-rpath,'$$ORIGIN/../paper_2011_03082_b200'
 
 lib: $(LIB) $(PEAKLIB)
 
@@ -43,5 +48,5 @@ oracle:
 	$(MAKE) -C oracle all
 
 clean:
-	rm -rf $(BUILD) $(LIB) $(PEAKLIB)
+	rm -rf $(BUILD) $(LIB) $(PEAKLIB) tools/sst_render
 	$(MAKE) -C oracle clean

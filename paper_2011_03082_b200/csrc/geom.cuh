@@ -166,20 +166,36 @@ constexpr int kStack = 48;
 
 // Nearest hit with t in (t_min, t_max), ignoring triangle `skip` (FP32
 // self-intersection guard for rays leaving a surface; -1 = none).
+//
+// While-while traversal with postponed leaves (Aila & Laine 2009): a lane that
+// reaches a leaf parks it and keeps descending interior nodes until every lane
+// of the (active) warp holds a leaf, then the leaves are intersected together --
+// interior-node work and triangle work each run on mostly full warps.
+constexpr int kDone = 0x7fffffff;
+
 template <class R>
 SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
                              R* t_hit, Hit* hit) {
     int stack_n[kStack];
     R stack_t[kStack];
     int sp = 0;
-    int cur = 0;
+    int node = 0;   // interior (>= 0), leaf (< 0) or kDone
+    int leaf = 0;   // postponed leaf (< 0) or 0 = none
     R t_best = t_max;
     bool found = false;
-    for (;;) {
-        if (cur >= 0) {
+    auto pop = [&]() -> int {
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp] <= t_best) return stack_n[sp];
+        }
+        return kDone;
+    };
+    while (node != kDone || leaf != 0) {
+        // interior nodes until this lane holds a leaf and all lanes do
+        while (node != kDone && node >= 0) {
             R b[12];
             int c0, c1;
-            load_node<R>(sc.nodes, cur, b, c0, c1);
+            load_node<R>(sc.nodes, node, b, c0, c1);
             R t0, t1;
             const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_best, &t0);
             const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_best, &t1);
@@ -188,40 +204,46 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
                 stack_n[sp] = first0 ? c1 : c0;
                 stack_t[sp] = first0 ? t1 : t0;
                 ++sp;
-                cur = first0 ? c0 : c1;
-                continue;
+                node = first0 ? c0 : c1;
+            } else if (h0) {
+                node = c0;
+            } else if (h1) {
+                node = c1;
+            } else {
+                node = pop();
             }
-            if (h0) { cur = c0; continue; }
-            if (h1) { cur = c1; continue; }
-        } else {
-            const uint32_t leaf = static_cast<uint32_t>(~cur);
-            const uint32_t first = leaf >> 3, count = leaf & 7u;
+            if (node < 0 && leaf == 0) {  // park the leaf, keep descending
+                leaf = node;
+                node = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == 0)) break;
+        }
+        // intersect the parked leaf (and any leaf the traversal is sitting on)
+        while (leaf < 0) {
+            const uint32_t code = static_cast<uint32_t>(~leaf);
+            const uint32_t first = code >> 3, count = code & 7u;
             for (uint32_t i = first; i < first + count; ++i) {
                 V3<R> v0, e1, e2;
                 uint32_t obj, id;
                 load_tri<R>(sc.tris, i, v0, e1, e2, obj, id);
-                if (static_cast<int>(id) == skip) continue;
                 R det;
                 const R t = ray_tri(ray, v0, e1, e2, t_min, t_best, &det);
-                if (t >= R(0)) {
+                if (t >= R(0) && static_cast<int>(id) != skip) {
                     t_best = t;
                     hit->tri = id;
                     hit->obj = obj;
                     found = true;
                 }
             }
-        }
-        // pop the next node still in front of the best hit
-        for (;;) {
-            if (sp == 0) {
-                *t_hit = t_best;
-                return found;
+            leaf = 0;
+            if (node != kDone && node < 0) {
+                leaf = node;
+                node = pop();
             }
-            --sp;
-            if (stack_t[sp] <= t_best) break;
         }
-        cur = stack_n[sp];
     }
+    *t_hit = t_best;
+    return found;
 }
 
 // Optical depth along [0, t_max] from a point inside a medium (order-free signed sum;

@@ -104,3 +104,16 @@ def test_error_codes_map_to_reference_exception_classes():
     assert issubclass(abi.DomainError, ValueError)
     with pytest.raises(abi.InvalidArgument):
         abi.check(abi.lib().sst_gpu_set_precision(None, 0))
+
+
+def test_cpp_header_mirror_and_cli_build():
+    """include/sst_b200.hpp compiles against the C ABI; the CLI reports usage / no-GPU codes."""
+    import shutil
+    import subprocess
+    cli = os.path.join(ROOT, "tools", "sst_render")
+    r = subprocess.run(["make", "-C", ROOT, "tools"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([cli, "--bogus"], capture_output=True).returncode == 1  # usage (SPEC.md:674)
+    if not shutil.which("nvidia-smi"):
+        res = subprocess.run([cli, "--scene", "c1"], capture_output=True, text=True, cwd=ROOT)
+        assert res.returncode == 3 and "no CPU fallback" in res.stderr

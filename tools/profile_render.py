@@ -20,11 +20,14 @@ ap.add_argument("--spp", type=int, default=2)
 ap.add_argument("--integrator", default="st")
 ap.add_argument("--nee", type=int, default=1)
 ap.add_argument("--precision", default="f32")
+ap.add_argument("--cap", type=int, default=0, help="max ST steps / PT events (0 = reference caps); profiling only")
+ap.add_argument("--chunks", type=int, default=1)
 a = ap.parse_args()
 r = sb.Renderer(0, a.precision)
 r.load_models_dir(os.path.join(ROOT, "tests", "golden", "models"))
 mesh = sb.make_icosphere(3, 1.0)
 scene = sb.c5_scene(mesh) if a.scene == "c5" else sb.c1_scene(mesh)
+scene.max_st_steps = scene.max_pt_events = a.cap
 r.upload_scene(scene)
 integ = sb.ST if a.integrator == "st" else sb.PT
 for i in range(2):
