@@ -226,6 +226,9 @@ typedef struct {
     uint64_t decodes_length, decodes_path, decodes_event;
     uint64_t absorbed, escaped, capped, errors;
     uint64_t shadow_rays;
+    /* work counters: nearest-hit traversals, BVH interior nodes visited, triangle
+     * tests (nearest + shadow), live-lane loop iterations, warp loop iterations */
+    uint64_t traversals, node_visits, triangle_tests, lane_iterations, warp_iterations;
     double device_ms;        /* kernel time of the render call */
 } sst_path_stats;
 

@@ -83,7 +83,9 @@ class PathStats(C.Structure):
     _fields_ = [("paths", U64), ("segments", U64), ("sphere_steps", U64), ("pt_events", U64),
                 ("decodes_length", U64), ("decodes_path", U64), ("decodes_event", U64),
                 ("absorbed", U64), ("escaped", U64), ("capped", U64), ("errors", U64),
-                ("shadow_rays", U64), ("device_ms", D)]
+                ("shadow_rays", U64), ("traversals", U64), ("node_visits", U64),
+                ("triangle_tests", U64), ("lane_iterations", U64), ("warp_iterations", U64),
+                ("device_ms", D)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -319,7 +319,7 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
     const uint32_t n = bvh.n_tris;
     const uint32_t res = n <= 4096 ? 128u : 256u;
     const double pad = 2e-5;
-    std::vector<double> caps(6ull * n);
+    std::vector<double> caps(static_cast<size_t>(kCapStride) * n);
     for (uint32_t k = 0; k < n; ++k) {
         const auto& t = tv[bvh.order[k]];
         double dir[3][3], ax[3] = {0, 0, 0};
@@ -346,12 +346,15 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
             // a cap contains the geodesic triangle only below a hemisphere
             if (alpha > 1.5) alpha = 3.14159265358979323846;
         }
-        caps[6ull * k] = ax[0];
-        caps[6ull * k + 1] = ax[1];
-        caps[6ull * k + 2] = ax[2];
-        caps[6ull * k + 3] = alpha;
-        caps[6ull * k + 4] = std::cos(alpha);
-        caps[6ull * k + 5] = std::sin(alpha);
+        double* q = caps.data() + static_cast<size_t>(kCapStride) * k;
+        q[0] = ax[0];
+        q[1] = ax[1];
+        q[2] = ax[2];
+        q[3] = alpha;
+        q[4] = std::cos(alpha);
+        q[5] = std::sin(alpha);
+        for (int c = 0; c < 3; ++c)
+            for (int a = 0; a < 3; ++a) q[6 + 3 * c + a] = dir[c][a];
     }
     const uint32_t ncell = 6u * res * res;
     DevBuf dcaps, dcounts;
@@ -534,6 +537,11 @@ void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
     out->escaped += v[kStEscaped];
     out->capped += v[kStCapped];
     out->shadow_rays += v[kStShadow];
+    out->traversals += v[kStTraversals];
+    out->node_visits += v[kStNodes];
+    out->triangle_tests += v[kStTriTests];
+    out->lane_iterations += v[kStLaneIters];
+    out->warp_iterations += v[kStWarpIters];
 }
 
 void check_render_ready(sst_gpu_ctx* ctx, int integrator) {
@@ -902,6 +910,9 @@ int sst_gpu_sphere_step_batch(sst_gpu_ctx* ctx, uint64_t n, const sst_step_in* i
 int sst_gpu_upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* scene) {
     return guarded([&] {
         require_device(ctx);
+        // in-flight asynchronous renders read the scene buffers: drain them first
+        join_slots(ctx);
+        CK(cudaStreamSynchronize(ctx->stream));
         upload_scene(ctx, scene);
     });
 }

@@ -175,7 +175,7 @@ constexpr int kDone = 0x7fffffff;
 
 template <class R>
 SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
-                             R* t_hit, Hit* hit) {
+                             R* t_hit, Hit* hit, uint64_t& n_nodes, uint64_t& n_tris) {
     int stack_n[kStack];
     R stack_t[kStack];
     int sp = 0;
@@ -196,6 +196,7 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
             R b[12];
             int c0, c1;
             load_node<R>(sc.nodes, node, b, c0, c1);
+            ++n_nodes;
             R t0, t1;
             const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_best, &t0);
             const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_best, &t1);
@@ -222,6 +223,7 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
         while (leaf < 0) {
             const uint32_t code = static_cast<uint32_t>(~leaf);
             const uint32_t first = code >> 3, count = code & 7u;
+            n_tris += count;
             for (uint32_t i = first; i < first + count; ++i) {
                 V3<R> v0, e1, e2;
                 uint32_t obj, id;
@@ -320,9 +322,11 @@ SST_HD uint32_t cube_cell(R x, R y, R z, uint32_t res) {
 // candidate set (every triangle whose footprint seen from the light overlaps the
 // cell of this direction), so the hit set is identical -- without pointer chasing.
 template <class R>
-SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int c) {
+SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int c,
+                           uint64_t& n_tris) {
     const uint32_t cell = cube_cell<R>(-ray.d.x, -ray.d.y, -ray.d.z, sc.grid_res);
     const uint32_t b = __ldg(sc.grid_off + cell), e = __ldg(sc.grid_off + cell + 1);
+    n_tris += e - b;
     R tau = R(0);
     for (uint32_t k = b; k < e; ++k) {
         const uint32_t i = __ldg(sc.grid_tri + k);

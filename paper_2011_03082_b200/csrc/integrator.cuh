@@ -47,13 +47,15 @@ SST_D R hg_eval(R g, R c) {
 // NEE toward the point light from p (in object obj, channel c) with incoming w:
 // weight * Phi * hg(g, w.wl) * exp(-tau) / d^2.
 template <class R>
-SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<R> w, R weight) {
+SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<R> w, R weight,
+                 uint64_t& tri_tests) {
     const V3<R> to_l = sc.light - p;
     const R d2 = dot(to_l, to_l);
     const R d = Real<R>::sqrt_(d2);
     const V3<R> wl = to_l / d;
     const RayK<R> ray = make_ray(p, wl);
-    const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c) : optical_depth(sc, ray, sc.t_min, d, c);
+    const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c, tri_tests)
+                              : optical_depth(sc, ray, sc.t_min, d, c);
     const R phase = hg_eval(m.g, dot(w, wl));
     return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) / d2;
 }
@@ -77,6 +79,7 @@ struct PathLocal {
 struct LaneStats {
     uint32_t paths = 0, absorbed = 0, escaped = 0, capped = 0, errors = 0;
     uint64_t seg = 0, sphere = 0, events = 0, shadow = 0;
+    uint64_t traversals = 0, nodes = 0, tris = 0, lane_iters = 0, warp_iters = 0;
     DecodeCount dc;
 };
 
@@ -164,7 +167,9 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     Hit h{0, 0};
     if (trace) {
         const RayK<R> ray = make_ray(p.x, p.w);
-        hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, &t_hit, &h);
+        hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, &t_hit, &h,
+                                st.nodes, st.tris);
+        ++st.traversals;
     }
     // ---- 2. resolve
     bool collide = false;
@@ -259,7 +264,7 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     }
     // ---- 5. NEE
     if (nee) {
-        p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt);
+        p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt, st.tris);
         ++st.shadow;
     }
     return end;
@@ -296,6 +301,8 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
             }
         }
         if (!__any_sync(0xffffffffu, alive)) break;
+        st.lane_iters += alive;
+        st.warp_iters += lane == 0;
         const int end = path_advance<R, ST>(a, p, st, alive);
         if (alive && end >= 0) {
             a.radiance[p.id] = p.L;
@@ -310,7 +317,8 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
         }
     }
     unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
-                                      st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow};
+                                      st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow,
+                                      st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters};
 #pragma unroll
     for (int k = 0; k < kStCount; ++k) {
         const unsigned long long s = warp_sum(v[k]);

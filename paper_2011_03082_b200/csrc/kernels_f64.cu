@@ -133,19 +133,59 @@ __global__ void __launch_bounds__(128) k_sdf_build(SdfBuildArgs a) {
     a.values[v] = static_cast<float>(inside ? -cons : cons);
 }
 
-constexpr int kGridTile = 256;
+constexpr int kGridTile = 128;
 
-// Light grid build: one cube-map cell per thread; a triangle belongs to the cell
-// when their angular caps overlap: angle(c, a) <= r_cell + alpha_tri, tested as
-// dot(c, a) >= cos(r)cos(alpha) - sin(r)sin(alpha) (alpha already padded).
+// Exact test of a (projected) triangle against a cube-map cell. Directions are
+// projected gnomonically onto the cell's face plane (great circles -> straight
+// lines), so the spherical triangle becomes a 2D triangle and the cell a square:
+// separating-axis test with padding. Returns -1 when a vertex is not strictly in
+// front of the face (caller keeps the cone result).
+__device__ int tri_cell_overlap(const double* q, int face, double s0, double s1, double t0, double t1,
+                                double pad) {
+    const int major = face >> 1;
+    const double sign = (face & 1) ? -1.0 : 1.0;
+    const int ia = major == 0 ? 1 : 0, ib = major == 2 ? 1 : 2;
+    double ps[3], pt[3];
+    for (int c = 0; c < 3; ++c) {
+        const double* d = q + 6 + 3 * c;
+        const double m = sign * d[major];
+        if (!(m > 1e-3)) return -1;
+        ps[c] = d[ia] / m;
+        pt[c] = d[ib] / m;
+    }
+    s0 -= pad; s1 += pad; t0 -= pad; t1 += pad;
+    if (fmax(ps[0], fmax(ps[1], ps[2])) < s0 || fmin(ps[0], fmin(ps[1], ps[2])) > s1) return 0;
+    if (fmax(pt[0], fmax(pt[1], pt[2])) < t0 || fmin(pt[0], fmin(pt[1], pt[2])) > t1) return 0;
+    for (int e = 0; e < 3; ++e) {
+        const int i = e, j = (e + 1) % 3, k = (e + 2) % 3;
+        const double nx = -(pt[j] - pt[i]), ny = ps[j] - ps[i];
+        const double side = nx * (ps[k] - ps[i]) + ny * (pt[k] - pt[i]);
+        if (fabs(side) < 1e-14) continue;  // degenerate (edge-on) projection: keep
+        // the square is separated if all four corners are strictly on the far side
+        bool sep = true;
+        for (int cc = 0; cc < 4 && sep; ++cc) {
+            const double cs = (cc & 1) ? s1 : s0, ct = (cc & 2) ? t1 : t0;
+            const double v = nx * (cs - ps[i]) + ny * (ct - pt[i]);
+            sep = side > 0 ? v < 0 : v > 0;
+        }
+        if (sep) return 0;
+    }
+    return 1;
+}
+
+// Light grid build: one cube-map cell per thread. A triangle is listed in a cell
+// when the cell's bounding cone overlaps the triangle's cone AND (where the
+// projection is valid) the exact 2D test on the cell's face passes.
 __global__ void __launch_bounds__(128) k_light_grid(LightGridArgs a) {
-    __shared__ double tile[kGridTile * 6];
+    __shared__ double tile[kGridTile * kCapStride];
     const uint32_t ncell = 6u * a.res * a.res;
     const uint32_t cell = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = cell < ncell;
-    double cx = 0, cy = 0, cz = 1, cr = 1, sr = 0, r = 0;
+    double cx = 0, cy = 0, cz = 1, cr = 1, sr = 0, r = 0, s0 = 0, s1 = 0, t0 = 0, t1 = 0;
+    int face = 0;
     if (active) {
-        const uint32_t face = cell / (a.res * a.res), rem = cell % (a.res * a.res);
+        face = static_cast<int>(cell / (a.res * a.res));
+        const uint32_t rem = cell % (a.res * a.res);
         const uint32_t j = rem / a.res, i = rem % a.res;
         auto dir = [&](double s, double t, double* o) {
             double v[3];
@@ -161,7 +201,11 @@ __global__ void __launch_bounds__(128) k_light_grid(LightGridArgs a) {
             o[0] = v[0] / l; o[1] = v[1] / l; o[2] = v[2] / l;
         };
         const double h = 1.0 / a.res;
-        const double sc = (i + 0.5) * 2.0 * h - 1.0, tc = (j + 0.5) * 2.0 * h - 1.0;
+        s0 = i * 2.0 * h - 1.0;
+        s1 = s0 + 2.0 * h;
+        t0 = j * 2.0 * h - 1.0;
+        t1 = t0 + 2.0 * h;
+        const double sc = 0.5 * (s0 + s1), tc = 0.5 * (t0 + t1);
         double c[3];
         dir(sc, tc, c);
         double mind = 1.0;
@@ -174,19 +218,22 @@ __global__ void __launch_bounds__(128) k_light_grid(LightGridArgs a) {
         cx = c[0]; cy = c[1]; cz = c[2];
         cr = cos(r); sr = sin(r);
     }
+    const double pad = 2.0 * a.eps;  // face-plane units: |d(s,t)/d angle| >= 1
     const uint32_t base_out = (a.fill && active) ? a.offsets[cell] : 0;
     uint32_t count = 0;
     for (uint32_t base = 0; base < a.n_tris; base += kGridTile) {
         const uint32_t n = min(static_cast<uint32_t>(kGridTile), a.n_tris - base);
         __syncthreads();
-        for (uint32_t k = threadIdx.x; k < n * 6; k += blockDim.x) tile[k] = a.caps[base * 6ull + k];
+        for (uint32_t k = threadIdx.x; k < n * kCapStride; k += blockDim.x)
+            tile[k] = a.caps[static_cast<uint64_t>(base) * kCapStride + k];
         __syncthreads();
         if (!active) continue;
         for (uint32_t t = 0; t < n; ++t) {
-            const double* q = tile + 6 * t;  // axis xyz, alpha, cos alpha, sin alpha
+            const double* q = tile + kCapStride * t;
             bool hit;
             if (r + q[3] >= 3.14159265358979323846) hit = true;
             else hit = cx * q[0] + cy * q[1] + cz * q[2] >= cr * q[4] - sr * q[5];
+            if (hit && q[3] < 3.0) hit = tri_cell_overlap(q, face, s0, s1, t0, t1, pad) != 0;
             if (hit) {
                 if (a.fill) a.lists[base_out + count] = base + t;
                 ++count;

@@ -37,8 +37,10 @@ struct SdfBuildArgs {
 };
 cudaError_t launch_sdf_build(const SdfBuildArgs& a, cudaStream_t s);
 
-// Light-space culling grid build (kernels_f64.cu). caps: per triangle
-// {axis.x, axis.y, axis.z, half_angle} of the cone (from the light) that contains it.
+// Light-space culling grid build (kernels_f64.cu). caps: per triangle kCapStride
+// doubles: cone {axis xyz, half angle, cos, sin} (from the light) that contains it,
+// then the three unit vertex directions (exact gnomonic test per cube face).
+constexpr int kCapStride = 15;
 struct LightGridArgs {
     const double* caps;
     uint32_t n_tris;

@@ -89,7 +89,10 @@ enum : int { kEndEscaped = 0, kEndAbsorbed = 1, kEndCapped = 2, kEndError = 3 };
 // Stats slots (device u64 array).
 enum : int {
     kStPaths = 0, kStSegments, kStSphere, kStEvents, kStDecL, kStDecP, kStDecE, kStAbsorbed,
-    kStEscaped, kStCapped, kStErrors, kStShadow, kStCount
+    kStEscaped, kStCapped, kStErrors, kStShadow,
+    // work counters (profiling): nearest-hit traversals, interior nodes visited,
+    // triangle tests (nearest + shadow), live-lane iterations, warp iterations
+    kStTraversals, kStNodes, kStTriTests, kStLaneIters, kStWarpIters, kStCount
 };
 
 template <class R>

@@ -177,3 +177,34 @@ def test_async_pipelined_render_equals_sync(renderer, ico3):
     st = renderer.read_stats()
     assert st.paths == rst.paths and st.segments == rst.segments
     assert np.allclose(s.cpu().numpy(), ref.sum, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
+def test_multi_object_scene_paths_match_oracle(renderer, oracle, models_dir, ico3, precision, rtol, frac):
+    """C5-style scene (4 media; shadow rays crossing other objects, light grid culling)."""
+    from paper_2011_03082_b200.scene import SdfGrid, c5_scene
+    sc = c5_scene(ico3, 64, 36, sdf_resolution=24)
+    sc.light_position = (-4.0, 1.0, 0.5)  # grazing light: shadow rays cross neighbouring media
+    renderer.upload_scene(sc)
+    sdfs = [SdfGrid(*renderer.get_sdf(o)) for o in range(4)]
+    osc_scene = c5_scene(ico3, 64, 36)
+    osc_scene.light_position = sc.light_position
+    for o, g in zip(osc_scene.objects, sdfs):
+        o.sdf = g
+    osc = oracle.Scene(osc_scene.to_desc())
+    om = oracle.Models(models_dir)
+    rng = np.random.default_rng(21)
+    n = 4000
+    pix = rng.integers(0, 64 * 36, n)
+    smp = rng.integers(0, 1000, n)
+    ch = rng.integers(0, 3, n)
+    renderer.set_precision(precision)
+    try:
+        for integ in (0, 1):
+            g_rad, g_seg = renderer.trace_paths(integ, 1, 5, pix, smp, ch)
+            o_rad, o_seg = osc.trace_paths(om, integ, 1, 5, pix, smp, ch)
+            ok = (g_seg == o_seg) & (np.abs(g_rad - o_rad) <= 1e-12 + rtol * np.abs(o_rad))
+            assert ok.mean() >= frac, (precision, integ, ok.mean())
+            assert (o_rad > 0).mean() > 0.05  # the test actually sees light
+    finally:
+        renderer.set_precision("f32")
