@@ -88,6 +88,11 @@ struct ObjectHost {
     uint32_t dims[3];
     std::vector<float> sdf;
     sst_medium media[3];
+    // acceleration-only skip grid (types.cuh ObjK::skip)
+    std::vector<uint8_t> skip;
+    double skip_voxel = 0.0, skip_unit = 0.0;
+    uint32_t skip_dims[3] = {0, 0, 0};
+    bool convex = false;
 };
 
 }  // namespace
@@ -110,7 +115,7 @@ struct sst_gpu_ctx {
     sst_scene_desc desc{};
     DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri;
     uint32_t grid_res = 0;
-    std::vector<DevBuf> sdf_dev;
+    std::vector<DevBuf> sdf_dev, skip_dev;
     DevScene<float> sc32{};
     DevScene<double> sc64{};
 
@@ -245,6 +250,37 @@ void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, 
     oh.sdf_voxel = a.voxel;
 }
 
+// Fine skip grid of one object (2x the SDF resolution over the SDF's box).
+void build_skip_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh) {
+    SkipBuildArgs a{};
+    a.voxel = 0.5 * oh.sdf_voxel;
+    a.half_diagonal = 0.5 * std::sqrt(3.0) * a.voxel;
+    a.unit = a.voxel / 8.0;
+    for (int k = 0; k < 3; ++k) {
+        a.origin[k] = oh.sdf_origin[k];
+        a.dims[k] = 2 * oh.dims[k];
+    }
+    a.n_tris = od.n_triangles;
+    std::vector<double> tv(9ull * od.n_triangles);
+    for (uint32_t t = 0; t < od.n_triangles; ++t)
+        for (int c = 0; c < 3; ++c)
+            for (int k = 0; k < 3; ++k) tv[9ull * t + 3 * c + k] = od.positions[3ull * od.triangles[3 * t + c] + k];
+    const size_t nvox = static_cast<size_t>(a.dims[0]) * a.dims[1] * a.dims[2];
+    DevBuf dtv, dval;
+    dtv.reserve(tv.size() * sizeof(double));
+    dval.reserve(nvox);
+    CK(cudaMemcpyAsync(dtv.p, tv.data(), tv.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    a.tri_vertices = dtv.as<double>();
+    a.values = dval.as<uint8_t>();
+    CK(launch_skip_build(a, ctx->stream));
+    oh.skip.resize(nvox);
+    CK(cudaMemcpyAsync(oh.skip.data(), dval.p, nvox, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    oh.skip_voxel = a.voxel;
+    oh.skip_unit = a.unit;
+    for (int k = 0; k < 3; ++k) oh.skip_dims[k] = a.dims[k];
+}
+
 template <class R>
 void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const DevBuf& tris, DevBuf& objs) {
     const sst_scene_desc& d = ctx->desc;
@@ -259,6 +295,13 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
         ok[o].sdf_voxel = static_cast<R>(oh.sdf_voxel);
         ok[o].sdf_inv_voxel = static_cast<R>(1.0 / oh.sdf_voxel);
         ok[o].sdf = ctx->sdf_dev[o].as<float>();
+        const char* no_skip = std::getenv("SST_NO_SKIP_GRID");
+        const bool use_skip = !oh.skip.empty() && !(no_skip && no_skip[0] == '1');
+        ok[o].skip = use_skip ? ctx->skip_dev[o].as<uint8_t>() : nullptr;
+        ok[o].skip_inv_voxel = static_cast<R>(oh.skip_voxel > 0 ? 1.0 / oh.skip_voxel : 0.0);
+        ok[o].skip_unit = static_cast<R>(oh.skip_unit);
+        for (int a = 0; a < 3; ++a) ok[o].skip_dims[a] = oh.skip_dims[a];
+        ok[o].convex = oh.convex ? 1u : 0u;
     }
     objs.reserve(ok.size() * sizeof(ObjK<R>));
     CK(cudaMemcpyAsync(objs.p, ok.data(), ok.size() * sizeof(ObjK<R>), cudaMemcpyHostToDevice, ctx->stream));
@@ -445,6 +488,8 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         } else {
             build_sdf_gpu(ctx, od, objs[o], is_watertight(tri));
         }
+        build_skip_gpu(ctx, od, objs[o]);
+        objs[o].convex = is_convex(od.positions, od.n_vertices, tri);
     }
     const FlatBvh bvh = build_bvh(tv, tobj);
     build_light_grid(ctx, d, tv, bvh);
@@ -461,14 +506,19 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     up(ctx->nodes64, bvh.nodes_f64);
     up(ctx->tris64, bvh.tris_f64);
     for (auto& b : ctx->sdf_dev) b.release();
+    for (auto& b : ctx->skip_dev) b.release();
     ctx->sdf_dev.assign(ctx->objects.size(), DevBuf{});
+    ctx->skip_dev.assign(ctx->objects.size(), DevBuf{});
     for (size_t o = 0; o < ctx->objects.size(); ++o) {
         const auto& s = ctx->objects[o].sdf;
         ctx->sdf_dev[o].reserve(s.size() * sizeof(float));
         CK(cudaMemcpyAsync(ctx->sdf_dev[o].p, s.data(), s.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        const auto& k = ctx->objects[o].skip;
+        ctx->skip_dev[o].reserve(std::max<size_t>(k.size(), 1));
+        if (!k.empty()) CK(cudaMemcpyAsync(ctx->skip_dev[o].p, k.data(), k.size(), cudaMemcpyHostToDevice, ctx->stream));
     }
     uint64_t bytes = bvh.nodes_f32.size() + bvh.tris_f32.size() + bvh.nodes_f64.size() + bvh.tris_f64.size();
-    for (const auto& o : ctx->objects) bytes += o.sdf.size() * sizeof(float);
+    for (const auto& o : ctx->objects) bytes += o.sdf.size() * sizeof(float) + o.skip.size();
     bytes += ctx->scene_bytes_grid;
     bytes += ctx->objects.size() * (sizeof(ObjK<float>) + sizeof(ObjK<double>));
     ctx->scene_bytes = bytes;
@@ -729,6 +779,7 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
                       &ctx->film_sq, &ctx->keys_pix, &ctx->keys_smp, &ctx->keys_ch, &ctx->step_in, &ctx->step_out})
         b->release();
     for (auto& b : ctx->sdf_dev) b.release();
+    for (auto& b : ctx->skip_dev) b.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);

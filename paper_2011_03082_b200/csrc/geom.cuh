@@ -50,6 +50,20 @@ SST_D R sdf_radius(const ObjK<R>& o, V3<R> p) {
     return v < R(0) ? -v : R(0);
 }
 
+// Conservative distance-to-surface bound from the fine skip grid (0 outside it).
+template <class R>
+SST_D R skip_radius(const ObjK<R>& o, V3<R> p) {
+    if (!o.skip) return R(0);
+    const R rx = (p.x - o.sdf_origin[0]) * o.skip_inv_voxel;
+    const R ry = (p.y - o.sdf_origin[1]) * o.skip_inv_voxel;
+    const R rz = (p.z - o.sdf_origin[2]) * o.skip_inv_voxel;
+    if (rx < R(0) || ry < R(0) || rz < R(0)) return R(0);
+    const uint32_t x = static_cast<uint32_t>(rx), y = static_cast<uint32_t>(ry), z = static_cast<uint32_t>(rz);
+    if (x >= o.skip_dims[0] || y >= o.skip_dims[1] || z >= o.skip_dims[2]) return R(0);
+    const uint8_t q = __ldg(o.skip + (static_cast<size_t>(z) * o.skip_dims[1] + y) * o.skip_dims[0] + x);
+    return static_cast<R>(q) * o.skip_unit;
+}
+
 // --------------------------------------------------------------- ray setup
 template <class R>
 struct RayK {
@@ -116,9 +130,9 @@ SST_D R ray_tri(const RayK<R>& r, V3<R> v0, V3<R> e1, V3<R> e2, R t_min, R t_max
 }
 
 template <class R>
-SST_D void load_node(const void* nodes, int i, R (&b)[12], int& c0, int& c1);
+SST_D void load_node(const void* nodes, int i, R (&b)[12], int& c0, int& c1, int& o0, int& o1);
 template <>
-SST_D void load_node<float>(const void* nodes, int i, float (&b)[12], int& c0, int& c1) {
+SST_D void load_node<float>(const void* nodes, int i, float (&b)[12], int& c0, int& c1, int& o0, int& o1) {
     const NodeF* n = static_cast<const NodeF*>(nodes) + i;
     const float4 a = __ldg(&n->a), bb = __ldg(&n->b), c = __ldg(&n->c);
     const int4 d = __ldg(&n->d);
@@ -127,14 +141,18 @@ SST_D void load_node<float>(const void* nodes, int i, float (&b)[12], int& c0, i
     b[6] = bb.x; b[7] = bb.y; b[8] = bb.z; b[9] = bb.w; b[10] = c.z; b[11] = c.w;
     c0 = d.x;
     c1 = d.y;
+    o0 = d.z;
+    o1 = d.w;
 }
 template <>
-SST_D void load_node<double>(const void* nodes, int i, double (&b)[12], int& c0, int& c1) {
+SST_D void load_node<double>(const void* nodes, int i, double (&b)[12], int& c0, int& c1, int& o0, int& o1) {
     const NodeD* n = static_cast<const NodeD*>(nodes) + i;
     b[0] = n->lo0[0]; b[1] = n->hi0[0]; b[2] = n->lo0[1]; b[3] = n->hi0[1]; b[4] = n->lo0[2]; b[5] = n->hi0[2];
     b[6] = n->lo1[0]; b[7] = n->hi1[0]; b[8] = n->lo1[1]; b[9] = n->hi1[1]; b[10] = n->lo1[2]; b[11] = n->hi1[2];
     c0 = n->c0;
     c1 = n->c1;
+    o0 = n->pad0;
+    o1 = n->pad1;
 }
 
 template <class R>
@@ -173,9 +191,14 @@ constexpr int kStack = 48;
 // interior-node work and triangle work each run on mostly full warps.
 constexpr int kDone = 0x7fffffff;
 
+// want_sign: +1 accept only entering crossings (det > 0), -1 only leaving ones,
+// 0 any. FP32 rays use it (a ray outside every medium can only enter, a flight
+// inside can only leave): with outward-wound meshes this rejects the spurious
+// re-hits of neighbouring triangles that FP32 rounding produces at surfaces.
 template <class R>
 SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
-                             R* t_hit, Hit* hit, uint64_t& n_nodes, uint64_t& n_tris) {
+                             int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
+                             uint64_t& n_tris) {
     int stack_n[kStack];
     R stack_t[kStack];
     int sp = 0;
@@ -194,12 +217,14 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
         // interior nodes until this lane holds a leaf and all lanes do
         while (node != kDone && node >= 0) {
             R b[12];
-            int c0, c1;
-            load_node<R>(sc.nodes, node, b, c0, c1);
+            int c0, c1, o0, o1;
+            load_node<R>(sc.nodes, node, b, c0, c1, o0, o1);
             ++n_nodes;
             R t0, t1;
-            const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_best, &t0);
-            const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_best, &t1);
+            const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_best, &t0) &&
+                            (cull_obj < 0 || o0 != cull_obj);
+            const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_best, &t1) &&
+                            (cull_obj < 0 || o1 != cull_obj);
             if (h0 && h1) {
                 const bool first0 = t0 <= t1;
                 stack_n[sp] = first0 ? c1 : c0;
@@ -230,7 +255,8 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
                 load_tri<R>(sc.tris, i, v0, e1, e2, obj, id);
                 R det;
                 const R t = ray_tri(ray, v0, e1, e2, t_min, t_best, &det);
-                if (t >= R(0) && static_cast<int>(id) != skip) {
+                const bool orient = want_sign == 0 || (want_sign > 0 ? det > R(0) : det < R(0));
+                if (t >= R(0) && static_cast<int>(id) != skip && orient) {
                     t_best = t;
                     hit->tri = id;
                     hit->obj = obj;
@@ -259,8 +285,8 @@ SST_D R optical_depth(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_ma
     for (;;) {
         if (cur >= 0) {
             R b[12];
-            int c0, c1;
-            load_node<R>(sc.nodes, cur, b, c0, c1);
+            int c0, c1, o0, o1;
+            load_node<R>(sc.nodes, cur, b, c0, c1, o0, o1);
             R t0, t1;
             const bool h0 = slab(ray, b[0], b[1], b[2], b[3], b[4], b[5], t_min, t_max, &t0);
             const bool h1 = slab(ray, b[6], b[7], b[8], b[9], b[10], b[11], t_min, t_max, &t1);

@@ -223,6 +223,33 @@ HostMesh load_obj(const std::string& path, double scale) {
     return m;
 }
 
+bool is_convex(const double* pos, uint32_t nv, const std::vector<std::array<uint32_t, 3>>& tri) {
+    if (static_cast<double>(nv) * tri.size() > 4e8) return false;  // too big to check: assume not
+    double scale = 0.0;
+    for (uint32_t i = 0; i < 3 * nv; ++i) scale = std::fmax(scale, std::fabs(pos[i]));
+    const double tol = 1e-9 * std::fmax(scale, 1.0);
+    for (const auto& f : tri) {
+        const double* a = pos + 3 * f[0];
+        const double* b = pos + 3 * f[1];
+        const double* c = pos + 3 * f[2];
+        const double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        const double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+        double n[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+        const double l = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        if (!(l > 0)) continue;
+        for (int k = 0; k < 3; ++k) n[k] /= l;
+        double lo = 0.0, hi = 0.0;
+        for (uint32_t v = 0; v < nv; ++v) {
+            const double* p = pos + 3 * v;
+            const double d = n[0] * (p[0] - a[0]) + n[1] * (p[1] - a[1]) + n[2] * (p[2] - a[2]);
+            lo = std::fmin(lo, d);
+            hi = std::fmax(hi, d);
+        }
+        if (lo < -tol && hi > tol) return false;  // vertices on both sides of a face plane
+    }
+    return !tri.empty();
+}
+
 bool is_watertight(const std::vector<std::array<uint32_t, 3>>& tri) {
     std::unordered_map<uint64_t, int> edges;
     for (const auto& f : tri)
@@ -401,6 +428,23 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
     out.n_nodes = static_cast<uint32_t>(bld.nodes.size());
     out.n_tris = n;
     out.order = bld.order;
+    // Object id of every child subtree (-1 when mixed): lets a traversal cull the
+    // object a ray is leaving when that object is convex.
+    auto code_obj = [&](int32_t code, const std::vector<int32_t>& node_obj) -> int32_t {
+        if (code >= 0) return node_obj[code];
+        const uint32_t leaf = static_cast<uint32_t>(~code);
+        const uint32_t first = leaf >> 3, count = leaf & 7u;
+        if (count == 0) return -1;
+        const int32_t o = static_cast<int32_t>(tri_obj[bld.order[first]]);
+        for (uint32_t k = first + 1; k < first + count; ++k)
+            if (static_cast<int32_t>(tri_obj[bld.order[k]]) != o) return -1;
+        return o;
+    };
+    std::vector<int32_t> node_obj(out.n_nodes, -1);
+    for (int32_t i = static_cast<int32_t>(out.n_nodes) - 1; i >= 0; --i) {  // children have larger indices
+        const int32_t a = code_obj(bld.nodes[i].c0, node_obj), b = code_obj(bld.nodes[i].c1, node_obj);
+        node_obj[i] = (a == b) ? a : -1;
+    }
     std::vector<NodeF> nf(out.n_nodes);
     std::vector<NodeD> nd(out.n_nodes);
     for (uint32_t i = 0; i < out.n_nodes; ++i) {
@@ -408,7 +452,8 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
         nf[i].a = make_float4(down(t.b0.lo[0]), up(t.b0.hi[0]), down(t.b0.lo[1]), up(t.b0.hi[1]));
         nf[i].b = make_float4(down(t.b1.lo[0]), up(t.b1.hi[0]), down(t.b1.lo[1]), up(t.b1.hi[1]));
         nf[i].c = make_float4(down(t.b0.lo[2]), up(t.b0.hi[2]), down(t.b1.lo[2]), up(t.b1.hi[2]));
-        nf[i].d = make_int4(t.c0, t.c1, 0, 0);
+        const int32_t o0 = code_obj(t.c0, node_obj), o1 = code_obj(t.c1, node_obj);
+        nf[i].d = make_int4(t.c0, t.c1, o0, o1);
         for (int a = 0; a < 3; ++a) {
             nd[i].lo0[a] = pad_lo(t.b0.lo[a]);
             nd[i].hi0[a] = pad_hi(t.b0.hi[a]);
@@ -417,7 +462,8 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
         }
         nd[i].c0 = t.c0;
         nd[i].c1 = t.c1;
-        nd[i].pad0 = nd[i].pad1 = 0;
+        nd[i].pad0 = o0;
+        nd[i].pad1 = o1;
     }
     std::vector<TriF> tf(n);
     std::vector<TriD> td(n);

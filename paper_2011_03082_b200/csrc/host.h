@@ -51,6 +51,8 @@ HostMesh make_icosphere(int subdivisions, double radius);
 HostMesh make_bumpy_sphere(int subdivisions, double radius, double amplitude, double frequency);
 HostMesh load_obj(const std::string& path, double scale);
 bool is_watertight(const std::vector<std::array<uint32_t, 3>>& tri);
+// Every vertex on one side of every face plane (closed convex polyhedron).
+bool is_convex(const double* pos, uint32_t nv, const std::vector<std::array<uint32_t, 3>>& tri);
 
 // Flattened BVH2 for the device (binned-SAH build, <= 4 triangles per leaf).
 struct FlatBvh {

@@ -70,6 +70,7 @@ struct PathLocal {
     uint32_t seg, pixel;
     int obj;        // -1 outside every medium
     int skip;       // triangle to ignore on the next traversal (FP32 surface start)
+    int cull;       // convex object just left: its subtree is culled on the next traversal
     uint8_t c;
     bool r_valid;
     bool pending;   // a sphere step is requested and waits for its warp batch
@@ -112,6 +113,7 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
     p.pixel = pixel;
     p.obj = -1;
     p.skip = -1;
+    p.cull = -1;
     p.c = static_cast<uint8_t>(c);
     p.r_valid = false;
     p.pending = false;
@@ -154,9 +156,11 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
                 p.r_here = sdf_radius(*ob, p.x);
                 p.r_valid = true;
             }
-            // A flight shorter than the conservative SDF radius cannot reach the
-            // boundary: skip the traversal (exact).
+            // A flight shorter than a conservative distance to the surface cannot
+            // reach the boundary: skip the traversal (exact). Bounds: the scene SDF
+            // radius and, when that is too coarse, the finer skip grid.
             trace = !(t_free < p.r_here);
+            if (trace) trace = !(t_free < skip_radius(*ob, p.x));
             t_max = t_free;
         } else {
             trace = true;
@@ -167,8 +171,9 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     Hit h{0, 0};
     if (trace) {
         const RayK<R> ray = make_ray(p.x, p.w);
-        hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, &t_hit, &h,
-                                st.nodes, st.tris);
+        const int want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
+        hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, p.cull, want,
+                                &t_hit, &h, st.nodes, st.tris);
         ++st.traversals;
     }
     // ---- 2. resolve
@@ -181,11 +186,13 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             } else {  // medium entry (index-matched boundary)
                 p.x = p.x + p.w * t_hit;
                 p.obj = static_cast<int>(h.obj);
+                p.cull = -1;
                 p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
                 p.r_valid = false;
             }
         } else if (hit) {  // leaves the medium
             p.x = p.x + p.w * t_hit;
+            p.cull = ob->convex ? p.obj : -1;
             p.obj = -1;
             p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(h.tri);
         } else {  // collision

@@ -133,6 +133,34 @@ __global__ void __launch_bounds__(128) k_sdf_build(SdfBuildArgs a) {
     a.values[v] = static_cast<float>(inside ? -cons : cons);
 }
 
+__global__ void __launch_bounds__(128) k_skip_build(SkipBuildArgs a) {
+    __shared__ double tile[kSdfTile * 9];
+    const uint64_t nvox = static_cast<uint64_t>(a.dims[0]) * a.dims[1] * a.dims[2];
+    const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const bool active = v < nvox;
+    const uint32_t x = active ? static_cast<uint32_t>(v % a.dims[0]) : 0;
+    const uint32_t y = active ? static_cast<uint32_t>((v / a.dims[0]) % a.dims[1]) : 0;
+    const uint32_t z = active ? static_cast<uint32_t>(v / (static_cast<uint64_t>(a.dims[0]) * a.dims[1])) : 0;
+    const D3 c = add(d3(a.origin[0], a.origin[1], a.origin[2]),
+                     d3((x + 0.5) * a.voxel, (y + 0.5) * a.voxel, (z + 0.5) * a.voxel));
+    double best = 1e300;
+    for (uint32_t base = 0; base < a.n_tris; base += kSdfTile) {
+        const uint32_t n = min(static_cast<uint32_t>(kSdfTile), a.n_tris - base);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < n * 9; k += blockDim.x) tile[k] = a.tri_vertices[base * 9ull + k];
+        __syncthreads();
+        if (!active) continue;
+        for (uint32_t t = 0; t < n; ++t) {
+            const double* q = tile + 9 * t;
+            best = fmin(best, pt_tri_d2(c, d3(q[0], q[1], q[2]), d3(q[3], q[4], q[5]), d3(q[6], q[7], q[8])));
+        }
+    }
+    if (!active) return;
+    // 0.999: margin against the float rounding of positions at lookup time
+    const double cons = fmax(0.0, 0.999 * sqrt(best) - a.half_diagonal);
+    a.values[v] = static_cast<uint8_t>(fmin(255.0, floor(cons / a.unit)));
+}
+
 constexpr int kGridTile = 128;
 
 // Exact test of a (projected) triangle against a cube-map cell. Directions are
@@ -244,6 +272,12 @@ __global__ void __launch_bounds__(128) k_light_grid(LightGridArgs a) {
 }
 
 }  // namespace
+
+cudaError_t launch_skip_build(const SkipBuildArgs& a, cudaStream_t s) {
+    const uint64_t nvox = static_cast<uint64_t>(a.dims[0]) * a.dims[1] * a.dims[2];
+    k_skip_build<<<static_cast<unsigned>((nvox + 127) / 128), 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_light_grid(const LightGridArgs& a, cudaStream_t s) {
     const uint32_t ncell = 6u * a.res * a.res;

@@ -37,6 +37,18 @@ struct SdfBuildArgs {
 };
 cudaError_t launch_sdf_build(const SdfBuildArgs& a, cudaStream_t s);
 
+// Skip-grid build (kernels_f64.cu): q = floor(max(0, d(center) - half_diag) / unit),
+// d = exact unsigned point-triangle distance (FP64), saturated at 255.
+struct SkipBuildArgs {
+    const double* tri_vertices;  // [9 * n_tris]
+    uint32_t n_tris;
+    double origin[3];
+    double voxel, half_diagonal, unit;
+    uint32_t dims[3];
+    uint8_t* values;
+};
+cudaError_t launch_skip_build(const SkipBuildArgs& a, cudaStream_t s);
+
 // Light-space culling grid build (kernels_f64.cu). caps: per triangle kCapStride
 // doubles: cone {axis xyz, half angle, cos, sin} (from the light) that contains it,
 // then the three unit vertex directions (exact gnomonic test per cube face).

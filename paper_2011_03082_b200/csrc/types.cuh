@@ -34,7 +34,7 @@ struct DecodeCount {
 // child >= 0: interior node index; child < 0: leaf, ~child = (first << 3) | count.
 struct alignas(16) NodeF {
     float4 a, b, c;
-    int4 d;
+    int4 d;  // child0, child1, object of child0 subtree, object of child1 subtree (-1 mixed)
 };
 struct alignas(16) NodeD {
     double lo0[3], hi0[3], lo1[3], hi1[3];
@@ -57,6 +57,14 @@ struct ObjK {
     R sdf_inv_voxel;
     uint32_t dims[3];
     const float* sdf;
+    // Acceleration-only skip grid (2x the SDF resolution, same origin): per voxel a
+    // lower bound on the distance from ANY point of the voxel to this object's
+    // surface, in units of skip_unit (uint8, floor-quantised). Never changes results:
+    // it only proves that a free flight cannot reach the boundary.
+    const uint8_t* skip;
+    R skip_inv_voxel, skip_unit;
+    uint32_t skip_dims[3];
+    uint32_t convex;  // closed convex mesh: a ray leaving it cannot hit it again
 };
 
 template <class R>

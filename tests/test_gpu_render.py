@@ -208,3 +208,15 @@ def test_multi_object_scene_paths_match_oracle(renderer, oracle, models_dir, ico
             assert (o_rad > 0).mean() > 0.05  # the test actually sees light
     finally:
         renderer.set_precision("f32")
+
+
+def test_fp32_has_no_surface_leaks(renderer, ico3):
+    """FP32 surface robustness: orientation-aware hits + convex-object culling leave no
+    path wandering outside a medium (such paths run into the 1e5-step cap)."""
+    from paper_2011_03082_b200 import ST, abi
+    from paper_2011_03082_b200.scene import c5_scene
+    renderer.upload_scene(c5_scene(ico3, 480, 270))
+    st = abi.PathStats()
+    renderer.render_film(ST, 5000, 1, True, 0, 8, stats=st)
+    assert st.capped == 0, st.capped
+    assert st.errors == 0
