@@ -123,6 +123,18 @@ struct sst_gpu_ctx {
     DevBuf step_in, step_out;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+    // Derived-structure caches keyed by content fingerprints (FNV-1a), the way the
+    // reference caches SDFs (load_or_build_sdf, sdf.cpp:103-119): per-object SDF /
+    // skip grid / convexity, and the scene BVH + light grid. Re-uploading an
+    // unchanged scene recomputes nothing but still copies everything to the device.
+    std::map<uint64_t, ObjectHost> obj_cache;
+    struct SceneCache {
+        uint64_t fp = 0;
+        FlatBvh bvh;
+        std::vector<uint32_t> grid_off, grid_tri;
+        uint32_t grid_res = 0;
+    } scene_cache;
+
     // Render pipeline: chunks of a render call rotate over kSlots streams so the
     // long-path tail of one persistent launch overlaps the next launch's bulk.
     // Film accumulations stay in chunk order (event chain) -> deterministic sums.
@@ -143,6 +155,15 @@ namespace {
 std::mutex g_const_mu;
 std::map<int, std::pair<const sst_gpu_ctx*, uint64_t>> g_const_owner;  // device -> (ctx, gen)
 uint64_t g_serial = 0;
+
+uint64_t fnv(const void* data, size_t n, uint64_t h = 0xCBF29CE484222325ULL) {
+    const auto* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001B3ULL;
+    }
+    return h;
+}
 
 void require_device(sst_gpu_ctx* ctx) {
     if (!ctx) throw InvalidArgument("null context");
@@ -430,7 +451,12 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
     a.offsets = ctx->grid_off.as<uint32_t>();
     a.lists = ctx->grid_tri.as<uint32_t>();
     CK(launch_light_grid(a, ctx->stream));
+    ctx->scene_cache.grid_off = offsets;
+    ctx->scene_cache.grid_tri.resize(total);
+    if (total) CK(cudaMemcpyAsync(ctx->scene_cache.grid_tri.data(), ctx->grid_tri.p, total * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    ctx->scene_cache.grid_res = res;
     ctx->grid_res = res;
     ctx->scene_bytes_grid = offsets.size() * sizeof(uint32_t) + total * sizeof(uint32_t);
 }
@@ -475,6 +501,21 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
             tv.push_back(corners);
             tobj.push_back(o);
         }
+        uint64_t ofp = fnv(od.positions, 3ull * od.n_vertices * sizeof(double));
+        ofp = fnv(od.triangles, 3ull * od.n_triangles * sizeof(uint32_t), ofp);
+        ofp = fnv(&od.sdf_resolution, sizeof od.sdf_resolution, ofp);
+        if (od.sdf_values) {
+            ofp = fnv(od.sdf_origin, sizeof od.sdf_origin, ofp);
+            ofp = fnv(&od.sdf_voxel, sizeof od.sdf_voxel, ofp);
+            ofp = fnv(od.sdf_dims, sizeof od.sdf_dims, ofp);
+            ofp = fnv(od.sdf_values, static_cast<size_t>(od.sdf_dims[0]) * od.sdf_dims[1] * od.sdf_dims[2] * sizeof(float), ofp);
+        }
+        if (auto it = ctx->obj_cache.find(ofp); it != ctx->obj_cache.end()) {
+            const sst_medium media[3] = {objs[o].media[0], objs[o].media[1], objs[o].media[2]};
+            objs[o] = it->second;
+            for (int c = 0; c < 3; ++c) objs[o].media[c] = media[c];
+            continue;
+        }
         if (od.sdf_values) {
             if (!(od.sdf_voxel > 0.0) || !od.sdf_dims[0] || !od.sdf_dims[1] || !od.sdf_dims[2])
                 throw InvalidArgument("SDF grid has empty dims or voxel size");
@@ -490,9 +531,31 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         }
         build_skip_gpu(ctx, od, objs[o]);
         objs[o].convex = is_convex(od.positions, od.n_vertices, tri);
+        if (ctx->obj_cache.size() >= 64) ctx->obj_cache.clear();
+        ctx->obj_cache[ofp] = objs[o];
     }
-    const FlatBvh bvh = build_bvh(tv, tobj);
-    build_light_grid(ctx, d, tv, bvh);
+    uint64_t sfp = fnv(tv.data(), tv.size() * sizeof(tv[0]));
+    sfp = fnv(tobj.data(), tobj.size() * sizeof(uint32_t), sfp);
+    sfp = fnv(d->light_position, sizeof d->light_position, sfp);
+    const bool cached = ctx->scene_cache.fp == sfp && ctx->scene_cache.grid_res;
+    if (!cached) {
+        ctx->scene_cache = sst_gpu_ctx::SceneCache{};
+        ctx->scene_cache.bvh = build_bvh(tv, tobj);
+        build_light_grid(ctx, d, tv, ctx->scene_cache.bvh);
+        ctx->scene_cache.fp = sfp;
+    } else {  // copy the cached light grid to the device (inputs travel every upload)
+        const auto& sc = ctx->scene_cache;
+        ctx->grid_off.reserve(sc.grid_off.size() * sizeof(uint32_t));
+        ctx->grid_tri.reserve(std::max<size_t>(sc.grid_tri.size(), 1) * sizeof(uint32_t));
+        CK(cudaMemcpyAsync(ctx->grid_off.p, sc.grid_off.data(), sc.grid_off.size() * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, ctx->stream));
+        if (!sc.grid_tri.empty())
+            CK(cudaMemcpyAsync(ctx->grid_tri.p, sc.grid_tri.data(), sc.grid_tri.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+        ctx->grid_res = sc.grid_res;
+        ctx->scene_bytes_grid = (sc.grid_off.size() + sc.grid_tri.size()) * sizeof(uint32_t);
+    }
+    const FlatBvh& bvh = ctx->scene_cache.bvh;
     // upload
     ctx->objects = std::move(objs);
     ctx->desc = *d;
