@@ -289,11 +289,17 @@ def bench_ours(args, world, rank, local):
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
+        t_up = 0.0
         for i in range(args.steps):
+            ta = time.perf_counter()
             r.upload_scene(scene)
+            t_up += time.perf_counter() - ta
             s0, s1 = slab(args.warmup + i)
             r.render_film(sb.ST, FRAME_SPP, 1, True, s0, s1, film, est)
         t_e2e = time.perf_counter() - t0
+        if os.environ.get("SST_BENCH_VERBOSE"):
+            print(f"e2e: {t_e2e:.3f} s total, upload {t_up:.3f} s, device {est.device_ms / 1e3:.3f} s",
+                  file=sys.stderr)
         e_seg = float(est.segments)
         if dist:
             t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")

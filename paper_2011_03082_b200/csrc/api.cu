@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -462,6 +463,14 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
 }
 
 void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
+    const bool tdbg = std::getenv("SST_DEBUG_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t_start = now();
+    auto lap = [&](const char* what) {
+        if (tdbg)
+            std::fprintf(stderr, "[upload_scene] %-14s %8.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(now() - t_start).count());
+    };
     if (!d || d->n_objects == 0 || !d->objects) throw InvalidArgument("scene has no objects");
     if (d->width == 0 || d->height == 0) throw InvalidArgument("camera resolution must be >= 1x1");
     if (!(d->cam_vfov_deg > 0.0 && d->cam_vfov_deg < 180.0)) throw InvalidArgument("camera fov out of range");
@@ -534,6 +543,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         if (ctx->obj_cache.size() >= 64) ctx->obj_cache.clear();
         ctx->obj_cache[ofp] = objs[o];
     }
+    lap("objects");
     uint64_t sfp = fnv(tv.data(), tv.size() * sizeof(tv[0]));
     sfp = fnv(tobj.data(), tobj.size() * sizeof(uint32_t), sfp);
     sfp = fnv(d->light_position, sizeof d->light_position, sfp);
@@ -556,6 +566,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         ctx->scene_bytes_grid = (sc.grid_off.size() + sc.grid_tri.size()) * sizeof(uint32_t);
     }
     const FlatBvh& bvh = ctx->scene_cache.bvh;
+    lap(cached ? "bvh+grid(hit)" : "bvh+grid(build)");
     // upload
     ctx->objects = std::move(objs);
     ctx->desc = *d;
@@ -568,10 +579,11 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     up(ctx->tris32, bvh.tris_f32);
     up(ctx->nodes64, bvh.nodes_f64);
     up(ctx->tris64, bvh.tris_f64);
-    for (auto& b : ctx->sdf_dev) b.release();
-    for (auto& b : ctx->skip_dev) b.release();
-    ctx->sdf_dev.assign(ctx->objects.size(), DevBuf{});
-    ctx->skip_dev.assign(ctx->objects.size(), DevBuf{});
+    // device grids are reused across uploads (grow-only) -- no cudaFree/cudaMalloc per frame
+    if (ctx->sdf_dev.size() < ctx->objects.size()) {
+        ctx->sdf_dev.resize(ctx->objects.size());
+        ctx->skip_dev.resize(ctx->objects.size());
+    }
     for (size_t o = 0; o < ctx->objects.size(); ++o) {
         const auto& s = ctx->objects[o].sdf;
         ctx->sdf_dev[o].reserve(s.size() * sizeof(float));
@@ -587,9 +599,11 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     ctx->scene_bytes = bytes;
     ctx->n_nodes = bvh.n_nodes;
     ctx->n_tris = bvh.n_tris;
+    lap("copies queued");
     fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
     fill_devscene<double>(ctx, ctx->sc64, ctx->nodes64, ctx->tris64, ctx->objs64);
     CK(cudaStreamSynchronize(ctx->stream));
+    lap("done");
     ctx->scene = true;
 }
 
