@@ -814,7 +814,11 @@ static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint
         x = add(x, mul(w, t));
         for (;;) {
             const double t_free = m.sigma_t > 0.0 ? -log1p(-so_uniform(&rng)) / m.sigma_t : 1e300;
-            if (intersect(s, x, w, 1e-9, t_free, &t, &tri)) { x = add(x, mul(w, t)); break; }
+            const int hit_ = intersect(s, x, w, 1e-9, t_free, &t, &tri);
+            if (getenv("SO_TRACE_DEBUG"))
+                fprintf(stderr, "[orc] seg=%u obj=%u x=(%.17g,%.17g,%.17g) w=(%.17g,%.17g,%.17g) tfree=%.17g hit=%d thit=%.17g\n",
+                        r->seg, obj, x.x, x.y, x.z, w.x, w.y, w.z, t_free, hit_, hit_ ? t : 0.0);
+            if (hit_) { x = add(x, mul(w, t)); break; }
             x = add(x, mul(w, t_free));
             if (r->seg >= cap) { r->L = 0.0; r->end = 2; return; }
             ++r->seg;
@@ -822,6 +826,7 @@ static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint
             if (integ == SST_INTEGRATOR_ST) {
                 const double xp[3] = {x.x, x.y, x.z};
                 rad = so_query_safe_radius(s->sdf_o[obj], s->sdf_v[obj], s->sdf_d[obj], s->sdf_vals[obj], xp);
+                if (getenv("SO_TRACE_DEBUG")) fprintf(stderr, "[orc]   collide r=%.17g r_min=%.17g\n", rad, rmin);
             }
             if (integ == SST_INTEGRATOR_ST && rad > rmin) {
                 ++r->steps;

@@ -8,6 +8,9 @@
 #pragma once
 
 #include "common.cuh"
+#ifdef SST_TRACE_DEBUG
+#include <cstdio>
+#endif
 #include "geom.cuh"
 #include "rng.cuh"
 #include "step.cuh"
@@ -176,6 +179,11 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
                                 &t_hit, &h, st.nodes, st.tris);
         ++st.traversals;
     }
+#ifdef SST_TRACE_DEBUG
+    if (active) printf("[gpu] seg=%u obj=%d x=(%.17g,%.17g,%.17g) w=(%.17g,%.17g,%.17g) trace=%d tfree=%.17g hit=%d thit=%.17g rhere=%.17g\n",
+                       p.seg, p.obj, (double)p.x.x, (double)p.x.y, (double)p.x.z, (double)p.w.x, (double)p.w.y, (double)p.w.z,
+                       (int)trace, (double)t_free, (int)hit, (double)t_hit, (double)p.r_here);
+#endif
     // ---- 2. resolve
     bool collide = false;
     if (active) {
@@ -216,6 +224,9 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     if (ST && collide) {
         p.r_here = sdf_radius(*ob, p.x);
         p.r_valid = true;
+#ifdef SST_TRACE_DEBUG
+        printf("[gpu]   collide r=%.17g r_min=%.17g\n", (double)p.r_here, (double)ob->med[p.c].r_min);
+#endif
         if (p.r_here > ob->med[p.c].r_min) {
             p.pending = true;
             p.waited = 0;

@@ -112,6 +112,9 @@ class Scene:
         d.r_min = self.r_min
         d.max_pt_events = self.max_pt_events
         d.max_st_steps = self.max_st_steps
+        # the descriptor owns the buffers it points to (temporaries like
+        # `Scene(...).to_desc()` must not leave dangling pointers)
+        d._keep = keep
         self._keep = keep
         return d
 

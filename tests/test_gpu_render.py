@@ -220,3 +220,28 @@ def test_fp32_has_no_surface_leaks(renderer, ico3):
     renderer.render_film(ST, 5000, 1, True, 0, 8, stats=st)
     assert st.capped == 0, st.capped
     assert st.errors == 0
+
+
+@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
+def test_nonconvex_bumpy_scene_paths_match_oracle(renderer, oracle, models_dir, precision, rtol, frac):
+    """Config-3 geometry (bumpy sphere, non-convex: no exit culling; FP32 relies on the
+    orientation-aware hits), density 40, both integrators, NEE on."""
+    from paper_2011_03082_b200 import make_bumpy_sphere
+    from paper_2011_03082_b200.scene import SdfGrid, c1_scene
+    mesh = make_bumpy_sphere(4, 1.0, 0.2, 3.0)
+    sc = c1_scene(mesh, 48, 48, sigma_t=40.0, sdf_resolution=48)
+    renderer.upload_scene(sc)
+    osc = oracle.Scene(c1_scene(mesh, 48, 48, sigma_t=40.0, sdf=SdfGrid(*renderer.get_sdf(0))).to_desc())
+    om = oracle.Models(models_dir)
+    rng = np.random.default_rng(8)
+    n = 3000
+    pix, smp, ch = rng.integers(0, 48 * 48, n), rng.integers(0, 500, n), rng.integers(0, 3, n)
+    renderer.set_precision(precision)
+    try:
+        for integ in (0, 1):
+            g_rad, g_seg = renderer.trace_paths(integ, 1, 9, pix, smp, ch)
+            o_rad, o_seg = osc.trace_paths(om, integ, 1, 9, pix, smp, ch)
+            ok = (g_seg == o_seg) & (np.abs(g_rad - o_rad) <= 1e-12 + rtol * np.abs(o_rad))
+            assert ok.mean() >= frac, (precision, integ, ok.mean())
+    finally:
+        renderer.set_precision("f32")
