@@ -257,6 +257,42 @@ int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed
                         const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
                         double* radiance, uint32_t* segments, sst_path_stats* stats);
 
+/* ------------------------------------------------------------------------ */
+/* Config 4: CVAE training-data generation, the device form of  */
+/* generate_dataset (dataset.cpp:40-92) over walk_sphere / parameterize_exit /    */
+/* sample_representative (sphere_walk.cpp:22-102). Sample i uses                 */
+/* RandomStream(seed, kDataset, i) like the reference, so any index range can be */
+/* generated on any GPU (sharding: disjoint [first_index, first_index + n)).      */
+/* ------------------------------------------------------------------------ */
+
+/* TrainingSample (dataset.hpp:17-27): 52 bytes, the SSWK record layout. */
+typedef struct {
+    float sigma_t, g, phi;
+    uint32_t n_events;
+    float cos_theta, alpha, beta;
+    float rep_position[3];
+    float rep_direction[3];
+} sst_training_sample;
+
+/* PhiSampler kinds (dataset.hpp:30-41). */
+enum { SST_PHI_LOG_COMPLEMENT = 0, SST_PHI_FIXED = 1, SST_PHI_UNIFORM = 2 };
+
+typedef struct {
+    uint64_t walks;           /* samples generated */
+    uint64_t events;          /* scattering events simulated (sum of N) */
+    uint64_t replay_events;   /* events re-simulated to reach the representative */
+    uint64_t max_events;      /* largest N */
+    double device_ms;
+} sst_dataset_stats;
+
+/* Samples [first_index, first_index + n). Host or device `out` per ptr_kind.
+ * Errors: SST_E_INVALID_ARGUMENT for the reference's range checks
+ * (dataset.cpp:44-48); SST_E_RUNTIME when a walk exceeds 1e6 events. */
+int sst_gpu_generate_dataset(sst_gpu_ctx* ctx, uint64_t n, double sigma_t_lo, double sigma_t_hi,
+                             double g_lo, double g_hi, int phi_kind, double phi_a, double phi_b,
+                             uint64_t seed, uint64_t first_index, sst_training_sample* out,
+                             int ptr_kind, sst_dataset_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

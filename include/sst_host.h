@@ -34,6 +34,12 @@ int sst_sdf_load(const char* path, double origin[3], double* voxel, uint32_t dim
                  float** values, uint64_t* mesh_fingerprint);
 void sst_sdf_free(float* values);
 
+/* save_dataset (dataset.cpp:94-119): SSWK v1, little-endian, 52-byte records
+ * (sst_training_sample from sst_gpu.h). phi_kind/phi_a/phi_b as PhiSampler. */
+int sst_dataset_save(const char* path, uint64_t count, float sigma_t_lo, float sigma_t_hi, float g_lo,
+                     float g_hi, uint32_t phi_kind, float phi_a, float phi_b, uint64_t seed,
+                     const void* samples);
+
 /* save_pfm (image.cpp:32-41): little-endian "PF", bottom row first. */
 int sst_image_save_pfm(const char* path, uint32_t width, uint32_t height, const float* rgb);
 

@@ -127,6 +127,17 @@ def main():
             rad, seg = rs.trace_paths(M, integ, nee, 1, pix, smp, ch, st)
             out[f"path_{integ}{nee}_radiance"] = rad
             out[f"path_{integ}{nee}_segments"] = seg
+    # --- config 4: generate_dataset (dataset.cpp:40-92), TrainingSample records as bytes
+    ds_a = reflib.generate_dataset(2000, sigma=(0.0, 40.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), seed=11)
+    ds_b = reflib.generate_dataset(300, sigma=(0.0, 200.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), seed=12)
+    ds_c = reflib.generate_dataset(300, sigma=(5.0, 50.0), g=(0.0, 0.9), phi=(2, 0.5, 1.0), seed=13)
+    out["ds_a"] = np.frombuffer(ds_a.tobytes(), np.uint8)
+    out["ds_b"] = np.frombuffer(ds_b.tobytes(), np.uint8)
+    out["ds_c"] = np.frombuffer(ds_c.tobytes(), np.uint8)
+    path = os.path.join("/tmp", "golden_ds.sswk")
+    reflib.check(reflib.lib().ref_save_dataset(path.encode(), 300, 0.0, 200.0, -1.0, 1.0, 0, -5.0, -0.5, 12,
+                                               ds_b.ctypes.data_as(C.c_void_p)))
+    out["ds_b_sswk"] = np.frombuffer(open(path, "rb").read(), np.uint8)
     np.savez_compressed(os.path.join(GOLD, "reference_golden.npz"), **out)
     sz = os.path.getsize(os.path.join(GOLD, "reference_golden.npz"))
     print(f"wrote tests/golden/reference_golden.npz ({sz / 1e6:.2f} MB, {len(out)} arrays)")

@@ -56,6 +56,7 @@ def lib():
         L.so_scene_free.argtypes = [P]
         L.so_scene_free.restype = None
         L.so_bvh_intersect.argtypes = [P, P, P, D, D, P, P]
+        L.so_generate_dataset.argtypes = [U64, D, D, D, D, I, D, D, U64, U64, P]
         L.so_trace_paths.argtypes = [P, P, I, I, U64, U64, P, P, P, P, P, C.POINTER(abi.PathStats)]
     return _lib
 
@@ -192,3 +193,15 @@ class Scene:
                                    int(nee), seed, n, ptr(pixel), ptr(sample), ptr(channel), ptr(rad),
                                    ptr(seg), C.byref(stats) if stats is not None else None))
         return rad, seg
+
+
+SAMPLE_DTYPE = np.dtype([("sigma_t", "<f4"), ("g", "<f4"), ("phi", "<f4"), ("n_events", "<u4"),
+                         ("cos_theta", "<f4"), ("alpha", "<f4"), ("beta", "<f4"),
+                         ("rep_position", "<f4", (3,)), ("rep_direction", "<f4", (3,))])
+
+
+def generate_dataset(n, sigma=(0.0, 200.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), seed=7, first=0):
+    out = np.zeros(n, dtype=SAMPLE_DTYPE)
+    check(lib().so_generate_dataset(n, sigma[0], sigma[1], g[0], g[1], phi[0], phi[1], phi[2], seed,
+                                    first, ptr(out)))
+    return out

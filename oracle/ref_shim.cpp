@@ -215,6 +215,40 @@ int ref_make_weights(const char* outdir, uint64_t n_samples, uint32_t epochs, ui
     });
 }
 
+// generate_dataset (dataset.cpp:40-92) -> TrainingSample records (52 B each, dataset.hpp:17-27).
+int ref_generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi, int phi_kind,
+                         double phi_a, double phi_b, uint64_t seed, void* out) {
+    return guarded([&] {
+        PhiSampler ps;
+        ps.kind = static_cast<PhiSampler::Kind>(phi_kind);
+        ps.a = phi_a;
+        ps.b = phi_b;
+        const Dataset ds = generate_dataset(n, s_lo, s_hi, g_lo, g_hi, ps, seed);
+        static_assert(sizeof(TrainingSample) == 52, "TrainingSample layout");
+        std::memcpy(out, ds.samples.data(), n * sizeof(TrainingSample));
+    });
+}
+
+// save_dataset (dataset.cpp:94-119) of n records (for SSWK byte-compatibility tests).
+int ref_save_dataset(const char* path, uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi,
+                     int phi_kind, double phi_a, double phi_b, uint64_t seed, const void* samples) {
+    return guarded([&] {
+        Dataset ds;
+        ds.header.count = n;
+        ds.header.sigma_t_lo = static_cast<float>(s_lo);
+        ds.header.sigma_t_hi = static_cast<float>(s_hi);
+        ds.header.g_lo = static_cast<float>(g_lo);
+        ds.header.g_hi = static_cast<float>(g_hi);
+        ds.header.phi.kind = static_cast<PhiSampler::Kind>(phi_kind);
+        ds.header.phi.a = phi_a;
+        ds.header.phi.b = phi_b;
+        ds.header.seed = seed;
+        ds.samples.resize(n);
+        std::memcpy(ds.samples.data(), samples, n * sizeof(TrainingSample));
+        save_dataset(path, ds);
+    });
+}
+
 // Ground-truth unit-sphere walks (sphere_walk.cpp:22-50) -> (N, cos_theta, alpha, beta).
 int ref_walk_stats(double sigma_t, double g, uint64_t seed, uint64_t n, uint32_t* n_events,
                    double* exit_params) {

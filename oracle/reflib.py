@@ -65,6 +65,8 @@ def _declare(L):
     L.ref_sphere_step_batch.argtypes = [P, U64] + [P] * 17
     L.ref_make_weights.argtypes = [C.c_char_p, U64, U32, U64, U64, P]
     L.ref_walk_stats.argtypes = [D, D, U64, U64, P, P]
+    L.ref_generate_dataset.argtypes = [U64, D, D, D, D, I, D, D, U64, P]
+    L.ref_save_dataset.argtypes = [C.c_char_p, U64, D, D, D, D, I, D, D, U64, P]
     L.ref_make_icosphere.argtypes = [I, D, P, P, P, P]
     L.ref_make_icosphere.restype = None
     L.ref_make_bumpy_sphere.argtypes = [I, D, D, D, P, P, P, P]
@@ -232,3 +234,16 @@ class Scene:
                                     int(nee), seed, n, ptr(pixel), ptr(sample), ptr(channel), ptr(rad),
                                     ptr(seg), C.byref(stats) if stats is not None else None))
         return rad, seg
+
+
+# TrainingSample (dataset.hpp:17-27), 52 bytes, no padding.
+SAMPLE_DTYPE = np.dtype([("sigma_t", "<f4"), ("g", "<f4"), ("phi", "<f4"), ("n_events", "<u4"),
+                         ("cos_theta", "<f4"), ("alpha", "<f4"), ("beta", "<f4"),
+                         ("rep_position", "<f4", (3,)), ("rep_direction", "<f4", (3,))])
+
+
+def generate_dataset(n, sigma=(0.0, 200.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), seed=7):
+    out = np.zeros(n, dtype=SAMPLE_DTYPE)
+    check(lib().ref_generate_dataset(n, sigma[0], sigma[1], g[0], g[1], phi[0], phi[1], phi[2], seed,
+                                     ptr(out)))
+    return out

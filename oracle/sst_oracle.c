@@ -878,3 +878,118 @@ int so_trace_paths(const so_scene* s, so_models* m, int integ, int nee, uint64_t
     }
     return err ? fail(SST_E_RUNTIME, "decoder produced non-finite output twice") : 0;
 }
+
+/* ------------------------------------------------------------------ config 4: dataset */
+#ifndef SO_HG_ARG_ORDER_RTL
+#define SO_HG_ARG_ORDER_RTL 1 /* g++ x86-64 evaluates hg_sample(g, w, rng.uniform(), rng.uniform())
+                                 right to left: u2 is drawn first (pinned by the golden vectors) */
+#endif
+
+/* sphere_exit_t, sphere_walk.cpp:14-18 */
+static double sphere_exit_t(v3 pos, v3 dir, double radius) {
+    const double b = dot(pos, dir);
+    const double c = dot(pos, pos) - radius * radius;
+    return -b + sqrt(fmax(0.0, b * b - c));
+}
+
+typedef struct { v3 p, w; } walk_ev;
+
+/* walk_sphere (sphere_walk.cpp:22-50) with radius 1; events grow in *ev. Returns n or 0 on cap. */
+static uint64_t walk_unit(double sigma_t, double g, so_rng* rng, walk_ev** ev, uint64_t* cap,
+                          v3* exit_pos, v3* exit_dir) {
+    uint64_t n = 0;
+    (*ev)[n].p = V(0.0, 0.0, 0.0);
+    (*ev)[n].w = V(0.0, 0.0, 1.0);
+    ++n;
+    const int vacuum = sigma_t <= 1e-6;
+    v3 pos = V(0.0, 0.0, 0.0), incoming = V(0.0, 0.0, 1.0);
+    for (;;) {
+        double u1, u2;
+#if SO_HG_ARG_ORDER_RTL
+        u2 = so_uniform(rng);
+        u1 = so_uniform(rng);
+#else
+        u1 = so_uniform(rng);
+        u2 = so_uniform(rng);
+#endif
+        const v3 dir = hg_sample(g, incoming, u1, u2);
+        const double step = vacuum ? 2.0 : -log1p(-so_uniform(rng)) / sigma_t;
+        const double t_exit = sphere_exit_t(pos, dir, 1.0);
+        if (vacuum || step >= t_exit) {
+            *exit_pos = add(pos, mul(dir, t_exit));
+            *exit_dir = dir;
+            return n;
+        }
+        pos = add(pos, mul(dir, step));
+        if (n == *cap) {
+            *cap *= 2;
+            *ev = (walk_ev*)realloc(*ev, *cap * sizeof(walk_ev));
+        }
+        (*ev)[n].p = pos;
+        (*ev)[n].w = dir;
+        ++n;
+        incoming = dir;
+        if (n > 1000000) return 0;
+    }
+}
+
+int so_generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi, int phi_kind,
+                        double phi_a, double phi_b, uint64_t seed, uint64_t first, so_sample* out) {
+    if (n == 0) return fail(SST_E_INVALID_ARGUMENT, "generate_dataset: n_samples must be > 0");
+    if (!(s_lo >= 0.0 && s_hi >= s_lo)) return fail(SST_E_INVALID_ARGUMENT, "generate_dataset: invalid sigma_t range");
+    if (!(g_lo >= -1.0 && g_hi <= 1.0 && g_hi >= g_lo)) return fail(SST_E_INVALID_ARGUMENT, "generate_dataset: invalid g range");
+    uint64_t cap = 4096;
+    walk_ev* ev = (walk_ev*)malloc(cap * sizeof(walk_ev));
+    for (uint64_t j = 0; j < n; ++j) {
+        const uint64_t i = first + j;
+        so_rng rng = {so_rng_init(seed, SST_SALT_DATASET, i, 0)};          /* dataset.cpp:59 */
+        const double sigma_t = s_lo + so_uniform(&rng) * (s_hi - s_lo);
+        double g = g_lo + so_uniform(&rng) * (g_hi - g_lo);
+        g = fmin(1.0 - 1e-6, fmax(-(1.0 - 1e-6), g));
+        double phi;                                                        /* PhiSampler::sample */
+        if (phi_kind == 0) phi = 1.0 - pow(10.0, phi_a + so_uniform(&rng) * (phi_b - phi_a));
+        else if (phi_kind == 1) phi = phi_a;
+        else phi = phi_a + so_uniform(&rng) * (phi_b - phi_a);
+        v3 xe, we;
+        const uint64_t ne = walk_unit(sigma_t, g, &rng, &ev, &cap, &xe, &we);
+        if (ne == 0) { free(ev); return fail(SST_E_RUNTIME, "walk_sphere: event cap exceeded"); }
+        /* parameterize_exit, sphere_walk.cpp:52-73 (w_in = (0,0,1), radius 1) */
+        const v3 w_in = V(0.0, 0.0, 1.0);
+        const v3 x_hat = dvs(xe, 1.0);
+        const double ct = dot(w_in, x_hat);
+        v3 e_b, b2;
+        if (fabs(ct) > 1.0 - 1e-9) onb(x_hat, &e_b, &b2);
+        else e_b = normalize(cross(w_in, x_hat));
+        const v3 e_t = cross(e_b, x_hat);
+        /* sample_representative, sphere_walk.cpp:75-102 */
+        uint64_t k = 1;
+        if (phi <= 0.0) {
+            k = 1;
+        } else if (phi >= 1.0) {
+            uint64_t t = (uint64_t)(so_uniform(&rng) * (double)ne);
+            k = 1 + (ne - 1 < t ? ne - 1 : t);
+        } else {
+            const double u = so_uniform(&rng);
+            const double phi_n = exp((double)ne * log(phi));
+            const double target = 1.0 - u * (1.0 - phi_n);
+            k = (uint64_t)ceil(log(target) / log(phi));
+            k = k < 1 ? 1 : (k > ne ? ne : k);
+        }
+        /* rotate by -psi_exit (dataset.cpp:71-74) */
+        const double psi = atan2(xe.y, xe.x);
+        const m3 undo = rotation_z(-psi);
+        const v3 xs = mv(undo, ev[k - 1].p), ws = mv(undo, ev[k - 1].w);
+        so_sample* o = out + j;
+        o->sigma_t = (float)sigma_t;
+        o->g = (float)g;
+        o->phi = (float)phi;
+        o->n_events = (uint32_t)ne;
+        o->cos_theta = (float)ct;
+        o->alpha = (float)dot(we, e_b);
+        o->beta = (float)dot(we, e_t);
+        o->rep_position[0] = (float)xs.x; o->rep_position[1] = (float)xs.y; o->rep_position[2] = (float)xs.z;
+        o->rep_direction[0] = (float)ws.x; o->rep_direction[1] = (float)ws.y; o->rep_direction[2] = (float)ws.z;
+    }
+    free(ev);
+    return 0;
+}

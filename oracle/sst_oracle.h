@@ -70,6 +70,18 @@ int so_trace_paths(const so_scene* s, so_models* m, int integrator, int nee, uin
                    const uint8_t* channel, double* radiance, uint32_t* segments,
                    sst_path_stats* stats);
 
+/* Config 4: training-data generation (dataset.cpp:40-92 generate_dataset,
+ * sphere_walk.cpp:22-102). Record layout = TrainingSample (dataset.hpp:17-27). */
+typedef struct {
+    float sigma_t, g, phi;
+    uint32_t n_events;
+    float cos_theta, alpha, beta;
+    float rep_position[3];
+    float rep_direction[3];
+} so_sample;
+int so_generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi, int phi_kind,
+                        double phi_a, double phi_b, uint64_t seed, uint64_t first_index, so_sample* out);
+
 const char* so_last_error(void);
 
 #ifdef __cplusplus

@@ -91,16 +91,31 @@ class PathStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class DatasetStats(C.Structure):
+    _fields_ = [("walks", U64), ("events", U64), ("replay_events", U64), ("max_events", U64),
+                ("device_ms", D)]
+
+
+# TrainingSample (dataset.hpp:17-27) as a numpy record, 52 bytes.
+try:
+    import numpy as _np
+    SAMPLE_DTYPE = _np.dtype([("sigma_t", "<f4"), ("g", "<f4"), ("phi", "<f4"), ("n_events", "<u4"),
+                              ("cos_theta", "<f4"), ("alpha", "<f4"), ("beta", "<f4"),
+                              ("rep_position", "<f4", (3,)), ("rep_direction", "<f4", (3,))])
+except ImportError:  # pragma: no cover
+    SAMPLE_DTYPE = None
+
+
 # Every symbol include/sst_gpu.h declares (checked by tests/test_abi.py).
 EXPORTED = [
     "sst_gpu_abi_version", "sst_gpu_last_error", "sst_gpu_create", "sst_gpu_destroy",
     "sst_gpu_set_precision", "sst_gpu_get_device", "sst_gpu_stream", "sst_gpu_synchronize",
     "sst_gpu_upload_models", "sst_gpu_load_models_dir", "sst_rng_init",
     "sst_gpu_sphere_step_batch", "sst_gpu_upload_scene", "sst_gpu_scene_info", "sst_gpu_get_sdf", "sst_gpu_render",
-    "sst_gpu_trace_paths", "sst_gpu_read_stats",
+    "sst_gpu_trace_paths", "sst_gpu_read_stats", "sst_gpu_generate_dataset",
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
-    "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm",
+    "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm", "sst_dataset_save",
 ]
 
 _lib = None
@@ -141,6 +156,10 @@ def _declare(L):
     L.sst_gpu_scene_info.argtypes = [P, P, P, P]
     L.sst_gpu_render.argtypes = [P, I, I, U32, U32, U32, U64, P, P, I, C.POINTER(PathStats)]
     L.sst_gpu_read_stats.argtypes = [P, C.POINTER(PathStats)]
+    L.sst_gpu_generate_dataset.argtypes = [P, U64, D, D, D, D, I, D, D, U64, U64, P, I,
+                                           C.POINTER(DatasetStats)]
+    L.sst_dataset_save.argtypes = [C.c_char_p, U64, C.c_float, C.c_float, C.c_float, C.c_float, U32,
+                                   C.c_float, C.c_float, U64, P]
     L.sst_gpu_trace_paths.argtypes = [P, I, I, U64, U64, P, P, P, P, P, C.POINTER(PathStats)]
     L.sst_mesh_icosphere.argtypes = [I, D, P, P, P, P]
     L.sst_mesh_bumpy_sphere.argtypes = [I, D, D, D, P, P, P, P]

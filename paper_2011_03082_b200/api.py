@@ -50,6 +50,13 @@ def _mesh_out(fn, *args):
     return P, T
 
 
+def save_dataset(path, samples, sigma_t, g, phi, seed):
+    """SSWK file (save_dataset, dataset.cpp:94-119) from TrainingSample records."""
+    samples = np.ascontiguousarray(samples, dtype=abi.SAMPLE_DTYPE)
+    abi.check(abi.lib().sst_dataset_save(path.encode(), len(samples), sigma_t[0], sigma_t[1], g[0], g[1],
+                                         int(phi[0]), phi[1], phi[2], seed, _p(samples)))
+
+
 def make_icosphere(subdivisions: int = 3, radius: float = 1.0):
     return _mesh_out(abi.lib().sst_mesh_icosphere, subdivisions, radius)
 
@@ -241,6 +248,17 @@ class Renderer:
         stats = stats if stats is not None else abi.PathStats()
         abi.check(abi.lib().sst_gpu_read_stats(self.h, C.byref(stats)))
         return stats
+
+    # -- config 4: training data (generate_dataset, dataset.cpp:40-92)
+    def generate_dataset(self, n, sigma_t=(0.0, 200.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), seed=7,
+                         first_index=0, stats=None):
+        """TrainingSample records (abi.SAMPLE_DTYPE) for sample indices [first, first + n)."""
+        out = np.zeros(n, dtype=abi.SAMPLE_DTYPE)
+        stats = stats if stats is not None else abi.DatasetStats()
+        abi.check(abi.lib().sst_gpu_generate_dataset(self.h, n, sigma_t[0], sigma_t[1], g[0], g[1],
+                                                     int(phi[0]), phi[1], phi[2], seed, first_index,
+                                                     _p(out), abi.SST_PTR_HOST, C.byref(stats)))
+        return out, stats
 
     def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None):
         pixel = np.ascontiguousarray(pixel, dtype=np.uint32)

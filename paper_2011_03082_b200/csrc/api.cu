@@ -1088,6 +1088,76 @@ int sst_gpu_render(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total
     });
 }
 
+int sst_gpu_generate_dataset(sst_gpu_ctx* ctx, uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi,
+                             int phi_kind, double phi_a, double phi_b, uint64_t seed, uint64_t first,
+                             sst_training_sample* out, int ptr_kind, sst_dataset_stats* stats) {
+    static_assert(sizeof(sst_training_sample) == sizeof(TrainingSampleDev), "sample layout");
+    return guarded([&] {
+        require_device(ctx);
+        // generate_dataset argument checks (dataset.cpp:44-48)
+        if (n == 0) throw InvalidArgument("generate_dataset: n_samples must be > 0");
+        if (!(s_lo >= 0.0 && s_hi >= s_lo)) throw InvalidArgument("generate_dataset: invalid sigma_t range");
+        if (!(g_lo >= -1.0 && g_hi <= 1.0 && g_hi >= g_lo)) throw InvalidArgument("generate_dataset: invalid g range");
+        if (phi_kind < 0 || phi_kind > 2) throw InvalidArgument("unknown PhiSampler kind");
+        if (!out) throw InvalidArgument("null output buffer");
+        if (ptr_kind != SST_PTR_HOST && ptr_kind != SST_PTR_DEVICE) throw InvalidArgument("bad ptr_kind");
+        ensure_pipeline(ctx);
+        join_slots(ctx);
+        const uint64_t chunk = ptr_kind == SST_PTR_DEVICE ? n : std::min<uint64_t>(n, 1ull << 24);
+        DevBuf dout, dmisc;
+        if (ptr_kind == SST_PTR_HOST) dout.reserve(chunk * sizeof(TrainingSampleDev));
+        dmisc.reserve(8 + 8 + 4 * 8);
+        unsigned long long* work = dmisc.as<unsigned long long>();
+        unsigned long long* st = work + 1;
+        int* err = reinterpret_cast<int*>(st + 3);
+        CK(cudaMemsetAsync(dmisc.p, 0, 8 + 8 + 4 * 8, ctx->stream));
+        if (!ctx->ev0) {
+            CK(cudaEventCreate(&ctx->ev0));
+            CK(cudaEventCreate(&ctx->ev1));
+        }
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        for (uint64_t b = 0; b < n; b += chunk) {
+            const uint64_t m = std::min(chunk, n - b);
+            DatasetArgs a{};
+            a.n = m;
+            a.first = first + b;
+            a.s_lo = s_lo;
+            a.s_hi = s_hi;
+            a.g_lo = g_lo;
+            a.g_hi = g_hi;
+            a.phi_kind = phi_kind;
+            a.phi_a = phi_a;
+            a.phi_b = phi_b;
+            a.seed = seed;
+            a.out = ptr_kind == SST_PTR_DEVICE ? reinterpret_cast<TrainingSampleDev*>(out) + b
+                                               : dout.as<TrainingSampleDev>();
+            a.work = work;
+            a.stats = st;
+            a.error = err;
+            CK(cudaMemsetAsync(work, 0, 8, ctx->stream));
+            CK(ctx->precision == SST_PREC_F64 ? f64::launch_dataset(a, ctx->stream) : f32::launch_dataset(a, ctx->stream));
+            if (ptr_kind == SST_PTR_HOST)
+                CK(cudaMemcpyAsync(out + b, dout.p, m * sizeof(TrainingSampleDev), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        unsigned long long hs[3];
+        int herr = 0;
+        CK(cudaMemcpyAsync(hs, st, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&herr, err, sizeof herr, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        if (herr) throw RuntimeError("walk_sphere: event cap exceeded");
+        if (stats) {
+            stats->walks += n;
+            stats->events += hs[0];
+            stats->replay_events += hs[1];
+            stats->max_events = std::max<uint64_t>(stats->max_events, hs[2]);
+            stats->device_ms += ms;
+        }
+    });
+}
+
 int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
                         const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel, double* radiance,
                         uint32_t* segments, sst_path_stats* stats) {
@@ -1202,6 +1272,31 @@ int sst_sdf_load(const char* path, double origin[3], double* voxel, uint32_t dim
 }
 
 void sst_sdf_free(float* values) { std::free(values); }
+
+int sst_dataset_save(const char* path, uint64_t count, float s_lo, float s_hi, float g_lo, float g_hi,
+                     uint32_t phi_kind, float phi_a, float phi_b, uint64_t seed, const void* samples) {
+    return guarded([&] {
+        if (!path || (!samples && count)) throw InvalidArgument("null argument");
+        std::ofstream f(path, std::ios::binary | std::ios::trunc);
+        if (!f) throw RuntimeError(std::string("cannot open for writing: ") + path);
+        auto put = [&](const void* p, size_t n) { f.write(static_cast<const char*>(p), static_cast<std::streamsize>(n)); };
+        const uint32_t version = 1;
+        put("SSWK", 4);
+        put(&version, 4);
+        put(&count, 8);
+        put(&s_lo, 4);
+        put(&s_hi, 4);
+        put(&g_lo, 4);
+        put(&g_hi, 4);
+        put(&phi_kind, 4);
+        put(&phi_a, 4);
+        put(&phi_b, 4);
+        put(&seed, 8);
+        put(samples, count * sizeof(TrainingSampleDev));  // records are the packed little-endian fields
+        f.close();
+        if (!f) throw RuntimeError("write failure on close");
+    });
+}
 
 int sst_image_save_pfm(const char* path, uint32_t w, uint32_t h, const float* rgb) {
     return guarded([&] {

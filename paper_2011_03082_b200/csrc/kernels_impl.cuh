@@ -3,6 +3,7 @@
 // (SST_REAL=double, SST_NS=f64, compiled with -fmad=false).
 #pragma once
 
+#include "dataset.cuh"
 #include "integrator.cuh"
 #include "launch.h"
 
@@ -68,6 +69,10 @@ template <bool ST, bool EXPLICIT>
 __global__ void __launch_bounds__(kTraceBlock, 16) k_trace(TraceArgs<R> a) {
     trace_persistent<R, ST, EXPLICIT>(a);
 }
+
+// ---------------------------------------------------------------------------
+// Config 4: training-data generation (persistent, one sample per lane).
+__global__ void __launch_bounds__(kTraceBlock) k_dataset(DatasetArgs a) { dataset_persistent<R>(a); }
 
 // ---------------------------------------------------------------------------
 // Film accumulation: deterministic fixed-order FP64 sums over the slab's samples.
@@ -138,6 +143,20 @@ cudaError_t launch_trace(const TraceArgs<R>& a, bool st, bool explicit_keys, cud
     if (a.n_paths == 0) return cudaSuccess;
     if (st) return explicit_keys ? launch_trace_t<true, true>(a, s) : launch_trace_t<true, false>(a, s);
     return explicit_keys ? launch_trace_t<false, true>(a, s) : launch_trace_t<false, false>(a, s);
+}
+
+cudaError_t launch_dataset(const DatasetArgs& a, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_dataset, kTraceBlock, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    uint64_t grid = static_cast<uint64_t>(sm_count()) * blocks_per_sm;
+    const uint64_t max_grid = (a.n + kTraceBlock - 1) / kTraceBlock;
+    if (grid > max_grid) grid = max_grid;
+    k_dataset<<<static_cast<unsigned>(grid), kTraceBlock, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_film(const R* radiance, uint64_t stride, uint32_t n_samples, double* sum,

@@ -121,6 +121,29 @@ struct TraceArgs {
     int sphere_batch;           // warp regrouping threshold for sphere steps (lanes)
 };
 
+// TrainingSample (dataset.hpp:17-27): the SSWK record, 52 bytes, no padding.
+struct TrainingSampleDev {
+    float sigma_t, g, phi;
+    uint32_t n_events;
+    float cos_theta, alpha, beta;
+    float rep_position[3];
+    float rep_direction[3];
+};
+static_assert(sizeof(TrainingSampleDev) == 52, "TrainingSample layout");
+
+// Arguments of the dataset kernel (dataset.cuh).
+struct DatasetArgs {
+    uint64_t n, first;
+    double s_lo, s_hi, g_lo, g_hi;
+    int phi_kind;
+    double phi_a, phi_b;
+    uint64_t seed;
+    TrainingSampleDev* out;          // [n]
+    unsigned long long* work;        // sample counter
+    unsigned long long* stats;       // [0] events (pass 1), [1] replayed events, [2] max N
+    int* error;                      // walk exceeded 1e6 events (the reference throws)
+};
+
 // Arguments of the sphere-step batch kernel (C ABI sst_gpu_sphere_step_batch).
 struct StepBatchArgs {
     uint64_t n;
