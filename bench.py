@@ -278,8 +278,10 @@ def bench_ours(args, world, rank, local):
     # dominant kernel: the persistent trace kernel (plus the tiny film sum) of this rank
     achieved = flops / (dev_ms / 1e3) / 1e12
     traffic = load_traffic()
-    chunk = max(1, (1 << 24) // (3 * n_pix))
-    launches_per_step = 2 * math.ceil(S / chunk)
+    per_sample = 3 * n_pix
+    target = min(1 << 24, max(per_sample * S // 8, 1 << 20))
+    chunk = max(1, target // per_sample)
+    launches_per_step = 2 * math.ceil(S / min(chunk, S))
 
     # ---- e2e: the public host-buffer API per step (scene upload + render + film D2H)
     e2e = None
@@ -312,6 +314,29 @@ def bench_ours(args, world, rank, local):
                "h2d_bytes_per_step": int(info["h2d_bytes"]),
                "d2h_bytes_per_step": int(2 * 3 * n_pix * 8),
                "path": "sst_gpu_upload_scene + sst_gpu_render(SST_PTR_HOST) per step"}
+
+    # ---- secondary configs (rank 0, single GPU work; not the headline metric)
+    extra = None
+    if rank == 0 and not args.no_extra:
+        extra = {}
+        mesh = sb.make_icosphere(3, 1.0)
+        for name, integ in (("c1_st_nee", sb.ST), ("c2_pt_nee", sb.PT)):
+            r.upload_scene(sb.c1_scene(mesh, 256, 256))
+            r.render_film(integ, 64, 1, True, 0, 8)  # warm-up
+            est = abi.PathStats()
+            r.render_film(integ, 64, 1, True, 0, 64, stats=est)
+            extra[name] = {"frame": "256x256 @ 64 spp", "frame_ms": est.device_ms,
+                           "segments_per_s": est.segments / (est.device_ms / 1e3),
+                           "segments_per_path": est.segments / est.paths}
+        dst = abi.DatasetStats()
+        out, _ = r.generate_dataset(200000, seed=7)  # warm-up
+        dst = abi.DatasetStats()
+        r.generate_dataset(2000000, seed=7, first_index=200000, stats=dst)
+        extra["c4_dataset"] = {"walks_per_s": dst.walks / (dst.device_ms / 1e3),
+                               "events_per_s": dst.events / (dst.device_ms / 1e3),
+                               "time_1e8_walks_s": 1e8 / (dst.walks / (dst.device_ms / 1e3)),
+                               "sample": "2e6 walks, sigma_t U[0,200], g U[-1,1], phi 1-10^U[-5,-0.5]"}
+        r.upload_scene(scene)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -347,6 +372,7 @@ def bench_ours(args, world, rank, local):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
+            "extra": extra,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -365,6 +391,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -722,7 +722,12 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
     const uint32_t n_pix = ctx->desc.width * ctx->desc.height;
     const uint64_t per_sample = 3ull * n_pix;
     const uint32_t n_samples = s1 - s0;
-    uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, kChunkPaths / per_sample));
+    // chunk: <= 2^24 paths, and at least ~8 chunks per call when the call is big
+    // enough (>= 2^20 paths per chunk) so the long-path tail of one launch overlaps
+    // the next ones on the pipeline slots
+    uint64_t target = std::min<uint64_t>(kChunkPaths, std::max<uint64_t>(per_sample * n_samples / 8, 1ull << 20));
+    if (const char* e = std::getenv("SST_CHUNK_PATHS")) target = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+    uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, target / per_sample));
     if (chunk > n_samples) chunk = n_samples;
     ensure_pipeline(ctx);
     const bool sync = ptr_kind == SST_PTR_HOST || stats != nullptr;

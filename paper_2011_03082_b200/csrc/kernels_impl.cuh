@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(128) k_step_batch(StepBatchArgs a) {
 // ---------------------------------------------------------------------------
 // Persistent path-tracing megakernel (PT or ST; render ids or explicit keys).
 template <bool ST, bool EXPLICIT>
-__global__ void __launch_bounds__(kTraceBlock, 16) k_trace(TraceArgs<R> a) {
+__global__ void __launch_bounds__(kTraceBlock, ST ? 16 : 24) k_trace(TraceArgs<R> a) {
     trace_persistent<R, ST, EXPLICIT>(a);
 }
 
