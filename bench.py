@@ -376,6 +376,8 @@ def bench_ours(args, world, rank, local):
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()  # rank 0 may still be on the extras / JSON line
     r.close()
     if dist:
         dist.destroy_process_group()
