@@ -278,6 +278,7 @@ def bench_ours(args, world, rank, local):
     # dominant kernel: the persistent trace kernel (plus the tiny film sum) of this rank
     achieved = flops / (dev_ms / 1e3) / 1e12
     traffic = load_traffic()
+    hbm_bytes = paths_all * 8.0 + args.steps * world * 3 * n_pix * 32.0
     per_sample = 3 * n_pix
     target = min(1 << 24, max(per_sample * S // 8, 1 << 20))
     chunk = max(1, target // per_sample)
@@ -359,6 +360,7 @@ def bench_ours(args, world, rank, local):
                 "l2": "flushed between steps by a 256 MB device write (scene is L2-resident by design)",
                 "parallelism": f"sample slabs per rank x{world}" + (" + NCCL film reduce" if world > 1 else ""),
                 "bvh_nodes": info["bvh_nodes"], "triangles": info["triangles"],
+                "paths_per_s": paths_all / (ms / 1e3),
             },
             "roofline": {
                 "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -368,6 +370,9 @@ def bench_ours(args, world, rank, local):
                 "achieved_def": "decoder MLP FLOPs 2*(112 nL + 480 nP + 640 nE) from device decode counters / "
                                 "CUDA-event time of the render launches on the context stream",
                 "peak_source": "measured FFMA throughput (csrc/peak.cu) on this GPU; MEASURED_PEAKS.json has no FP32 figure",
+                "hbm": {"algorithmic_bytes_per_s": hbm_bytes / (ms / 1e3),
+                        "frac_of_measured": hbm_bytes / (ms / 1e3) / 6551.7e9,
+                        "def": "per path 4 B radiance write + 4 B film read; film 2x8 B RMW per pixel-channel per slab"},
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
