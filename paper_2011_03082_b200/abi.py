@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsst_gpu.so")
+# SST_GPU_LIB overrides the library path (A/B builds of the same ABI); no CPU fallback either way.
+LIB_PATH = os.environ.get("SST_GPU_LIB") or os.path.join(HERE, "libsst_gpu.so")
 
 SST_OK = 0
 SST_E_INVALID_ARGUMENT = 1
