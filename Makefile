@@ -33,6 +33,11 @@ $(BUILD)/kernels_f64.o: $(CSRC)/kernels_f64.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -fmad=false -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_f64.log || (cat $(BUILD)/ptxas_f64.log; false)
 
+# CVAE training (FP64, reference operation order): no FMA contraction either.
+$(BUILD)/train.o: $(CSRC)/train.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -fmad=false -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_train.log || (cat $(BUILD)/ptxas_train.log; false)
+
 $(BUILD)/api.o: $(CSRC)/api.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
@@ -41,7 +46,7 @@ $(BUILD)/host.o: $(CSRC)/host.cpp $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
-$(LIB): $(BUILD)/kernels_f32.o $(BUILD)/kernels_f64.o $(BUILD)/api.o $(BUILD)/host.o
+$(LIB): $(BUILD)/kernels_f32.o $(BUILD)/kernels_f64.o $(BUILD)/train.o $(BUILD)/api.o $(BUILD)/host.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 oracle:

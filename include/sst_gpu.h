@@ -293,6 +293,76 @@ int sst_gpu_generate_dataset(sst_gpu_ctx* ctx, uint64_t n, double sigma_t_lo, do
                              uint64_t seed, uint64_t first_index, sst_training_sample* out,
                              int ptr_kind, sst_dataset_stats* stats);
 
+/* ------------------------------------------------------------------------ */
+/* CVAE training: the device form of train_model            */
+/* (cvae.cpp:234-347) -- minibatch AdamW on the ELBO (cvae.cpp:117-183,          */
+/* mlp.cpp:100-228), FP64 like the reference. Same init (make_cvae, cvae.cpp:79-91),*/
+/* validation split, per-epoch shuffle and per-sample latent noise streams       */
+/* (RandomStream salts kTrainInit/Shuffle/Latent/Split, rng.hpp:55-58), the same   */
+/* per-sample operation order and the same in-order batch gradient sums.         */
+/* ------------------------------------------------------------------------ */
+
+/* TrainConfig (cvae.hpp:101-114); depth/width/latent <= 0 keep the production  */
+/* default of the model kind (CvaeSpec::production_default, cvae.cpp:51-57).     */
+typedef struct {
+    double lr;
+    uint32_t batch_size;
+    uint32_t epochs;
+    double weight_decay;
+    uint64_t seed;
+    double validation_fraction;
+    int32_t depth, width, latent;
+} sst_train_config;
+
+/* EpochStats (cvae.hpp:116-119). */
+typedef struct {
+    double train_loss;
+    double validation_loss;
+} sst_epoch_stats;
+
+typedef struct {
+    uint64_t steps;              /* AdamW steps taken (finite batches) */
+    uint64_t rejected_batches;   /* batches skipped for a non-finite loss */
+    uint64_t sample_passes;      /* training-sample forward+backward passes */
+    uint32_t encoder_params, decoder_params;
+    uint64_t dataset_fingerprint;  /* Dataset::fingerprint (dataset.cpp:32-38) */
+    double device_ms;
+} sst_train_stats;
+
+/* The reference defaults (lr 1e-3, batch 512, 100 epochs, wd 1e-4, seed 1, 5% validation). */
+void sst_train_config_default(sst_train_config* cfg);
+
+/* train_model(kind, dataset, cfg) for kind 0 = LengthGen, 1 = PathGen, 2 = EventGen.
+ * `samples` (host or device per ptr_kind) holds the n TrainingSample records of a
+ * dataset whose header seed is `dataset_seed` (only used for the model's dataset
+ * fingerprint). `epochs` (may be NULL) receives cfg->epochs EpochStats. When
+ * `ssnn_path` is non-NULL the trained model is written with save_model
+ * (cvae.cpp:349-377; encoder included iff include_encoder). `params_out` (may be
+ * NULL) receives the f32-quantised encoder then decoder parameters as doubles in
+ * flatten_parameters order (mlp.cpp:230-238). When `install` is non-zero the
+ * trained decoder replaces the context's decoder of that kind (like
+ * ScatterModels::load_dir on the saved files).
+ * Errors mirror the reference: SST_E_INVALID_ARGUMENT for TrainConfig::validate /
+ * CvaeSpec::validate / empty data / no training samples left, SST_E_RUNTIME when
+ * every batch of an epoch is non-finite ("diverged") or the file cannot be
+ * written; SST_E_INVALID_ARGUMENT also for specs beyond the device kernel's
+ * limits (depth <= 4, width <= 32, latent <= 16). */
+int sst_gpu_train_model(sst_gpu_ctx* ctx, int kind, const sst_training_sample* samples, uint64_t n,
+                        int ptr_kind, uint64_t dataset_seed, const sst_train_config* cfg,
+                        sst_epoch_stats* epochs, const char* ssnn_path, int include_encoder,
+                        double* params_out, int install, sst_train_stats* stats);
+
+/* The three decoders of a ScatterModels bundle (LengthGen, PathGen, EventGen) trained
+ * CONCURRENTLY on one dataset and config (each kind on its own stream and cluster;
+ * results identical to three sst_gpu_train_model calls). `epochs` (may be NULL) is
+ * [3][cfg->epochs]; `stats` (may be NULL) is [3]. With out_dir non-NULL the models
+ * are written as out_dir/{lengthgen,pathgen,eventgen}.ssnn (the layout
+ * ScatterModels::load_dir reads, scatter.cpp:29-32); install != 0 makes them the
+ * context's decoders. */
+int sst_gpu_train_models(sst_gpu_ctx* ctx, const sst_training_sample* samples, uint64_t n, int ptr_kind,
+                         uint64_t dataset_seed, const sst_train_config* cfg, sst_epoch_stats* epochs,
+                         const char* out_dir, int include_encoder, int install, sst_train_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

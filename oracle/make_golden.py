@@ -27,6 +27,14 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 MODELS = os.path.join(GOLD, "models")
 
 
+# (name, kind, TrainConfig overrides) -- trained on the ds_a records (2000 samples, seed 11)
+TRAIN_CASES = [("len", 0, dict(epochs=3, batch_size=64, seed=1)),
+               ("path", 1, dict(epochs=3, batch_size=64, seed=1)),
+               ("event", 2, dict(epochs=3, batch_size=64, seed=1)),
+               ("path_custom", 1, dict(epochs=2, batch_size=100, seed=5, lr=3e-3, weight_decay=1e-3,
+                                        validation_fraction=0.1, depth=3, width=12, latent=1))]
+
+
 def step_inputs(n, seed):
     rng = np.random.default_rng(seed)
     sig = np.concatenate([rng.uniform(0, 200, n - 8), [0.0, 0.0, 1e-3, 50.0, 50.0, 200.0, 10.0, 10.0]])
@@ -138,6 +146,16 @@ def main():
     reflib.check(reflib.lib().ref_save_dataset(path.encode(), 300, 0.0, 200.0, -1.0, 1.0, 0, -5.0, -0.5, 12,
                                                ds_b.ctypes.data_as(C.c_void_p)))
     out["ds_b_sswk"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+    # --- CVAE training (cvae.cpp:234-347) on ds_a: SSNN bytes (save_model with encoder),
+    # epoch stats and the f32-quantised parameters, for the three production specs and
+    # one overridden spec / config.
+    for name, kind, cfg in TRAIN_CASES:
+        d = os.path.join("/tmp", f"golden_{name}.ssnn")
+        params, ep, fp = reflib.train_model(kind, ds_a, dataset_seed=11, path=d, **cfg)
+        blob = open(d, "rb").read()
+        out[f"train_{name}_ssnn"] = np.frombuffer(blob, np.uint8)
+        out[f"train_{name}_epochs"] = ep
+        out[f"train_{name}_fingerprint"] = np.array([fp], np.uint64)
     np.savez_compressed(os.path.join(GOLD, "reference_golden.npz"), **out)
     sz = os.path.getsize(os.path.join(GOLD, "reference_golden.npz"))
     print(f"wrote tests/golden/reference_golden.npz ({sz / 1e6:.2f} MB, {len(out)} arrays)")

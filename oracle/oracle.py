@@ -57,6 +57,9 @@ def lib():
         L.so_scene_free.restype = None
         L.so_bvh_intersect.argtypes = [P, P, P, D, D, P, P]
         L.so_generate_dataset.argtypes = [U64, D, D, D, D, I, D, D, U64, U64, P]
+        L.so_train_model.argtypes = [I, P, U64, P, P, P]
+        L.so_dataset_fingerprint.argtypes = [P, U64, U64]
+        L.so_dataset_fingerprint.restype = U64
         L.so_trace_paths.argtypes = [P, P, I, I, U64, U64, P, P, P, P, P, C.POINTER(abi.PathStats)]
     return _lib
 
@@ -205,3 +208,18 @@ def generate_dataset(n, sigma=(0.0, 200.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), 
     check(lib().so_generate_dataset(n, sigma[0], sigma[1], g[0], g[1], phi[0], phi[1], phi[2], seed,
                                     first, ptr(out)))
     return out
+
+
+def train_model(kind, samples, **cfg):
+    """train_model restatement -> (params [enc+dec] f64 quantised, epoch stats [E, 2])."""
+    c = abi.TrainConfig(**cfg)
+    samples = np.ascontiguousarray(samples, dtype=SAMPLE_DTYPE)
+    ep = np.zeros((c.epochs, 2))
+    params = np.zeros(1 << 16)
+    check(lib().so_train_model(kind, ptr(samples), len(samples), C.byref(c), ptr(ep), ptr(params)))
+    return params, ep
+
+
+def dataset_fingerprint(samples, seed):
+    samples = np.ascontiguousarray(samples, dtype=SAMPLE_DTYPE)
+    return int(lib().so_dataset_fingerprint(ptr(samples), len(samples), seed))

@@ -229,6 +229,43 @@ int ref_generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, doub
     });
 }
 
+// train_model (cvae.cpp:234-347) on n TrainingSample records; writes the SSNN file
+// (save_model, cvae.cpp:349-377) when path != NULL, the per-epoch stats, and the
+// f32-quantised encoder+decoder parameters in flatten_parameters order.
+int ref_train_model(int kind, const void* samples, uint64_t n, uint64_t dataset_seed,
+                    const sst_train_config* c, const char* path, int include_encoder,
+                    sst_epoch_stats* epochs, double* params_out, uint64_t* fingerprint) {
+    return guarded([&] {
+        Dataset ds;
+        ds.header.count = n;
+        ds.header.seed = dataset_seed;
+        ds.samples.resize(n);
+        std::memcpy(ds.samples.data(), samples, n * sizeof(TrainingSample));
+        TrainConfig cfg;
+        cfg.lr = c->lr;
+        cfg.batch_size = c->batch_size;
+        cfg.epochs = c->epochs;
+        cfg.weight_decay = c->weight_decay;
+        cfg.seed = c->seed;
+        cfg.validation_fraction = c->validation_fraction;
+        cfg.depth = c->depth;
+        cfg.width = c->width;
+        cfg.latent = c->latent;
+        const TrainResult res = train_model(static_cast<ModelKind>(kind), ds, cfg);
+        if (epochs)
+            for (size_t e = 0; e < res.epochs.size(); ++e)
+                epochs[e] = {res.epochs[e].train_loss, res.epochs[e].validation_loss};
+        if (params_out) {
+            const auto a = flatten_parameters(res.model.encoder);
+            const auto b = flatten_parameters(res.model.decoder);
+            std::memcpy(params_out, a.data(), a.size() * sizeof(double));
+            std::memcpy(params_out + a.size(), b.data(), b.size() * sizeof(double));
+        }
+        if (fingerprint) *fingerprint = res.model.dataset_fingerprint;
+        if (path) save_model(path, res.model, include_encoder != 0);
+    });
+}
+
 // save_dataset (dataset.cpp:94-119) of n records (for SSWK byte-compatibility tests).
 int ref_save_dataset(const char* path, uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi,
                      int phi_kind, double phi_a, double phi_b, uint64_t seed, const void* samples) {

@@ -66,6 +66,7 @@ def _declare(L):
     L.ref_make_weights.argtypes = [C.c_char_p, U64, U32, U64, U64, P]
     L.ref_walk_stats.argtypes = [D, D, U64, U64, P, P]
     L.ref_generate_dataset.argtypes = [U64, D, D, D, D, I, D, D, U64, P]
+    L.ref_train_model.argtypes = [I, P, U64, U64, P, C.c_char_p, I, P, P, P]
     L.ref_save_dataset.argtypes = [C.c_char_p, U64, D, D, D, D, I, D, D, U64, P]
     L.ref_make_icosphere.argtypes = [I, D, P, P, P, P]
     L.ref_make_icosphere.restype = None
@@ -247,3 +248,19 @@ def generate_dataset(n, sigma=(0.0, 200.0), g=(-1.0, 1.0), phi=(0, -5.0, -0.5), 
     check(lib().ref_generate_dataset(n, sigma[0], sigma[1], g[0], g[1], phi[0], phi[1], phi[2], seed,
                                      ptr(out)))
     return out
+
+
+def train_model(kind, samples, dataset_seed=7, path=None, include_encoder=True, **cfg):
+    """train_model (cvae.cpp:234-347) -> (params f64 [enc+dec], epoch stats [E,2], fingerprint)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_2011_03082_b200 import abi
+    c = abi.TrainConfig(**cfg)
+    samples = np.ascontiguousarray(samples)
+    ep = np.zeros((c.epochs, 2))
+    params = np.zeros(1 << 16)
+    fp = C.c_uint64()
+    check(lib().ref_train_model(kind, ptr(samples), len(samples), dataset_seed, C.byref(c),
+                                path.encode() if path else None, int(include_encoder), ptr(ep),
+                                ptr(params), C.byref(fp)))
+    return params, ep, fp.value

@@ -993,3 +993,296 @@ int so_generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, doubl
     free(ev);
     return 0;
 }
+
+/* ------------------------------------------------------------------ CVAE training
+ * train_model (cvae.cpp:234-347) restated in plain C: make_cvae (cvae.cpp:79-91) with
+ * make_mlp / make_gaussian_mlp (mlp.cpp:32-58), the ELBO forward / backward
+ * (elbo_forward + cvae_elbo_loss_grad, cvae.cpp:117-183) over mlp_forward_trace /
+ * mlp_backward (mlp.cpp:100-183), gaussian_kl / gaussian_loglik / reparameterize
+ * (mlp.cpp:185-212) and adamw_step (mlp.cpp:214-228). Parameters are kept flat in
+ * flatten_parameters order (per layer: weights row-major [out][in], then bias). */
+#define SO_TMAX 64 /* widest layer this restatement handles */
+typedef struct {
+    uint32_t n;
+    uint32_t in[8], out[8];
+    size_t woff[8];
+    size_t count;
+} so_mlp;
+
+static void so_mlp_shape(so_mlp* m, uint32_t input, uint32_t output, uint32_t depth, uint32_t width) {
+    uint32_t in = input;
+    size_t off = 0;
+    m->n = depth + 1;
+    for (uint32_t d = 0; d <= depth; ++d) {
+        const uint32_t out = d == depth ? output : width;
+        m->in[d] = in;
+        m->out[d] = out;
+        m->woff[d] = off;
+        off += (size_t)in * out + out;
+        in = out;
+    }
+    m->count = off;
+}
+
+/* make_gaussian_mlp: Glorot-uniform weights, zero bias, log-variance head bias -2 (mlp.hpp:43-44). */
+static void so_mlp_init(const so_mlp* m, double* p, uint32_t p_out, so_rng* rng) {
+    for (uint32_t l = 0; l < m->n; ++l) {
+        const double bound = sqrt(6.0 / ((double)m->in[l] + m->out[l]));
+        double* w = p + m->woff[l];
+        for (size_t i = 0; i < (size_t)m->in[l] * m->out[l]; ++i) {
+            const double u = so_uniform(rng);
+            w[i] = -bound + u * (bound - -bound);
+        }
+        double* b = w + (size_t)m->in[l] * m->out[l];
+        for (uint32_t r = 0; r < m->out[l]; ++r) b[r] = (l + 1 == m->n && r >= p_out) ? -2.0 : 0.0;
+    }
+    for (size_t i = 0; i < m->count; ++i) p[i] = (double)(float)p[i]; /* quantize_f32, mlp.cpp:25-30 */
+}
+
+static double so_softplus_derivative(double x) { /* mlp.cpp:64-68 */
+    if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+    const double e = exp(x);
+    return e / (1.0 + e);
+}
+
+/* mlp_forward_trace: xs[l] = input of layer l (xs[n] = output), pre[l] = pre-activations. */
+static void so_mlp_fwd(const so_mlp* m, const double* p, double xs[][SO_TMAX], double pre[][SO_TMAX]) {
+    for (uint32_t l = 0; l < m->n; ++l) {
+        const double* w = p + m->woff[l];
+        const double* b = w + (size_t)m->in[l] * m->out[l];
+        for (uint32_t r = 0; r < m->out[l]; ++r) {
+            double acc = b[r];
+            for (uint32_t c = 0; c < m->in[l]; ++c) acc += w[(size_t)r * m->in[l] + c] * xs[l][c];
+            pre[l][r] = acc;
+            xs[l + 1][r] = (l + 1 == m->n) ? acc : so_softplus(acc);
+        }
+    }
+}
+
+/* mlp_backward: accumulates into g (flat, same layout as p); input_grad may be NULL. */
+static void so_mlp_bwd(const so_mlp* m, const double* p, double xs[][SO_TMAX], double pre[][SO_TMAX],
+                       const double* upstream, double* g, double* input_grad) {
+    double delta[SO_TMAX], prev[SO_TMAX];
+    memcpy(delta, upstream, m->out[m->n - 1] * sizeof(double));
+    for (uint32_t li = m->n; li-- > 0;) {
+        const uint32_t in = m->in[li], out = m->out[li];
+        const double* w = p + m->woff[li];
+        double* gw = g + m->woff[li];
+        double* gb = gw + (size_t)in * out;
+        if (li + 1 != m->n)
+            for (uint32_t r = 0; r < out; ++r) delta[r] *= so_softplus_derivative(pre[li][r]);
+        for (uint32_t r = 0; r < out; ++r) {
+            gb[r] += delta[r];
+            for (uint32_t c = 0; c < in; ++c) gw[(size_t)r * in + c] += delta[r] * xs[li][c];
+        }
+        if (li > 0 || input_grad) {
+            for (uint32_t c = 0; c < in; ++c) prev[c] = 0.0;
+            for (uint32_t r = 0; r < out; ++r)
+                for (uint32_t c = 0; c < in; ++c) prev[c] += w[(size_t)r * in + c] * delta[r];
+            memcpy(delta, prev, in * sizeof(double));
+        }
+    }
+    if (input_grad) memcpy(input_grad, delta, m->in[0] * sizeof(double));
+}
+
+static double so_clamp_lv(double lv) { return fmin(10.0, fmax(-10.0, lv)); } /* cvae.cpp:22 */
+
+typedef struct {
+    uint32_t p_in, p_out, depth, width, latent;
+} so_spec;
+
+/* One ELBO evaluation (cvae_elbo_loss / cvae_elbo_loss_grad). */
+static double so_elbo(const so_spec* s, const so_mlp* me, const so_mlp* md, const double* pe, const double* pd,
+                      const double* x, const double* c, const double* eps, double* ge, double* gd) {
+    double xe[8][SO_TMAX], pre_e[8][SO_TMAX], xd[8][SO_TMAX], pre_d[8][SO_TMAX];
+    const uint32_t L = s->latent, P = s->p_out;
+    for (uint32_t i = 0; i < P; ++i) xe[0][i] = x[i];
+    for (uint32_t i = 0; i < s->p_in; ++i) xe[0][P + i] = c[i];
+    so_mlp_fwd(me, pe, xe, pre_e);
+    const double* oe = xe[me->n];
+    double mu_e[SO_TMAX], lv_e[SO_TMAX];
+    for (uint32_t i = 0; i < L; ++i) {
+        mu_e[i] = oe[i];
+        lv_e[i] = so_clamp_lv(oe[L + i]);
+        xd[0][i] = mu_e[i] + exp(0.5 * lv_e[i]) * eps[i]; /* reparameterize, mlp.cpp:204-212 */
+    }
+    for (uint32_t i = 0; i < s->p_in; ++i) xd[0][L + i] = c[i];
+    so_mlp_fwd(md, pd, xd, pre_d);
+    const double* od = xd[md->n];
+    double kl = 0.0, ll = 0.0;
+    for (uint32_t i = 0; i < L; ++i) kl += mu_e[i] * mu_e[i] + exp(lv_e[i]) - 1.0 - lv_e[i];
+    kl = 0.5 * kl;
+    for (uint32_t i = 0; i < P; ++i) {
+        const double lv = so_clamp_lv(od[P + i]);
+        const double d = x[i] - od[i];
+        ll += -0.91893853320467274178 - 0.5 * lv - d * d / (2.0 * exp(lv));
+    }
+    const double loss = kl - ll;
+    if (!ge) return loss;
+    double up_d[2 * SO_TMAX], din[SO_TMAX], up_e[2 * SO_TMAX];
+    for (uint32_t i = 0; i < P; ++i) {
+        const double lv = so_clamp_lv(od[P + i]);
+        const double inv_var = exp(-lv);
+        const double d = x[i] - od[i];
+        up_d[i] = -d * inv_var;
+        up_d[P + i] = fabs(lv) >= 10.0 ? 0.0 : 0.5 - 0.5 * d * d * inv_var;
+    }
+    so_mlp_bwd(md, pd, xd, pre_d, up_d, gd, din);
+    for (uint32_t i = 0; i < L; ++i) {
+        const double dz = din[i];
+        up_e[i] = mu_e[i] + dz;
+        const double dlv_kl = 0.5 * (exp(lv_e[i]) - 1.0);
+        const double dlv_rep = dz * 0.5 * exp(0.5 * lv_e[i]) * eps[i];
+        up_e[L + i] = fabs(lv_e[i]) >= 10.0 ? 0.0 : dlv_kl + dlv_rep;
+    }
+    so_mlp_bwd(me, pe, xe, pre_e, up_e, ge, NULL);
+    return loss;
+}
+
+static void so_adamw(double* p, double* m, double* v, const double* g, size_t n, uint64_t t, double lr, double wd) {
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8; /* AdamWConfig, mlp.hpp:95-101 */
+    const double bc1 = 1.0 - pow(b1, (double)t), bc2 = 1.0 - pow(b2, (double)t);
+    for (size_t i = 0; i < n; ++i) {
+        m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+        v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+        const double mh = m[i] / bc1, vh = v[i] / bc2;
+        p[i] -= lr * (mh / (sqrt(vh) + eps) + wd * p[i]);
+    }
+}
+
+static void so_shuffle(uint32_t* v, size_t n, so_rng* rng) {
+    for (size_t i = n; i > 1; --i) {
+        const size_t j = (size_t)(so_uniform(rng) * (double)i);
+        const uint32_t t = v[i - 1];
+        v[i - 1] = v[j];
+        v[j] = t;
+    }
+}
+
+uint64_t so_dataset_fingerprint(const so_sample* s, uint64_t n, uint64_t seed) { /* dataset.cpp:32-38 */
+    uint64_t h = 0xCBF29CE484222325ULL;
+    const uint32_t version = 1;
+    const unsigned char* parts[4] = {(const unsigned char*)&version, (const unsigned char*)&n,
+                                     (const unsigned char*)&seed, (const unsigned char*)s};
+    const size_t lens[4] = {4, 8, 8, (size_t)n * sizeof(so_sample)};
+    for (int k = 0; k < 4; ++k)
+        for (size_t i = 0; i < lens[k]; ++i) {
+            h ^= parts[k][i];
+            h *= 0x100000001B3ULL;
+        }
+    return h;
+}
+
+int so_train_model(int kind, const so_sample* samples, uint64_t n, const sst_train_config* cfg,
+                   sst_epoch_stats* epochs, double* params_out) {
+    if (!(cfg->lr > 0.0)) return fail(SST_E_INVALID_ARGUMENT, "TrainConfig: lr must be > 0");
+    if (cfg->batch_size == 0) return fail(SST_E_INVALID_ARGUMENT, "TrainConfig: batch_size must be > 0");
+    if (cfg->epochs == 0) return fail(SST_E_INVALID_ARGUMENT, "TrainConfig: epochs must be > 0");
+    if (!(cfg->weight_decay >= 0.0)) return fail(SST_E_INVALID_ARGUMENT, "TrainConfig: negative weight decay");
+    if (!(cfg->validation_fraction >= 0.0 && cfg->validation_fraction < 1.0))
+        return fail(SST_E_INVALID_ARGUMENT, "TrainConfig: validation fraction out of range");
+    if (n == 0) return fail(SST_E_INVALID_ARGUMENT, "train_model: empty dataset");
+    static const so_spec defaults[3] = {{2, 1, 2, 8, 2}, {3, 3, 2, 16, 5}, {7, 6, 2, 16, 5}}; /* cvae.cpp:51-57 */
+    if (kind < 0 || kind > 2) return fail(SST_E_INVALID_ARGUMENT, "unknown model kind");
+    so_spec s = defaults[kind];
+    if (cfg->depth > 0) s.depth = (uint32_t)cfg->depth;
+    if (cfg->width > 0) s.width = (uint32_t)cfg->width;
+    if (cfg->latent > 0) s.latent = (uint32_t)cfg->latent;
+    if ((s.p_in + s.latent) % 4 != 0)
+        return fail(SST_E_INVALID_ARGUMENT, "CvaeSpec: p_in + latent must be a multiple of four");
+    if (s.depth > 6 || s.width > SO_TMAX || 2 * s.latent > SO_TMAX)
+        return fail(SST_E_INVALID_ARGUMENT, "oracle: spec too large");
+    so_mlp me, md;
+    so_mlp_shape(&me, s.p_out + s.p_in, 2 * s.latent, s.depth, s.width);
+    so_mlp_shape(&md, s.latent + s.p_in, 2 * s.p_out, s.depth, s.width);
+    const size_t ne = me.count, nd = md.count;
+    double* buf = (double*)calloc(5 * (ne + nd), sizeof(double));
+    double *pe = buf, *pd = pe + ne, *ge = pd + nd, *gd = ge + ne, *me_ = gd + nd, *md_ = me_ + ne,
+           *ve = md_ + nd, *vd = ve + ne;
+    so_rng init = {so_rng_init(cfg->seed, 0x02, (uint64_t)kind, 0)}; /* kTrainInit */
+    so_mlp_init(&me, pe, s.latent, &init);
+    so_mlp_init(&md, pd, s.p_out, &init);
+    /* targets / conditions (cvae.cpp:185-212), NormConstants sigma_ref 200, n_ref 1e4 */
+    const uint32_t P = s.p_out, C = s.p_in;
+    double* X = (double*)malloc((size_t)n * (P + C) * sizeof(double));
+    double* Cn = X + (size_t)n * P;
+    for (uint64_t i = 0; i < n; ++i) {
+        const so_sample* t = samples + i;
+        const double ns = log1p(fmax(0.0, (double)t->sigma_t)) / log1p(200.0);
+        const double nn = log(fmax(1.0, (double)t->n_events)) / log(1e4);
+        double* x = X + i * P;
+        double* c = Cn + i * C;
+        if (kind == 0) {
+            x[0] = nn; c[0] = ns; c[1] = t->g;
+        } else if (kind == 1) {
+            x[0] = t->cos_theta; x[1] = t->alpha; x[2] = t->beta;
+            c[0] = ns; c[1] = t->g; c[2] = nn;
+        } else {
+            for (int k = 0; k < 3; ++k) { x[k] = t->rep_position[k]; x[3 + k] = t->rep_direction[k]; }
+            c[0] = ns; c[1] = t->g; c[2] = t->phi; c[3] = t->cos_theta; c[4] = t->alpha; c[5] = t->beta; c[6] = nn;
+        }
+    }
+    uint32_t* order = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+    for (uint64_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
+    so_rng split = {so_rng_init(cfg->seed, 0x05, 0, 0)}; /* kTrainSplit */
+    so_shuffle(order, n, &split);
+    const size_t n_val = (size_t)(cfg->validation_fraction * (double)n);
+    uint32_t* val = order;
+    uint32_t* tr = order + n_val;
+    const size_t n_tr = n - n_val;
+    int rc = 0;
+    if (n_tr == 0) {
+        rc = fail(SST_E_INVALID_ARGUMENT, "train_model: no training samples left");
+        goto done;
+    }
+    uint64_t t = 0;
+    double eps[SO_TMAX];
+    for (uint32_t e = 0; e < cfg->epochs; ++e) {
+        so_rng sh = {so_rng_init(cfg->seed, 0x03, e, 0)}; /* kTrainShuffle */
+        so_shuffle(tr, n_tr, &sh);
+        double epoch_loss = 0.0;
+        size_t epoch_samples = 0, finite = 0;
+        for (size_t start = 0; start < n_tr; start += cfg->batch_size) {
+            const size_t end = start + cfg->batch_size < n_tr ? start + cfg->batch_size : n_tr;
+            memset(ge, 0, (ne + nd) * sizeof(double));
+            double bl = 0.0;
+            for (size_t b = start; b < end; ++b) {
+                const uint32_t i = tr[b];
+                so_rng er = {so_rng_init(cfg->seed, 0x04, e, i)}; /* kTrainLatent */
+                for (uint32_t k = 0; k < s.latent; ++k) eps[k] = so_normal(&er);
+                bl += so_elbo(&s, &me, &md, pe, pd, X + (size_t)i * P, Cn + (size_t)i * C, eps, ge, gd);
+            }
+            const double inv = 1.0 / (double)(end - start);
+            if (!isfinite(bl)) continue;
+            ++finite;
+            epoch_loss += bl;
+            epoch_samples += end - start;
+            for (size_t k = 0; k < ne + nd; ++k) ge[k] *= inv;
+            ++t;
+            so_adamw(pe, me_, ve, ge, ne, t, cfg->lr, cfg->weight_decay);
+            so_adamw(pd, md_, vd, gd, nd, t, cfg->lr, cfg->weight_decay);
+        }
+        if (finite == 0) {
+            rc = fail(SST_E_RUNTIME, "train_model: diverged, every batch non-finite");
+            goto done;
+        }
+        const double train_loss = epoch_loss / (double)(epoch_samples ? epoch_samples : 1);
+        double vl = 0.0;
+        for (size_t k = 0; k < n_val; ++k) {
+            so_rng er = {so_rng_init(cfg->seed, 0x04, e, val[k])};
+            for (uint32_t j = 0; j < s.latent; ++j) eps[j] = so_normal(&er);
+            vl += so_elbo(&s, &me, &md, pe, pd, X + (size_t)val[k] * P, Cn + (size_t)val[k] * C, eps, NULL, NULL);
+        }
+        if (epochs) {
+            epochs[e].train_loss = train_loss;
+            epochs[e].validation_loss = n_val ? vl / (double)n_val : train_loss;
+        }
+    }
+    if (params_out)
+        for (size_t k = 0; k < ne + nd; ++k) params_out[k] = (double)(float)pe[k]; /* pe, pd contiguous */
+done:
+    free(order);
+    free(X);
+    free(buf);
+    return rc;
+}

@@ -82,6 +82,11 @@ typedef struct {
 int so_generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi, int phi_kind,
                         double phi_a, double phi_b, uint64_t seed, uint64_t first_index, so_sample* out);
 
+/* CVAE training (train_model, cvae.cpp:234-347); params_out = f32-quantised encoder then decoder. */
+int so_train_model(int kind, const so_sample* samples, uint64_t n, const sst_train_config* cfg,
+                   sst_epoch_stats* epochs, double* params_out);
+uint64_t so_dataset_fingerprint(const so_sample* s, uint64_t n, uint64_t seed);
+
 const char* so_last_error(void);
 
 #ifdef __cplusplus

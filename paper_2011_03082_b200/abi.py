@@ -97,6 +97,29 @@ class DatasetStats(C.Structure):
                 ("device_ms", D)]
 
 
+class TrainConfig(C.Structure):
+    """TrainConfig (cvae.hpp:101-114); defaults are the reference's."""
+    _fields_ = [("lr", D), ("batch_size", U32), ("epochs", U32), ("weight_decay", D), ("seed", U64),
+                ("validation_fraction", D), ("depth", C.c_int32), ("width", C.c_int32),
+                ("latent", C.c_int32)]
+
+    def __init__(self, **kw):
+        super().__init__(lr=1e-3, batch_size=512, epochs=100, weight_decay=1e-4, seed=1,
+                         validation_fraction=0.05, depth=-1, width=-1, latent=-1)
+        for k, v in kw.items():
+            setattr(self, k, v)
+
+
+class EpochStats(C.Structure):
+    _fields_ = [("train_loss", D), ("validation_loss", D)]
+
+
+class TrainStats(C.Structure):
+    _fields_ = [("steps", U64), ("rejected_batches", U64), ("sample_passes", U64),
+                ("encoder_params", U32), ("decoder_params", U32), ("dataset_fingerprint", U64),
+                ("device_ms", D)]
+
+
 # TrainingSample (dataset.hpp:17-27) as a numpy record, 52 bytes.
 try:
     import numpy as _np
@@ -114,6 +137,7 @@ EXPORTED = [
     "sst_gpu_upload_models", "sst_gpu_load_models_dir", "sst_rng_init",
     "sst_gpu_sphere_step_batch", "sst_gpu_upload_scene", "sst_gpu_scene_info", "sst_gpu_get_sdf", "sst_gpu_render",
     "sst_gpu_trace_paths", "sst_gpu_read_stats", "sst_gpu_generate_dataset",
+    "sst_train_config_default", "sst_gpu_train_model", "sst_gpu_train_models",
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
     "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm", "sst_dataset_save",
@@ -159,6 +183,10 @@ def _declare(L):
     L.sst_gpu_read_stats.argtypes = [P, C.POINTER(PathStats)]
     L.sst_gpu_generate_dataset.argtypes = [P, U64, D, D, D, D, I, D, D, U64, U64, P, I,
                                            C.POINTER(DatasetStats)]
+    L.sst_train_config_default.argtypes = [P]
+    L.sst_train_config_default.restype = None
+    L.sst_gpu_train_model.argtypes = [P, I, P, U64, I, U64, P, P, C.c_char_p, I, P, I, P]
+    L.sst_gpu_train_models.argtypes = [P, P, U64, I, U64, P, P, C.c_char_p, I, I, P]
     L.sst_dataset_save.argtypes = [C.c_char_p, U64, C.c_float, C.c_float, C.c_float, C.c_float, U32,
                                    C.c_float, C.c_float, U64, P]
     L.sst_gpu_trace_paths.argtypes = [P, I, I, U64, U64, P, P, P, P, P, C.POINTER(PathStats)]

@@ -260,6 +260,51 @@ class Renderer:
                                                      _p(out), abi.SST_PTR_HOST, C.byref(stats)))
         return out, stats
 
+    def train_model(self, kind, samples, dataset_seed=7, path=None, include_encoder=True, install=False,
+                    **config):
+        """train_model(kind, dataset, TrainConfig) (cvae.cpp:234-347) on the GPU.
+
+        `samples`: abi.SAMPLE_DTYPE records (host numpy) or a CUDA tensor / device pointer
+        holding them (pass `n=` in that case via a (ptr, n) tuple). `config` fields are
+        the TrainConfig ones (lr, batch_size, epochs, weight_decay, seed,
+        validation_fraction, depth, width, latent). Returns (params, epochs, stats):
+        the f32-quantised encoder+decoder parameters (flatten_parameters order), an
+        [epochs, 2] array of (train_loss, validation_loss), and abi.TrainStats.
+        """
+        cfg = abi.TrainConfig(**config)
+        if isinstance(samples, tuple):
+            ptr, n = samples
+            src, kind_ptr = C.c_void_p(int(ptr)), abi.SST_PTR_DEVICE
+        else:
+            samples = np.ascontiguousarray(samples, dtype=abi.SAMPLE_DTYPE)
+            n = len(samples)
+            src, kind_ptr = _p(samples), abi.SST_PTR_HOST
+        ep = np.zeros((cfg.epochs, 2))
+        params = np.zeros(1 << 16)
+        stats = abi.TrainStats()
+        abi.check(abi.lib().sst_gpu_train_model(self.h, int(kind), src, n, kind_ptr, dataset_seed, C.byref(cfg),
+                                                _p(ep), path.encode() if path else None, int(include_encoder),
+                                                _p(params), int(install), C.byref(stats)))
+        return params[:stats.encoder_params + stats.decoder_params].copy(), ep, stats
+
+    def train_models(self, samples, dataset_seed=7, out_dir=None, include_encoder=True, install=False, **config):
+        """The three decoders trained concurrently (sst_gpu_train_models). Returns
+        (epochs [3, E, 2], [abi.TrainStats] * 3)."""
+        cfg = abi.TrainConfig(**config)
+        if isinstance(samples, tuple):
+            ptr, n = samples
+            src, kind_ptr = C.c_void_p(int(ptr)), abi.SST_PTR_DEVICE
+        else:
+            samples = np.ascontiguousarray(samples, dtype=abi.SAMPLE_DTYPE)
+            n = len(samples)
+            src, kind_ptr = _p(samples), abi.SST_PTR_HOST
+        ep = np.zeros((3, cfg.epochs, 2))
+        stats = (abi.TrainStats * 3)()
+        abi.check(abi.lib().sst_gpu_train_models(self.h, src, n, kind_ptr, dataset_seed, C.byref(cfg), _p(ep),
+                                                 out_dir.encode() if out_dir else None, int(include_encoder),
+                                                 int(install), stats))
+        return ep, list(stats)
+
     def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None):
         pixel = np.ascontiguousarray(pixel, dtype=np.uint32)
         sample = np.ascontiguousarray(sample, dtype=np.uint32)

@@ -6,6 +6,7 @@
 // fails with SST_E_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <chrono>
@@ -15,6 +16,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -22,6 +24,7 @@
 #include "../../include/sst_host.h"
 #include "host.h"
 #include "launch.h"
+#include "train.h"
 #include "rng.cuh"
 #include "types.cuh"
 
@@ -83,6 +86,14 @@ struct DevBuf {
     }
 };
 
+// Function-local device buffer: released on every exit path (including CK throws).
+struct ScopedBuf : DevBuf {
+    ScopedBuf() = default;
+    ScopedBuf(const ScopedBuf&) = delete;
+    ScopedBuf& operator=(const ScopedBuf&) = delete;
+    ~ScopedBuf() { release(); }
+};
+
 struct ObjectHost {
     double sdf_origin[3];
     double sdf_voxel;
@@ -105,6 +116,8 @@ struct sst_gpu_ctx {
     uint64_t serial = 0;
 
     bool models = false;
+    HostModel host_models[3];
+    bool have_model[3] = {false, false, false};  // decoders staged for install (train_model)
     std::vector<double> weights;
     double norms[6] = {};
     uint64_t model_gen = 0;
@@ -186,6 +199,10 @@ void set_models(sst_gpu_ctx* ctx, const HostModel (&m)[3]) {
     std::vector<double> w;
     double norms[6];
     pack_models(m, w, norms);
+    for (int k = 0; k < 3; ++k) {
+        ctx->host_models[k] = m[k];
+        ctx->have_model[k] = true;
+    }
     ctx->weights = std::move(w);
     std::memcpy(ctx->norms, norms, sizeof norms);
     ctx->models = true;
@@ -253,7 +270,7 @@ void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, 
         for (int c = 0; c < 3; ++c)
             for (int k = 0; k < 3; ++k) tv[9ull * t + 3 * c + k] = od.positions[3ull * od.triangles[3 * t + c] + k];
     const size_t nvox = static_cast<size_t>(a.dims[0]) * a.dims[1] * a.dims[2];
-    DevBuf dtv, dval;
+    ScopedBuf dtv, dval;
     dtv.reserve(tv.size() * sizeof(double));
     dval.reserve(nvox * sizeof(float));
     CK(cudaMemcpyAsync(dtv.p, tv.data(), tv.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -288,7 +305,7 @@ void build_skip_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh)
         for (int c = 0; c < 3; ++c)
             for (int k = 0; k < 3; ++k) tv[9ull * t + 3 * c + k] = od.positions[3ull * od.triangles[3 * t + c] + k];
     const size_t nvox = static_cast<size_t>(a.dims[0]) * a.dims[1] * a.dims[2];
-    DevBuf dtv, dval;
+    ScopedBuf dtv, dval;
     dtv.reserve(tv.size() * sizeof(double));
     dval.reserve(nvox);
     CK(cudaMemcpyAsync(dtv.p, tv.data(), tv.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -422,7 +439,7 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
             for (int a = 0; a < 3; ++a) q[6 + 3 * c + a] = dir[c][a];
     }
     const uint32_t ncell = 6u * res * res;
-    DevBuf dcaps, dcounts;
+    ScopedBuf dcaps, dcounts;
     dcaps.reserve(caps.size() * sizeof(double));
     dcounts.reserve(ncell * sizeof(uint32_t));
     CK(cudaMemcpyAsync(dcaps.p, caps.data(), caps.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -1109,7 +1126,7 @@ int sst_gpu_generate_dataset(sst_gpu_ctx* ctx, uint64_t n, double s_lo, double s
         ensure_pipeline(ctx);
         join_slots(ctx);
         const uint64_t chunk = ptr_kind == SST_PTR_DEVICE ? n : std::min<uint64_t>(n, 1ull << 24);
-        DevBuf dout, dmisc;
+        ScopedBuf dout, dmisc;
         if (ptr_kind == SST_PTR_HOST) dout.reserve(chunk * sizeof(TrainingSampleDev));
         dmisc.reserve(8 + 8 + 4 * 8);
         unsigned long long* work = dmisc.as<unsigned long long>();
@@ -1317,3 +1334,462 @@ int sst_image_save_pfm(const char* path, uint32_t w, uint32_t h, const float* rg
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ CVAE training (§8f #3)
+void sst_train_config_default(sst_train_config* c) {
+    if (!c) return;
+    *c = sst_train_config{};
+    c->lr = 1e-3;
+    c->batch_size = 512;
+    c->epochs = 100;
+    c->weight_decay = 1e-4;
+    c->seed = 1;
+    c->validation_fraction = 0.05;
+    c->depth = c->width = c->latent = -1;
+}
+
+namespace {
+
+const char* kind_name(int kind) {  // model_kind_name (cvae.cpp:35-42)
+    static const char* names[3] = {"lengthgen", "pathgen", "eventgen"};
+    return names[kind];
+}
+
+// Fisher-Yates with RandomStream draws, exactly as train_model (cvae.cpp:261-266, 284-286).
+void shuffle_in_place(std::vector<uint32_t>& v, HostStream& rng) {
+    for (size_t i = v.size(); i > 1; --i) std::swap(v[i - 1], v[static_cast<size_t>(rng.uniform() * i)]);
+}
+
+// Trace / planar-buffer layout and the phase-2 ownership plan for one spec (train.h).
+void plan_training(TrainArgs& a, const CvaeSpecH& s, uint32_t batch, int cluster) {
+    const MlpShape sh[2] = {encoder_shape(s), decoder_shape(s)};
+    a.p_in = static_cast<int>(s.p_in);
+    a.p_out = static_cast<int>(s.p_out);
+    a.latent = static_cast<int>(s.latent);
+    int off = 0, poff = 0;
+    size_t goff = 0;
+    for (int m = 0; m < 2; ++m) {
+        TrainNetK& N = a.net[m];
+        N.n_layers = static_cast<int>(sh[m].in.size());
+        for (int l = 0; l < N.n_layers; ++l) {
+            N.in[l] = static_cast<int>(sh[m].in[l]);
+            N.out[l] = static_cast<int>(sh[m].out[l]);
+            N.woff[l] = poff;
+            poff += N.in[l] * N.out[l] + N.out[l];
+            N.xo[l] = off;
+            off += N.in[l];
+            N.po[l] = off;
+            off += N.out[l];
+            N.dlo[l] = off;
+            off += N.out[l];
+            // planar regions start 16-byte aligned (TMA bulk copies, train.cu)
+            N.gx[l] = goff;
+            goff += (static_cast<size_t>(batch) * N.in[l] + 1) & ~size_t(1);
+            N.gd[l] = goff;
+            goff += (static_cast<size_t>(batch) * N.out[l] + 1) & ~size_t(1);
+        }
+    }
+    a.din_o = off;
+    off += a.net[1].in[0];
+    a.eps_o = off;
+    off += a.latent;
+    a.term_o = off;  // per-component KL / log-likelihood terms
+    off += a.latent + a.p_out;
+    a.loss_o = off;
+    off += 1;
+    a.ts = off | 1;  // odd row stride: conflict-free 64-bit smem accesses across samples
+    a.gloss = goff;
+    a.n_params = poff;
+    a.n_params_pad = (poff + 1) & ~1;
+    // shared memory: parameters + max(chunk trace rows, phase-2 staging) + chunk ids
+    const size_t budget = 200 * 1024;
+    const size_t fixed = static_cast<size_t>(a.n_params_pad) * 8;
+    const uint32_t S = (batch + cluster - 1) / cluster;
+    int max_row = 0;
+    for (int m = 0; m < 2; ++m)
+        for (int l = 0; l < a.net[m].n_layers; ++l) max_row = std::max(max_row, a.net[m].in[l] + a.net[m].out[l] + 1);
+    const size_t avail = (budget - fixed) / 8 - 64;  // doubles, minus the ids slack
+    a.chunk = static_cast<int>(std::min<size_t>(std::min<size_t>(S, 64), avail / a.ts));
+    if (a.chunk < 1) throw InvalidArgument("GPU training: network too large for shared memory");
+    a.stage_cap = static_cast<int>(
+        std::min<size_t>(avail, static_cast<size_t>(std::min<uint32_t>(batch, 1024) + 2) * max_row + 6));
+    if (a.stage_cap < 2 * max_row + 6) throw InvalidArgument("GPU training: network too large for shared memory");
+    const size_t region = std::max<size_t>(static_cast<size_t>(a.chunk) * a.ts, a.stage_cap);
+    a.smem_bytes = fixed + region * 8 + static_cast<size_t>(a.chunk) * 4 + 16;
+    // phase-2 units: every layer gets >= 1 CTA; spare CTAs split the largest layers by rows.
+    struct Lay { int m, l, parts; double size; };
+    std::vector<Lay> lays;
+    for (int m = 0; m < 2; ++m)
+        for (int l = 0; l < a.net[m].n_layers; ++l) {
+            const int need = (a.net[m].out[l] * (a.net[m].in[l] + 1) + kTrainThreads * kTrainMaxQ - 1) /
+                             (kTrainThreads * kTrainMaxQ);
+            lays.push_back({m, l, need, static_cast<double>(a.net[m].out[l]) * (a.net[m].in[l] + 1)});
+        }
+    int used = 0;
+    for (auto& L : lays) used += L.parts;
+    if (used > cluster) throw InvalidArgument("GPU training: too many layers for one cluster (depth too large)");
+    while (used < cluster) {
+        Lay* best = nullptr;
+        for (auto& L : lays)
+            if (L.parts < a.net[L.m].out[L.l] && (!best || L.size / L.parts > best->size / best->parts)) best = &L;
+        if (!best) break;
+        ++best->parts;
+        ++used;
+    }
+    a.n_units = 0;
+    for (auto& L : lays) {
+        const int out = a.net[L.m].out[L.l];
+        for (int p = 0; p < L.parts; ++p) {
+            a.unit_model[a.n_units] = L.m;
+            a.unit_layer[a.n_units] = L.l;
+            a.unit_r0[a.n_units] = out * p / L.parts;
+            a.unit_r1[a.n_units] = out * (p + 1) / L.parts;
+            ++a.n_units;
+        }
+    }
+}
+
+}  // namespace
+
+namespace {
+
+// One model being trained (one kind, one cluster, one stream).
+struct KindRun {
+    int kind = 0;
+    CvaeSpecH spec;
+    std::vector<double> enc, dec, params;
+    TrainArgs a{};
+    int cluster = 16;
+    cudaStream_t st = nullptr;
+    ScopedBuf dx, dc, dpar, dm, dv, dt, dbc, dtrace, dbl, dvl;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, done[2] = {nullptr, nullptr};
+    std::vector<double> bl, vl;
+    unsigned long long t_final = 0;
+    ~KindRun() {
+        for (cudaEvent_t e : {ev0, ev1, done[0], done[1]})
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+void validate_train_config(const sst_train_config* cfg) {  // TrainConfig::validate (cvae.cpp:214-222)
+    if (!cfg) throw InvalidArgument("null TrainConfig");
+    if (!(cfg->lr > 0.0)) throw InvalidArgument("TrainConfig: lr must be > 0");
+    if (cfg->batch_size == 0) throw InvalidArgument("TrainConfig: batch_size must be > 0");
+    if (cfg->epochs == 0) throw InvalidArgument("TrainConfig: epochs must be > 0");
+    if (!(cfg->weight_decay >= 0.0)) throw InvalidArgument("TrainConfig: negative weight decay");
+    if (!(cfg->validation_fraction >= 0.0 && cfg->validation_fraction < 1.0))
+        throw InvalidArgument("TrainConfig: validation fraction out of range");
+}
+
+CvaeSpecH train_spec(int kind, const sst_train_config* cfg) {
+    CvaeSpecH spec = production_spec(kind);
+    if (cfg->depth > 0) spec.depth = static_cast<uint32_t>(cfg->depth);
+    if (cfg->width > 0) spec.width = static_cast<uint32_t>(cfg->width);
+    if (cfg->latent > 0) spec.latent = static_cast<uint32_t>(cfg->latent);
+    validate_spec(spec);
+    if (spec.depth + 1 > static_cast<uint32_t>(kTrainMaxLayers) || spec.width > static_cast<uint32_t>(kTrainMaxWidth) ||
+        spec.latent > static_cast<uint32_t>(kTrainMaxLatent))
+        throw InvalidArgument("GPU training supports depth <= 4, width <= 32, latent <= 16");
+    return spec;
+}
+
+// train_model (cvae.cpp:234-347) for nk kinds over the same dataset and config. The
+// validation split and the per-epoch shuffles depend only on (seed, epoch), so all
+// kinds share them; each kind trains on its own stream and cluster, concurrently.
+void train_impl(sst_gpu_ctx* ctx, const int* kinds, int nk, const sst_training_sample* samples, uint64_t n,
+                int ptr_kind, uint64_t dataset_seed, const sst_train_config* cfg, sst_epoch_stats* const* epochs_out,
+                const char* const* ssnn_paths, int include_encoder, double* const* params_out, int install,
+                sst_train_stats* const* stats_out) {
+    validate_train_config(cfg);
+    if (n == 0 || !samples) throw InvalidArgument("train_model: empty dataset");
+    if (ptr_kind != SST_PTR_HOST && ptr_kind != SST_PTR_DEVICE) throw InvalidArgument("bad ptr_kind");
+    if (n > 0xFFFFFFFFull) throw InvalidArgument("train_model: more than 2^32 samples");
+    std::vector<std::unique_ptr<KindRun>> runs;
+    for (int k = 0; k < nk; ++k) {
+        if (kinds[k] < 0 || kinds[k] > 2) throw InvalidArgument("unknown model kind");
+        auto r = std::make_unique<KindRun>();
+        r->kind = kinds[k];
+        r->spec = train_spec(r->kind, cfg);
+        make_cvae_params(r->kind, r->spec, cfg->seed, r->enc, r->dec);
+        runs.push_back(std::move(r));
+    }
+    // seed-fixed validation split (cvae.cpp:259-270)
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    {
+        HostStream split(cfg->seed, 0x05 /* kTrainSplit */);
+        shuffle_in_place(order, split);
+    }
+    const auto n_val = static_cast<size_t>(cfg->validation_fraction * static_cast<double>(n));
+    std::vector<uint32_t> val_idx(order.begin(), order.begin() + n_val);
+    std::vector<uint32_t> train_idx(order.begin() + n_val, order.end());
+    if (train_idx.empty()) throw InvalidArgument("train_model: no training samples left");
+    const uint32_t B = cfg->batch_size;
+    const uint32_t n_train = static_cast<uint32_t>(train_idx.size());
+    const uint32_t nb = (n_train + B - 1) / B;
+    const uint32_t E = cfg->epochs;
+    const double beta1 = 0.9, beta2 = 0.999, adam_eps = 1e-8;  // AdamWConfig (mlp.hpp:95-101)
+    // AdamW bias corrections 1 - beta^t (adamw_step, mlp.cpp:217-218) with the host's pow
+    const uint64_t t_max = static_cast<uint64_t>(E) * nb;
+    std::vector<double> bc(2 * (t_max + 1));
+    for (uint64_t t = 0; t <= t_max; ++t) {
+        bc[2 * t] = 1.0 - std::pow(beta1, static_cast<double>(t));
+        bc[2 * t + 1] = 1.0 - std::pow(beta2, static_cast<double>(t));
+    }
+
+    ensure_pipeline(ctx);
+    join_slots(ctx);
+    cudaStream_t main = ctx->stream;
+    ScopedBuf dsamp, dval, dord[2];
+    const void* sp = samples;
+    if (ptr_kind == SST_PTR_HOST) {
+        dsamp.reserve(n * sizeof(TrainingSampleDev));
+        CK(cudaMemcpyAsync(dsamp.p, samples, n * sizeof(TrainingSampleDev), cudaMemcpyHostToDevice, main));
+        sp = dsamp.p;
+    }
+    dval.reserve(std::max<size_t>(n_val, 1) * 4);
+    if (n_val) CK(cudaMemcpyAsync(dval.p, val_idx.data(), n_val * 4, cudaMemcpyHostToDevice, main));
+    for (auto& o : dord) o.reserve(static_cast<size_t>(n_train) * 4);
+    cudaEvent_t ev_ready = nullptr, ev_order[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+    uint32_t* pin[2] = {nullptr, nullptr};
+    struct Cleanup {
+        cudaEvent_t* evs[3];
+        uint32_t** pin;
+        ~Cleanup() {
+            for (int i = 0; i < 2; ++i) {
+                if (evs[2][i]) cudaEventSynchronize(evs[2][i]);
+                if (pin[i]) cudaFreeHost(pin[i]);
+            }
+            for (cudaEvent_t* e : {evs[0], evs[1], evs[1] + 1, evs[2], evs[2] + 1})
+                if (*e) cudaEventDestroy(*e);
+        }
+    } cleanup{{&ev_ready, ev_order, copied}, pin};
+    CK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&ev_order[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&pin[i]), static_cast<size_t>(n_train) * 4, cudaHostAllocDefault));
+    }
+    CK(cudaEventRecord(ev_ready, main));
+
+    for (int k = 0; k < nk; ++k) {
+        KindRun& r = *runs[k];
+        r.st = k == 0 ? main : ctx->slots[k - 1].s;
+        CK(cudaEventCreate(&r.ev0));
+        CK(cudaEventCreate(&r.ev1));
+        for (auto& d : r.done) CK(cudaEventCreateWithFlags(&d, cudaEventDisableTiming));
+        plan_training(r.a, r.spec, B, 16);
+        r.cluster = train_cluster_size(r.a.smem_bytes);
+        if (r.cluster == 0) throw CudaFailure("GPU training: no thread-block cluster fits this device");
+        if (r.cluster != 16) plan_training(r.a, r.spec, B, r.cluster);
+        CK(cudaStreamWaitEvent(r.st, ev_ready, 0));
+        r.dx.reserve(n * r.spec.p_out * sizeof(double));
+        r.dc.reserve(n * r.spec.p_in * sizeof(double));
+        TrainPrepArgs pa{};
+        pa.samples = sp;
+        pa.n = n;
+        pa.kind = r.kind;
+        pa.log1p_sigma_ref = std::log1p(200.0);  // NormConstants defaults (cvae.hpp:43-46)
+        pa.log_n_ref = std::log(1e4);
+        pa.x = r.dx.as<double>();
+        pa.cnd = r.dc.as<double>();
+        CK(launch_train_prep(pa, r.st));
+        r.params = r.enc;
+        r.params.insert(r.params.end(), r.dec.begin(), r.dec.end());
+        const size_t np = r.params.size();
+        r.dpar.reserve(np * 8);
+        r.dm.reserve(np * 8);
+        r.dv.reserve(np * 8);
+        r.dt.reserve(8);
+        CK(cudaMemcpyAsync(r.dpar.p, r.params.data(), np * 8, cudaMemcpyHostToDevice, r.st));
+        CK(cudaMemsetAsync(r.dm.p, 0, np * 8, r.st));
+        CK(cudaMemsetAsync(r.dv.p, 0, np * 8, r.st));
+        CK(cudaMemsetAsync(r.dt.p, 0, 8, r.st));
+        r.dbc.reserve(bc.size() * 8);
+        CK(cudaMemcpyAsync(r.dbc.p, bc.data(), bc.size() * 8, cudaMemcpyHostToDevice, r.st));
+        r.dtrace.reserve((r.a.gloss + B + 16) * 8);  // + slack: bulk copies round up to 16 bytes
+        r.dbl.reserve(static_cast<size_t>(E) * nb * 8);
+        r.dvl.reserve(std::max<size_t>(static_cast<size_t>(E) * n_val, 1) * 8);
+        TrainArgs& a = r.a;
+        a.x = r.dx.as<double>();
+        a.cnd = r.dc.as<double>();
+        a.batch = B;
+        a.n_batches = nb;
+        a.seed = cfg->seed;
+        a.params = r.dpar.as<double>();
+        a.adam_m = r.dm.as<double>();
+        a.adam_v = r.dv.as<double>();
+        a.t_io = r.dt.as<unsigned long long>();
+        a.bc = r.dbc.as<double>();
+        a.lr = cfg->lr;
+        a.wd = cfg->weight_decay;
+        a.beta1 = beta1;
+        a.beta2 = beta2;
+        a.eps = adam_eps;
+        a.gtrace = r.dtrace.as<double>();
+        CK(cudaEventRecord(r.ev0, r.st));
+    }
+
+    // Epoch loop: the host shuffles epoch e+1 while the device trains epoch e; the
+    // order buffers alternate so a copy never overwrites an order still being read.
+    for (uint32_t e = 0; e < E; ++e) {
+        const int slot = static_cast<int>(e & 1);
+        HostStream sh(cfg->seed, 0x03 /* kTrainShuffle */, e);
+        shuffle_in_place(train_idx, sh);
+        CK(cudaEventSynchronize(copied[slot]));
+        std::memcpy(pin[slot], train_idx.data(), static_cast<size_t>(n_train) * 4);
+        if (e >= 2)
+            for (auto& rp : runs) CK(cudaStreamWaitEvent(main, rp->done[slot], 0));
+        CK(cudaMemcpyAsync(dord[slot].p, pin[slot], static_cast<size_t>(n_train) * 4, cudaMemcpyHostToDevice, main));
+        CK(cudaEventRecord(copied[slot], main));
+        CK(cudaEventRecord(ev_order[slot], main));
+        for (auto& rp : runs) {
+            KindRun& r = *rp;
+            if (r.st != main) CK(cudaStreamWaitEvent(r.st, ev_order[slot], 0));
+            TrainArgs ta = r.a;
+            ta.order = dord[slot].as<uint32_t>();
+            ta.n_order = n_train;
+            ta.epoch = e;
+            ta.batch_loss = r.dbl.as<double>() + static_cast<size_t>(e) * nb;
+            CK(launch_train_epoch(ta, r.cluster, r.st));
+            if (n_val) {
+                TrainArgs va = r.a;
+                va.order = dval.as<uint32_t>();
+                va.n_order = static_cast<uint32_t>(n_val);
+                va.epoch = e;
+                va.batch_loss = r.dvl.as<double>() + static_cast<size_t>(e) * n_val;
+                CK(launch_train_eval(va, r.st));
+            }
+            CK(cudaEventRecord(r.done[slot], r.st));
+        }
+    }
+    for (auto& rp : runs) {
+        KindRun& r = *rp;
+        CK(cudaEventRecord(r.ev1, r.st));
+        r.bl.resize(static_cast<size_t>(E) * nb);
+        r.vl.resize(static_cast<size_t>(E) * n_val);
+        CK(cudaMemcpyAsync(r.bl.data(), r.dbl.p, r.bl.size() * 8, cudaMemcpyDeviceToHost, r.st));
+        if (n_val) CK(cudaMemcpyAsync(r.vl.data(), r.dvl.p, r.vl.size() * 8, cudaMemcpyDeviceToHost, r.st));
+        CK(cudaMemcpyAsync(r.params.data(), r.dpar.p, r.params.size() * 8, cudaMemcpyDeviceToHost, r.st));
+        CK(cudaMemcpyAsync(&r.t_final, r.dt.p, 8, cudaMemcpyDeviceToHost, r.st));
+    }
+    for (auto& rp : runs) CK(cudaStreamSynchronize(rp->st));
+
+    uint64_t fp = 0;
+    bool have_fp = false;
+    for (int k = 0; k < nk; ++k) {
+        KindRun& r = *runs[k];
+        // EpochStats (cvae.cpp:300-345): finite batches only; validation in val_idx order.
+        uint64_t rejected = 0;
+        for (uint32_t e = 0; e < E; ++e) {
+            double epoch_loss = 0.0;
+            size_t epoch_samples = 0, finite = 0;
+            for (uint32_t b = 0; b < nb; ++b) {
+                const double x = r.bl[static_cast<size_t>(e) * nb + b];
+                if (!std::isfinite(x)) {
+                    ++rejected;
+                    continue;
+                }
+                ++finite;
+                epoch_loss += x;
+                epoch_samples += std::min<size_t>(B, n_train - static_cast<size_t>(b) * B);
+            }
+            if (finite == 0)
+                throw RuntimeError(std::string("train_model(") + kind_name(r.kind) +
+                                   "): diverged, every batch non-finite in epoch " + std::to_string(e));
+            if (epochs_out && epochs_out[k]) {
+                sst_epoch_stats& es = epochs_out[k][e];
+                es.train_loss = epoch_loss / static_cast<double>(std::max<size_t>(1, epoch_samples));
+                double v = 0.0;
+                for (size_t i = 0; i < n_val; ++i) v += r.vl[static_cast<size_t>(e) * n_val + i];
+                es.validation_loss = n_val ? v / static_cast<double>(n_val) : es.train_loss;
+            }
+        }
+        for (double& v : r.params) v = static_cast<double>(static_cast<float>(v));  // quantize_f32
+        if (params_out && params_out[k]) std::memcpy(params_out[k], r.params.data(), r.params.size() * 8);
+        r.enc.assign(r.params.begin(), r.params.begin() + r.enc.size());
+        r.dec.assign(r.params.begin() + r.enc.size(), r.params.end());
+        const bool want_fp = (ssnn_paths && ssnn_paths[k]) || (stats_out && stats_out[k]);
+        if (want_fp && !have_fp) {  // Dataset::fingerprint (dataset.cpp:32-38): version, count, seed, records
+            std::vector<uint8_t> host_copy;
+            const uint8_t* bytes = reinterpret_cast<const uint8_t*>(samples);
+            if (ptr_kind == SST_PTR_DEVICE) {
+                host_copy.resize(n * sizeof(TrainingSampleDev));
+                CK(cudaMemcpy(host_copy.data(), samples, host_copy.size(), cudaMemcpyDeviceToHost));
+                bytes = host_copy.data();
+            }
+            const uint32_t version = 1;
+            const uint64_t count = n;
+            fp = fnv(&version, sizeof version);
+            fp = fnv(&count, sizeof count, fp);
+            fp = fnv(&dataset_seed, sizeof dataset_seed, fp);
+            fp = fnv(bytes, n * sizeof(TrainingSampleDev), fp);
+            have_fp = true;
+        }
+        if (ssnn_paths && ssnn_paths[k])
+            save_ssnn(ssnn_paths[k], r.kind, r.spec, 200.0, 1e4, fp, r.dec, include_encoder ? &r.enc : nullptr);
+        if (stats_out && stats_out[k]) {
+            sst_train_stats& st = *stats_out[k];
+            float ms = 0.0f;
+            CK(cudaEventElapsedTime(&ms, r.ev0, r.ev1));
+            st.steps = r.t_final;
+            st.rejected_batches = rejected;
+            st.sample_passes = static_cast<uint64_t>(E) * n_train;
+            st.encoder_params = static_cast<uint32_t>(r.enc.size());
+            st.decoder_params = static_cast<uint32_t>(r.dec.size());
+            st.dataset_fingerprint = fp;
+            st.device_ms = ms;
+        }
+    }
+    if (install) {
+        for (auto& rp : runs) {
+            ctx->host_models[rp->kind] = model_from_params(rp->kind, rp->spec, 200.0, 1e4, rp->dec);
+            ctx->have_model[rp->kind] = true;
+        }
+        if (ctx->have_model[0] && ctx->have_model[1] && ctx->have_model[2]) {
+            HostModel m[3] = {ctx->host_models[0], ctx->host_models[1], ctx->host_models[2]};
+            set_models(ctx, m);
+            ensure_constants(ctx);
+        }
+    }
+}
+
+}  // namespace
+
+int sst_gpu_train_model(sst_gpu_ctx* ctx, int kind, const sst_training_sample* samples, uint64_t n, int ptr_kind,
+                        uint64_t dataset_seed, const sst_train_config* cfg, sst_epoch_stats* epochs_out,
+                        const char* ssnn_path, int include_encoder, double* params_out, int install,
+                        sst_train_stats* stats) {
+    return guarded([&] {
+        require_device(ctx);
+        sst_epoch_stats* eo[1] = {epochs_out};
+        const char* paths[1] = {ssnn_path};
+        double* po[1] = {params_out};
+        sst_train_stats* so[1] = {stats};
+        train_impl(ctx, &kind, 1, samples, n, ptr_kind, dataset_seed, cfg, eo, paths, include_encoder, po, install, so);
+    });
+}
+
+int sst_gpu_train_models(sst_gpu_ctx* ctx, const sst_training_sample* samples, uint64_t n, int ptr_kind,
+                         uint64_t dataset_seed, const sst_train_config* cfg, sst_epoch_stats* epochs_out,
+                         const char* out_dir, int include_encoder, int install, sst_train_stats* stats) {
+    return guarded([&] {
+        require_device(ctx);
+        const int kinds[3] = {0, 1, 2};
+        const uint32_t E = cfg ? cfg->epochs : 0;
+        sst_epoch_stats* eo[3] = {nullptr, nullptr, nullptr};
+        sst_train_stats* so[3] = {nullptr, nullptr, nullptr};
+        std::string names[3];
+        const char* paths[3] = {nullptr, nullptr, nullptr};
+        for (int k = 0; k < 3; ++k) {
+            if (epochs_out) eo[k] = epochs_out + static_cast<size_t>(k) * E;
+            if (stats) so[k] = stats + k;
+            if (out_dir) {
+                names[k] = std::string(out_dir) + "/" + kind_name(k) + ".ssnn";
+                paths[k] = names[k].c_str();
+            }
+        }
+        train_impl(ctx, kinds, 3, samples, n, ptr_kind, dataset_seed, cfg, eo, paths, include_encoder, nullptr,
+                   install, so);
+    });
+}

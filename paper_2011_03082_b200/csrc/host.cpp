@@ -12,6 +12,7 @@
 #include <sstream>
 #include <unordered_map>
 
+#include "rng.cuh"
 #include "types.cuh"
 
 namespace sstg {
@@ -502,6 +503,147 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
     out.tris_f32 = bytes(tf);
     out.tris_f64 = bytes(td);
     return out;
+}
+
+// ------------------------------------------------------------------ training (host side)
+HostStream::HostStream(uint64_t seed, uint64_t s1, uint64_t s2, uint64_t s3) : s(rng_key(seed, s1, s2, s3)) {}
+
+uint64_t HostStream::next_u64() {
+    s += kGolden;
+    return mix64(s);
+}
+
+CvaeSpecH production_spec(int kind) {
+    CvaeSpecH s;
+    switch (kind) {
+        case 0: s = {2, 1, 2, 8, 2}; break;
+        case 1: s = {3, 3, 2, 16, 5}; break;
+        case 2: s = {7, 6, 2, 16, 5}; break;
+        default: throw InvalidArgument("unknown model kind");
+    }
+    return s;
+}
+
+void validate_spec(const CvaeSpecH& s) {
+    if (s.p_in == 0 || s.p_out == 0 || s.width == 0 || s.latent == 0)
+        throw InvalidArgument("CvaeSpec: zero dimension");
+    if ((s.p_in + s.latent) % 4 != 0)
+        throw InvalidArgument("CvaeSpec: p_in + latent must be a multiple of four");
+}
+
+size_t MlpShape::params() const {
+    size_t n = 0;
+    for (size_t i = 0; i < in.size(); ++i) n += static_cast<size_t>(in[i]) * out[i] + out[i];
+    return n;
+}
+
+static MlpShape mlp_shape(uint32_t input, uint32_t output, uint32_t depth, uint32_t width) {
+    MlpShape m;
+    uint32_t in = input;
+    for (uint32_t d = 0; d <= depth; ++d) {
+        const uint32_t out = d == depth ? output : width;
+        m.in.push_back(in);
+        m.out.push_back(out);
+        in = out;
+    }
+    return m;
+}
+
+MlpShape encoder_shape(const CvaeSpecH& s) { return mlp_shape(s.p_out + s.p_in, 2 * s.latent, s.depth, s.width); }
+MlpShape decoder_shape(const CvaeSpecH& s) { return mlp_shape(s.latent + s.p_in, 2 * s.p_out, s.depth, s.width); }
+
+// make_mlp + make_gaussian_mlp (mlp.cpp:32-58), flattened (weights then bias per layer).
+static std::vector<double> gaussian_mlp(const MlpShape& m, uint32_t p_out, HostStream& rng) {
+    std::vector<double> flat;
+    flat.reserve(m.params());
+    for (size_t l = 0; l < m.in.size(); ++l) {
+        const double bound = std::sqrt(6.0 / (static_cast<double>(m.in[l]) + m.out[l]));
+        for (size_t i = 0; i < static_cast<size_t>(m.in[l]) * m.out[l]; ++i) flat.push_back(rng.uniform(-bound, bound));
+        const bool head = l + 1 == m.in.size();
+        for (uint32_t r = 0; r < m.out[l]; ++r) flat.push_back(head && r >= p_out ? -2.0 : 0.0);
+    }
+    for (double& v : flat) v = static_cast<double>(static_cast<float>(v));  // quantize_f32 (mlp.cpp:25-30)
+    return flat;
+}
+
+void make_cvae_params(int kind, const CvaeSpecH& s, uint64_t seed, std::vector<double>& enc, std::vector<double>& dec) {
+    validate_spec(s);
+    HostStream rng(seed, 0x02 /* kTrainInit */, static_cast<uint64_t>(kind));
+    enc = gaussian_mlp(encoder_shape(s), s.latent, rng);
+    dec = gaussian_mlp(decoder_shape(s), s.p_out, rng);
+}
+
+namespace {
+struct Writer {
+    std::ofstream out;
+    std::string path;
+    explicit Writer(const std::string& p) : out(p, std::ios::binary | std::ios::trunc), path(p) {
+        if (!out) throw RuntimeError("cannot open for writing: " + p);
+    }
+    template <class T>
+    void put(T v) {  // little-endian host (x86-64 / aarch64)
+        out.write(reinterpret_cast<const char*>(&v), sizeof v);
+    }
+};
+
+void write_mlp(Writer& w, const MlpShape& m, const std::vector<double>& flat) {
+    w.put<uint32_t>(static_cast<uint32_t>(m.in.size()));
+    size_t off = 0;
+    for (size_t l = 0; l < m.in.size(); ++l) {
+        w.put<uint32_t>(m.out[l]);
+        w.put<uint32_t>(m.in[l]);
+        const size_t n = static_cast<size_t>(m.in[l]) * m.out[l] + m.out[l];
+        for (size_t i = 0; i < n; ++i) w.put<float>(static_cast<float>(flat[off + i]));
+        off += n;
+    }
+}
+}  // namespace
+
+void save_ssnn(const std::string& path, int kind, const CvaeSpecH& s, double sigma_ref, double n_ref,
+               uint64_t fingerprint, const std::vector<double>& dec, const std::vector<double>* enc) {
+    Writer w(path);
+    w.out.write("SSNN", 4);
+    w.put<uint32_t>(1);
+    w.put<uint32_t>(static_cast<uint32_t>(kind));
+    w.put<uint32_t>(enc ? 1u : 0u);
+    w.put<uint32_t>(s.p_in);
+    w.put<uint32_t>(s.p_out);
+    w.put<uint32_t>(s.depth);
+    w.put<uint32_t>(s.width);
+    w.put<uint32_t>(s.latent);
+    w.put<double>(sigma_ref);
+    w.put<double>(n_ref);
+    w.put<uint64_t>(fingerprint);
+    write_mlp(w, decoder_shape(s), dec);
+    if (enc) write_mlp(w, encoder_shape(s), *enc);
+    w.out.close();
+    if (!w.out) throw RuntimeError("write failure on close");
+}
+
+HostModel model_from_params(int kind, const CvaeSpecH& s, double sigma_ref, double n_ref,
+                            const std::vector<double>& dec) {
+    HostModel m;
+    m.kind = static_cast<uint32_t>(kind);
+    m.p_in = s.p_in;
+    m.p_out = s.p_out;
+    m.depth = s.depth;
+    m.width = s.width;
+    m.latent = s.latent;
+    m.sigma_ref = sigma_ref;
+    m.n_ref = n_ref;
+    const MlpShape sh = decoder_shape(s);
+    size_t off = 0;
+    for (size_t l = 0; l < sh.in.size(); ++l) {
+        HostLayer hl;
+        hl.out_dim = sh.out[l];
+        hl.in_dim = sh.in[l];
+        const size_t nw = static_cast<size_t>(hl.out_dim) * hl.in_dim;
+        for (size_t i = 0; i < nw; ++i) hl.w.push_back(static_cast<float>(dec[off + i]));
+        for (size_t i = 0; i < hl.out_dim; ++i) hl.b.push_back(static_cast<float>(dec[off + nw + i]));
+        off += nw + hl.out_dim;
+        m.layers.push_back(std::move(hl));
+    }
+    return m;
 }
 
 }  // namespace sstg

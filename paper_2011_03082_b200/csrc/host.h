@@ -65,4 +65,42 @@ struct FlatBvh {
 FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tri_vertices,
                   const std::vector<uint32_t>& tri_obj);
 
+// ------------------------------------------------------------------ training (host side)
+// RandomStream (rng.hpp:15-50) on the host: the split / shuffle / init streams.
+struct HostStream {
+    uint64_t s;
+    HostStream(uint64_t seed, uint64_t s1 = 0, uint64_t s2 = 0, uint64_t s3 = 0);
+    uint64_t next_u64();
+    double uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + uniform() * (hi - lo); }
+};
+
+// CvaeSpec (cvae.hpp:28-38).
+struct CvaeSpecH {
+    uint32_t p_in = 0, p_out = 0, depth = 2, width = 8, latent = 2;
+};
+CvaeSpecH production_spec(int kind);  // CvaeSpec::production_default (cvae.cpp:51-57)
+void validate_spec(const CvaeSpecH& s);  // CvaeSpec::validate (cvae.cpp:60-65)
+
+// Layer shapes of the encoder / decoder MLPs of a spec (make_gaussian_mlp, mlp.cpp:52-58).
+struct MlpShape {
+    std::vector<uint32_t> in, out;
+    size_t params() const;
+};
+MlpShape encoder_shape(const CvaeSpecH& s);
+MlpShape decoder_shape(const CvaeSpecH& s);
+
+// make_cvae (cvae.cpp:79-91): Glorot-uniform weights from RandomStream(seed, kTrainInit,
+// kind), encoder then decoder, log-variance head biases -2, quantised to f32.
+void make_cvae_params(int kind, const CvaeSpecH& s, uint64_t seed, std::vector<double>& enc,
+                      std::vector<double>& dec);
+
+// save_model (cvae.cpp:349-377). enc may be null (no encoder section).
+void save_ssnn(const std::string& path, int kind, const CvaeSpecH& s, double sigma_ref, double n_ref,
+               uint64_t fingerprint, const std::vector<double>& dec, const std::vector<double>* enc);
+
+// HostModel (decoder half) from flattened decoder parameters.
+HostModel model_from_params(int kind, const CvaeSpecH& s, double sigma_ref, double n_ref,
+                            const std::vector<double>& dec);
+
 }  // namespace sstg
