@@ -337,6 +337,15 @@ def bench_ours(args, world, rank, local):
                                "events_per_s": dst.events / (dst.device_ms / 1e3),
                                "time_1e8_walks_s": 1e8 / (dst.walks / (dst.device_ms / 1e3)),
                                "sample": "2e6 walks, sigma_t U[0,200], g U[-1,1], phi 1-10^U[-5,-0.5]"}
+        # CVAE training (row f3): the desk-scale weights job, 3 kinds concurrently
+        r.train_models(out[:5000], dataset_seed=7, epochs=1)  # warm-up
+        t0 = time.perf_counter()
+        _, tst = r.train_models(out, dataset_seed=7, epochs=20, seed=1)
+        tw = time.perf_counter() - t0
+        extra["cvae_training"] = {"sample_passes_per_s": sum(x.sample_passes for x in tst) / tw, "wall_s": tw,
+                                  "us_per_batch": [x.device_ms * 1e3 / max(x.steps, 1) for x in tst],
+                                  "workload": "train_model x3 kinds concurrently, 2e5 samples, 20 epochs, "
+                                              "batch 512 (desk-scale weights job)"}
         r.upload_scene(scene)
 
     cpu = None

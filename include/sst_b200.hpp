@@ -147,6 +147,28 @@ class Context {
         return img;
     }
 
+    // generate_dataset(n, sigma_t range, g range, phi sampler, seed)  (dataset.cpp:40-92)
+    std::vector<sst_training_sample> generate_dataset(uint64_t n, double s_lo, double s_hi, double g_lo, double g_hi,
+                                                      int phi_kind, double phi_a, double phi_b, uint64_t seed,
+                                                      sst_dataset_stats* stats = nullptr) {
+        std::vector<sst_training_sample> out(n);
+        check(sst_gpu_generate_dataset(ctx_, n, s_lo, s_hi, g_lo, g_hi, phi_kind, phi_a, phi_b, seed, 0, out.data(),
+                                       SST_PTR_HOST, stats));
+        return out;
+    }
+
+    // train_model(kind, dataset, cfg) + save_model(path, model, with_encoder)  (cvae.cpp:234-377)
+    std::vector<sst_epoch_stats> train_model(int kind, const std::vector<sst_training_sample>& samples,
+                                             uint64_t dataset_seed, const sst_train_config& cfg,
+                                             const std::string& ssnn_path = "", bool include_encoder = true,
+                                             bool install = false, sst_train_stats* stats = nullptr) {
+        std::vector<sst_epoch_stats> epochs(cfg.epochs);
+        check(sst_gpu_train_model(ctx_, kind, samples.data(), samples.size(), SST_PTR_HOST, dataset_seed, &cfg,
+                                  epochs.data(), ssnn_path.empty() ? nullptr : ssnn_path.c_str(),
+                                  include_encoder ? 1 : 0, nullptr, install ? 1 : 0, stats));
+        return epochs;
+    }
+
   private:
     sst_gpu_ctx* ctx_ = nullptr;
     uint32_t width_ = 0, height_ = 0;
