@@ -25,6 +25,9 @@ SST_INTEGRATOR_PT = 0
 SST_INTEGRATOR_ST = 1
 SST_PTR_HOST = 0
 SST_PTR_DEVICE = 1
+SST_PHI_LOG_COMPLEMENT = 0
+SST_PHI_FIXED = 1
+SST_PHI_UNIFORM = 2
 
 SALT_RENDER_PIXEL = 0x06
 SALT_RENDER_CHANNEL = 0x07
