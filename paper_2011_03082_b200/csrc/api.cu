@@ -162,6 +162,7 @@ struct sst_gpu_ctx {
     cudaEvent_t ev_start = nullptr, last_film = nullptr;
     bool timing_open = false;
     int sphere_batch = 16;  // SST_SPHERE_BATCH overrides (tuning)
+    int trace_batch = 0;    // SST_TRACE_BATCH overrides (tuning; 0 = traversals never wait)
 };
 
 namespace {
@@ -652,6 +653,7 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.work = work;
     a.stats = ctx->stats.as<unsigned long long>();
     a.sphere_batch = ctx->sphere_batch;
+    a.trace_batch = ctx->trace_batch;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
     else CK(f64::launch_trace(a, st, explicit_keys, stream));
@@ -860,6 +862,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->serial = ++g_serial;
         if (const char* e = std::getenv("SST_SPHERE_BATCH")) ctx->sphere_batch = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("SST_TRACE_BATCH")) ctx->trace_batch = std::max(0, std::atoi(e));
         *out = ctx.release();
     });
 }

@@ -77,7 +77,9 @@ struct PathLocal {
     uint8_t c;
     bool r_valid;
     bool pending;   // a sphere step is requested and waits for its warp batch
-    uint16_t waited;
+    bool tpend;     // a traversal is requested and waits for its warp batch (t_pend = flight)
+    uint16_t waited, twaited;
+    R t_pend;
 };
 
 struct LaneStats {
@@ -121,6 +123,9 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
     p.r_valid = false;
     p.pending = false;
     p.waited = 0;
+    p.tpend = false;
+    p.twaited = 0;
+    p.t_pend = R(0);
 }
 
 // One iteration of the path loop, written as a fixed sequence of phases in which
@@ -148,7 +153,10 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     const ObjK<R>* ob = alive && p.obj >= 0 ? &sc.objs[p.obj] : nullptr;
     if (active) {
         inside = p.obj >= 0;
-        if (inside) {
+        if (p.tpend) {  // flight drawn in an earlier iteration, traversal still pending
+            t_free = p.t_pend;
+            trace = true;
+        } else if (inside) {
             const MediumK<R>& m = ob->med[p.c];
             if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
                 const R u = p.rng.template uniform<R>();
@@ -164,15 +172,41 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             // radius and, when that is too coarse, the finer skip grid.
             trace = !(t_free < p.r_here);
             if (trace) trace = !(t_free < skip_radius(*ob, p.x));
-            t_max = t_free;
         } else {
             trace = true;
         }
+        if (inside) t_max = t_free;
     }
+    // Traversals are regrouped per warp like sphere steps (trace_batch > 0): a lane
+    // whose flight needs the BVH parks it (t_pend) while lanes with culled flights keep
+    // iterating, until enough lanes (or every live lane) wait.
+    if (a.trace_batch > 0) {
+        if (active && trace && !p.tpend) {
+            p.tpend = true;
+            p.t_pend = t_free;
+            p.twaited = 0;
+        }
+        const unsigned tp = __ballot_sync(0xffffffffu, alive && p.tpend);
+        if (tp) {
+            const unsigned live = __ballot_sync(0xffffffffu, alive);
+            const unsigned sp = __ballot_sync(0xffffffffu, alive && p.pending);
+            const bool starving = __any_sync(0xffffffffu, alive && p.tpend && p.twaited >= 32);
+            const bool go = __popc(tp) >= a.trace_batch || (live & ~(tp | sp)) == 0u || starving;
+            if (alive && p.tpend) {
+                if (go) {
+                    p.tpend = false;
+                } else {
+                    ++p.twaited;
+                    trace = false;
+                }
+            }
+        }
+    }
+    const bool proceed = active && !p.tpend;  // this lane's flight is resolved this iteration
     bool hit = false;
     R t_hit = R(0);
     Hit h{0, 0};
-    if (trace) {
+    if (trace && proceed) {
         const RayK<R> ray = make_ray(p.x, p.w);
         const int want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
         hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, p.cull, want,
@@ -186,7 +220,7 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
 #endif
     // ---- 2. resolve
     bool collide = false;
-    if (active) {
+    if (proceed) {
         if (!inside) {
             if (!hit) {
                 p.L += sc.bg[p.c];
@@ -253,7 +287,8 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
         if (pend) {
             const unsigned live = __ballot_sync(0xffffffffu, alive && end < 0);
             const bool starving = __any_sync(0xffffffffu, alive && p.pending && p.waited >= 64);
-            const bool go = __popc(pend) >= a.sphere_batch || (live & ~pend) == 0u || starving;
+            const unsigned tpend = __ballot_sync(0xffffffffu, alive && p.tpend);
+            const bool go = __popc(pend) >= a.sphere_batch || (live & ~(pend | tpend)) == 0u || starving;
             if (alive && p.pending) {
                 if (!go) {
                     ++p.waited;

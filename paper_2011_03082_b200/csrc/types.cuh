@@ -119,6 +119,7 @@ struct TraceArgs {
     unsigned long long* work;   // path-id counter
     unsigned long long* stats;  // [kStCount]
     int sphere_batch;           // warp regrouping threshold for sphere steps (lanes)
+    int trace_batch;            // warp regrouping threshold for BVH traversals (0 = off)
 };
 
 // TrainingSample (dataset.hpp:17-27): the SSWK record, 52 bytes, no padding.
