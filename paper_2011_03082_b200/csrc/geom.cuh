@@ -91,6 +91,15 @@ template <class R>
 SST_D bool slab(const RayK<R>& r, R lox, R hix, R loy, R hiy, R loz, R hiz, R t_min, R t_max,
                 R* t_enter) {
     R t0 = t_min, t1 = t_max;
+    if constexpr (!Real<R>::kIsDouble) {  // FP32: branch-free min/max (inv is finite, no NaN)
+        const R nx = (lox - r.o.x) * r.inv.x, fx = (hix - r.o.x) * r.inv.x;
+        const R ny = (loy - r.o.y) * r.inv.y, fy = (hiy - r.o.y) * r.inv.y;
+        const R nz = (loz - r.o.z) * r.inv.z, fz = (hiz - r.o.z) * r.inv.z;
+        t0 = fmaxf(fmaxf(t0, fminf(nx, fx)), fmaxf(fminf(ny, fy), fminf(nz, fz)));
+        t1 = fminf(fminf(t1, fmaxf(nx, fx)), fminf(fmaxf(ny, fy), fmaxf(nz, fz)));
+        *t_enter = t0;
+        return t0 <= t1;
+    }
     R n = (lox - r.o.x) * r.inv.x, f = (hix - r.o.x) * r.inv.x;
     if (n > f) { const R t = n; n = f; f = t; }
     t0 = Real<R>::fmax_(t0, n);
@@ -117,7 +126,7 @@ SST_D R ray_tri(const RayK<R>& r, V3<R> v0, V3<R> e1, V3<R> e2, R t_min, R t_max
     const R det = dot(e1, pvec);
     *det_out = det;
     if (Real<R>::fabs_(det) < R(1e-14)) return R(-1);
-    const R inv_det = R(1) / det;
+    const R inv_det = Real<R>::div_(R(1), det);  // FP32: MUFU reciprocal (2 ulp); FP64: IEEE
     const V3<R> tvec = r.o - v0;
     const R u = dot(tvec, pvec) * inv_det;
     if (u < R(0) || u > R(1)) return R(-1);

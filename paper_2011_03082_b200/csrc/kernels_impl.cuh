@@ -65,8 +65,15 @@ __global__ void __launch_bounds__(128) k_step_batch(StepBatchArgs a) {
 
 // ---------------------------------------------------------------------------
 // Persistent path-tracing megakernel (PT or ST; render ids or explicit keys).
+// Minimum resident one-warp blocks per SM (register cap) per integrator; tuning knobs.
+#ifndef SST_ST_MIN_BLOCKS
+#define SST_ST_MIN_BLOCKS 16
+#endif
+#ifndef SST_PT_MIN_BLOCKS
+#define SST_PT_MIN_BLOCKS 24
+#endif
 template <bool ST, bool EXPLICIT>
-__global__ void __launch_bounds__(kTraceBlock, ST ? 16 : 24) k_trace(TraceArgs<R> a) {
+__global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_MIN_BLOCKS) k_trace(TraceArgs<R> a) {
     trace_persistent<R, ST, EXPLICIT>(a);
 }
 
