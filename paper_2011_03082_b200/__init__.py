@@ -9,8 +9,8 @@ this package is the Python host mirror. See DESIGN.md.
 from . import abi  # noqa: F401
 from .api import (PT, ST, Film, Image, Renderer, image_metrics, load_obj,  # noqa: F401
                   make_bumpy_sphere, make_icosphere, rng_init, save_dataset)
-from .scene import Medium, Scene, SceneObject, SdfGrid, c1_scene, c5_scene, uniform_media  # noqa: F401
+from .scene import Medium, Scene, SceneObject, SdfGrid, c1_scene, c3_scene, c5_scene, uniform_media  # noqa: F401
 
 __all__ = ["abi", "PT", "ST", "Film", "Image", "Renderer", "image_metrics", "load_obj",
            "make_bumpy_sphere", "make_icosphere", "rng_init", "save_dataset", "Medium", "Scene", "SceneObject",
-           "SdfGrid", "c1_scene", "c5_scene", "uniform_media"]
+           "SdfGrid", "c1_scene", "c3_scene", "c5_scene", "uniform_media"]

@@ -128,6 +128,24 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
     p.t_pend = R(0);
 }
 
+// FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)
+// only if x is OUTSIDE the object -- a path that believes it is inside missed its
+// exit crossing (non-watertight FP32 Moller-Trumbore at an edge). FP64 keeps the
+// reference's semantics untouched.
+template <class R>
+SST_D bool leaked(const ObjK<R>& ob, R v, bool in_grid) {
+    return !Real<R>::kIsDouble && (!in_grid || v > ob.sdf_voxel * R(1e-4));
+}
+// Recovery: continue as an outside ray from x (it re-enters or escapes), instead of
+// random-walking in the void until absorbed (10^5+ events: a launch-long tail).
+template <class R>
+SST_D void recover_leak(PathLocal<R>& p, const ObjK<R>& ob) {
+    p.cull = ob.convex ? p.obj : -1;
+    p.obj = -1;
+    p.skip = -1;
+    p.r_valid = false;
+}
+
 // One iteration of the path loop, written as a fixed sequence of phases in which
 // every expensive operation (BVH traversal, sphere step, NEE shadow traversal)
 // has exactly ONE call site: the kernel is instruction-cache bound, and lanes of a
@@ -153,6 +171,16 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     const ObjK<R>* ob = alive && p.obj >= 0 ? &sc.objs[p.obj] : nullptr;
     if (active) {
         inside = p.obj >= 0;
+        if (inside && !p.tpend && !p.r_valid) {
+            bool in_grid;
+            const R v = sdf_raw(*ob, p.x, &in_grid);
+            p.r_here = v < R(0) ? -v : R(0);
+            p.r_valid = true;
+            if (leaked(*ob, v, in_grid)) {
+                recover_leak(p, *ob);
+                inside = false;
+            }
+        }
         if (p.tpend) {  // flight drawn in an earlier iteration, traversal still pending
             t_free = p.t_pend;
             trace = true;
@@ -162,10 +190,6 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
                 const R u = p.rng.template uniform<R>();
                 if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
                 else t_free = -Real<R>::log_(R(1) - u) / m.sigma_t;
-            }
-            if (!p.r_valid) {
-                p.r_here = sdf_radius(*ob, p.x);
-                p.r_valid = true;
             }
             // A flight shorter than a conservative distance to the surface cannot
             // reach the boundary: skip the traversal (exact). Bounds: the scene SDF
@@ -256,8 +280,15 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     R nee_wt = R(1);
     bool event = collide;
     if (ST && collide) {
-        p.r_here = sdf_radius(*ob, p.x);
+        bool in_grid;
+        const R v = sdf_raw(*ob, p.x, &in_grid);
+        p.r_here = v < R(0) ? -v : R(0);
         p.r_valid = true;
+        if (leaked(*ob, v, in_grid)) {  // not in the medium: no event here
+            recover_leak(p, *ob);
+            collide = false;
+            event = false;
+        }
 #ifdef SST_TRACE_DEBUG
         printf("[gpu]   collide r=%.17g r_min=%.17g\n", (double)p.r_here, (double)ob->med[p.c].r_min);
 #endif

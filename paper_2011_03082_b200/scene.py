@@ -130,6 +130,14 @@ def c1_scene(mesh, width=256, height=256, sigma_t=10.0, sdf=None, sdf_resolution
                  width=width, height=height)
 
 
+def c3_scene(mesh, sigma_t, width=512, height=512, sdf=None, sdf_resolution=64) -> Scene:
+    """Config 3: one SDF-boundary mesh (bumpy sphere / icosphere(4)), homogeneous medium of
+    density sigma_t (the density-doubling sweep runs sigma_t = 10..160), one point light."""
+    pos, tri = mesh
+    return Scene(objects=[SceneObject(pos, tri, uniform_media(sigma_t), sdf, sdf_resolution)],
+                 width=width, height=height)
+
+
 def c5_scene(mesh, width=1920, height=1080, sigmas=(20.0, 40.0, 80.0, 160.0), sdfs=None,
              sdf_resolution=64) -> Scene:
     """Config 5 teaser: four unit icospheres in a row, density doubling left to right."""

@@ -222,6 +222,28 @@ def test_fp32_has_no_surface_leaks(renderer, ico3):
     assert st.errors == 0
 
 
+def test_fp32_leak_recovery_bounds_path_length():
+    """FP32 Moller-Trumbore is not watertight: an exit crossing through a shared edge can
+    be missed (~1e-6 per path on icosphere(4)). Such a path used to random-walk outside
+    the medium until absorbed (~1e5 events at phi = 0.99999, a launch-long tail); the SDF
+    sign check at every flight start returns it to the outside instead. 8M PT paths at
+    sigma_t = 10: the longest path stays in the natural range (no 1e4+ event walks)."""
+    import paper_2011_03082_b200 as sb
+    r = sb.Renderer(0, "f32")
+    try:
+        r.upload_scene(sb.c3_scene(sb.make_icosphere(4, 1.0), 10.0, 512, 512))
+        rng = np.random.default_rng(7)
+        n = 8_000_000
+        pix = rng.integers(0, 512 * 512, n).astype(np.uint32)
+        smp = rng.integers(0, 1 << 20, n).astype(np.uint32)
+        ch = np.zeros(n, np.uint8)  # channel 0: phi = 0.99999
+        rad, seg = r.trace_paths(sb.PT, 1, 5, pix, smp, ch)
+        assert np.isfinite(rad).all()
+        assert seg.max() < 10_000, int(seg.max())
+    finally:
+        r.close()
+
+
 @pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
 def test_nonconvex_bumpy_scene_paths_match_oracle(renderer, oracle, models_dir, precision, rtol, frac):
     """Config-3 geometry (bumpy sphere, non-convex: no exit culling; FP32 relies on the
