@@ -337,6 +337,21 @@ def bench_ours(args, world, rank, local):
                                "events_per_s": dst.events / (dst.device_ms / 1e3),
                                "time_1e8_walks_s": 1e8 / (dst.walks / (dst.device_ms / 1e3)),
                                "sample": "2e6 walks, sigma_t U[0,200], g U[-1,1], phi 1-10^U[-5,-0.5]"}
+        # config 3: density-doubling sweep on the SDF-boundary bumpy-sphere scene (512x512)
+        bumpy = sb.make_bumpy_sphere(4, 1.0, 0.2, 3.0)
+        sweep = []
+        for sig in (10.0, 40.0, 160.0):
+            r.upload_scene(sb.c3_scene(bumpy, sig))
+            row = {"sigma_t": sig}
+            for iname, integ in (("st", sb.ST), ("pt", sb.PT)):
+                r.render_film(integ, 1000, 1, True, 0, 1)  # warm-up
+                est = abi.PathStats()
+                r.render_film(integ, 1000, 1, True, 1, 9, stats=est)
+                row[iname + "_segments_per_s"] = est.segments / (est.device_ms / 1e3)
+                row[iname + "_frame_1000spp_s"] = est.device_ms / 8
+            row["st_speedup_vs_pt"] = row["pt_frame_1000spp_s"] / row["st_frame_1000spp_s"]
+            sweep.append(row)
+        extra["c3_density_sweep"] = {"scene": "bumpy sphere(4), 512x512, NEE, 8 spp measured", "rows": sweep}
         # CVAE training (row f3): the desk-scale weights job, 3 kinds concurrently
         r.train_models(out[:5000], dataset_seed=7, epochs=1)  # warm-up
         t0 = time.perf_counter()
