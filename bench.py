@@ -332,11 +332,11 @@ def bench_ours(args, world, rank, local):
         dst = abi.DatasetStats()
         out, _ = r.generate_dataset(200000, seed=7)  # warm-up
         dst = abi.DatasetStats()
-        r.generate_dataset(2000000, seed=7, first_index=200000, stats=dst)
+        r.generate_dataset(8000000, seed=7, first_index=200000, stats=dst)
         extra["c4_dataset"] = {"walks_per_s": dst.walks / (dst.device_ms / 1e3),
                                "events_per_s": dst.events / (dst.device_ms / 1e3),
                                "time_1e8_walks_s": 1e8 / (dst.walks / (dst.device_ms / 1e3)),
-                               "sample": "2e6 walks, sigma_t U[0,200], g U[-1,1], phi 1-10^U[-5,-0.5]"}
+                               "sample": "8e6 walks, sigma_t U[0,200], g U[-1,1], phi 1-10^U[-5,-0.5]"}
         # config 3: density-doubling sweep on the SDF-boundary bumpy-sphere scene (512x512)
         bumpy = sb.make_bumpy_sphere(4, 1.0, 0.2, 3.0)
         sweep = []
@@ -357,7 +357,9 @@ def bench_ours(args, world, rank, local):
         t0 = time.perf_counter()
         _, tst = r.train_models(out, dataset_seed=7, epochs=20, seed=1)
         tw = time.perf_counter() - t0
-        extra["cvae_training"] = {"sample_passes_per_s": sum(x.sample_passes for x in tst) / tw, "wall_s": tw,
+        dev_s = max(x.device_ms for x in tst) / 1e3  # the three kinds run concurrently
+        extra["cvae_training"] = {"sample_passes_per_s": sum(x.sample_passes for x in tst) / dev_s,
+                                  "device_s": dev_s, "wall_s": tw,
                                   "us_per_batch": [x.device_ms * 1e3 / max(x.steps, 1) for x in tst],
                                   "workload": "train_model x3 kinds concurrently, 2e5 samples, 20 epochs, "
                                               "batch 512 (desk-scale weights job)"}
