@@ -26,7 +26,12 @@ struct Real<float> {
     // Free-flight epsilon for rays leaving a surface (FP32 self-intersection guard).
     static constexpr float kSurfaceEps = 2e-6f;
     static constexpr float kInf = 3e38f;
-    SST_D static float sqrt_(float x) { return sqrtf(x); }
+    // MUFU square root (sqrt.approx, ~1 ulp): FP32 statistical parity, FP64 stays IEEE
+    SST_D static float sqrt_(float x) {
+        float r;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+        return r;
+    }
     SST_D static float exp_(float x) { return __expf(x); }
     SST_D static float log_(float x) { return __logf(x); }
     SST_D static float log1p_(float x) { return log1pf(x); }
@@ -98,7 +103,9 @@ SST_HD V3<R> cross(V3<R> a, V3<R> b) {
 template <class R>
 SST_D V3<R> normalize(V3<R> v) {
     const R len = Real<R>::sqrt_(dot(v, v));
-    return {v.x / len, v.y / len, v.z / len};
+    if (Real<R>::kIsDouble) return {v.x / len, v.y / len, v.z / len};
+    const R inv = Real<R>::div_(R(1), len);
+    return {v.x * inv, v.y * inv, v.z * inv};
 }
 template <class R>
 SST_HD R comp(V3<R> v, int a) { return a == 0 ? v.x : (a == 1 ? v.y : v.z); }
@@ -107,7 +114,7 @@ SST_HD R comp(V3<R> v, int a) { return a == 0 ? v.x : (a == 1 ? v.y : v.z); }
 template <class R>
 SST_D void onb(V3<R> n, V3<R>* b1, V3<R>* b2) {
     const R sign = copysign(R(1), n.z);
-    const R a = R(-1) / (sign + n.z);
+    const R a = Real<R>::div_(R(-1), sign + n.z);  // |sign + n.z| >= 1
     const R b = n.x * n.y * a;
     *b1 = mk<R>(R(1) + sign * n.x * n.x * a, sign * b, -sign * n.x);
     *b2 = mk<R>(b, sign + n.y * n.y * a, -n.y);

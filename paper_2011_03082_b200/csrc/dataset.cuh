@@ -136,7 +136,7 @@ SST_D void dataset_persistent(const DatasetArgs& a) {
         R step;
         if (w.vacuum) step = R(2);
         else if (Real<R>::kIsDouble) step = -Real<R>::log1p_(-w.rng.template uniform<R>()) / w.sigma;
-        else step = -Real<R>::log_(R(1) - w.rng.template uniform<R>()) / w.sigma;
+        else step = -Real<R>::div_(Real<R>::log_(R(1) - w.rng.template uniform<R>()), w.sigma);
         const R t_exit = sphere_exit_t(w.pos, dir);
         if (w.vacuum || step >= t_exit) {
             // pass 2 never gets here (k <= N)

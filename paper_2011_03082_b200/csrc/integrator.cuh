@@ -23,8 +23,8 @@ namespace sstg {
 template <class R>
 SST_D R hg_cos(R g, R u) {
     if (Real<R>::fabs_(g) < R(1e-4)) return R(1) - R(2) * u;
-    const R s = (R(1) - g * g) / (R(1) + g - R(2) * g * u);
-    const R c = (R(1) + g * g - s * s) / (R(2) * g);
+    const R s = Real<R>::div_(R(1) - g * g, R(1) + g - R(2) * g * u);
+    const R c = Real<R>::div_(R(1) + g * g - s * s, R(2) * g);
     return c < R(-1) ? R(-1) : (c > R(1) ? R(1) : c);
 }
 
@@ -44,7 +44,7 @@ SST_D V3<R> hg_sample(R g, V3<R> w_in, R u1, R u2) {
 template <class R>
 SST_D R hg_eval(R g, R c) {
     const R denom = R(1) + g * g - R(2) * g * c;
-    return R(kInv4PiD) * (R(1) - g * g) / (denom * Real<R>::sqrt_(denom));
+    return Real<R>::div_(R(kInv4PiD) * (R(1) - g * g), denom * Real<R>::sqrt_(denom));
 }
 
 // NEE toward the point light from p (in object obj, channel c) with incoming w:
@@ -189,7 +189,7 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
                 const R u = p.rng.template uniform<R>();
                 if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
-                else t_free = -Real<R>::log_(R(1) - u) / m.sigma_t;
+                else t_free = -Real<R>::div_(Real<R>::log_(R(1) - u), m.sigma_t);
             }
             // A flight shorter than a conservative distance to the surface cannot
             // reach the boundary: skip the traversal (exact). Bounds: the scene SDF
