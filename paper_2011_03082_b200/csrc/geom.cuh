@@ -79,9 +79,9 @@ SST_D RayK<R> make_ray(V3<R> o, V3<R> d) {
         r.inv = mk<R>(R(1) / d.x, R(1) / d.y, R(1) / d.z);
     } else {
         const float e = 1e-20f;
-        r.inv = mk<R>(1.0f / (fabsf(d.x) > e ? d.x : copysignf(e, d.x)),
-                      1.0f / (fabsf(d.y) > e ? d.y : copysignf(e, d.y)),
-                      1.0f / (fabsf(d.z) > e ? d.z : copysignf(e, d.z)));
+        r.inv = mk<R>(__fdividef(1.0f, fabsf(d.x) > e ? d.x : copysignf(e, d.x)),
+                      __fdividef(1.0f, fabsf(d.y) > e ? d.y : copysignf(e, d.y)),
+                      __fdividef(1.0f, fabsf(d.z) > e ? d.z : copysignf(e, d.z)));
     }
     return r;
 }

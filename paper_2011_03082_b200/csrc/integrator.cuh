@@ -55,12 +55,14 @@ SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<
     const V3<R> to_l = sc.light - p;
     const R d2 = dot(to_l, to_l);
     const R d = Real<R>::sqrt_(d2);
-    const V3<R> wl = to_l / d;
+    const R inv_d = Real<R>::div_(R(1), d);  // FP64: IEEE 1/d (the reference divides; see below)
+    const V3<R> wl = Real<R>::kIsDouble ? to_l / d : to_l * inv_d;
     const RayK<R> ray = make_ray(p, wl);
     const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c, tri_tests)
                               : optical_depth(sc, ray, sc.t_min, d, c);
     const R phase = hg_eval(m.g, dot(w, wl));
-    return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) / d2;
+    if (Real<R>::kIsDouble) return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) / d2;
+    return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) * (inv_d * inv_d);
 }
 
 template <class R>
