@@ -344,8 +344,8 @@ SST_HD uint32_t cube_cell(R x, R y, R z, uint32_t res) {
         face = z > R(0) ? 4u : 5u;
         m = az; s = x; t = y;
     }
-    const R fs = (s / m + R(1)) * R(0.5) * static_cast<R>(res);
-    const R ft = (t / m + R(1)) * R(0.5) * static_cast<R>(res);
+    const R fs = (Real<R>::div_(s, m) + R(1)) * R(0.5) * static_cast<R>(res);
+    const R ft = (Real<R>::div_(t, m) + R(1)) * R(0.5) * static_cast<R>(res);
     int i = static_cast<int>(fs), j = static_cast<int>(ft);
     i = i < 0 ? 0 : (i >= static_cast<int>(res) ? static_cast<int>(res) - 1 : i);
     j = j < 0 ? 0 : (j >= static_cast<int>(res) ? static_cast<int>(res) - 1 : j);

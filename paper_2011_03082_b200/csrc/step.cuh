@@ -40,7 +40,7 @@ SST_D R lambda_weight(uint32_t n, const MediumK<R>& m) {
         const R phi_n = Real<R>::exp_(static_cast<R>(n) * m.log_phi);
         return m.phi * (R(1) - phi_n) / (R(1) - m.phi);
     }
-    return m.phi * (-Real<R>::expm1_(static_cast<R>(n) * m.log_phi)) / m.one_minus_phi;
+    return Real<R>::div_(m.phi * (-Real<R>::expm1_(static_cast<R>(n) * m.log_phi)), m.one_minus_phi);
 }
 
 // rotation_z(2 pi u) (vec3.hpp:75-78): returns (cos, sin).
@@ -142,7 +142,8 @@ SST_D bool sphere_step(const MediumK<R>& m, V3<R> w_in, V3<R> center, R r, bool 
         if (lx >= R(1)) X = X * (R(0.999) / lx);
         V3<R> W = mk<R>(out[3], out[4], out[5]);
         const R lw = Real<R>::sqrt_(dot(W, W));
-        W = lw > R(0) ? W / lw : mk<R>(R(0), R(0), R(1));
+        if (Real<R>::kIsDouble) W = lw > R(0) ? W / lw : mk<R>(R(0), R(0), R(1));
+        else W = lw > R(0) ? W * Real<R>::div_(R(1), lw) : mk<R>(R(0), R(0), R(1));
         o.rep_pos = center + (rot * X) * r;
         o.rep_dir = rot * W;
         o.lambda = lambda_weight(o.n, m);
