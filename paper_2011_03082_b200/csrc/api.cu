@@ -157,7 +157,18 @@ struct sst_gpu_ctx {
         cudaStream_t s = nullptr;
         DevBuf rad, work;
         cudaEvent_t film_done = nullptr;
+        // wavefront pool (wavefront.cuh) + pinned queue counters read by the host loop
+        DevBuf wf;
+        uint32_t* wf_host = nullptr;  // [2][kQCount]
+        cudaEvent_t wf_ev[2] = {nullptr, nullptr};
     } slots[kSlots];
+    // Wavefront integrator (SST_WAVEFRONT=0: megakernel only). Pool slots per launch,
+    // hand-off when live slots <= min(pool / 8, wf_tail), iterations per host check.
+    bool wavefront = true;
+    uint32_t wf_pool = 1u << 21;
+    uint32_t wf_tail = 1u << 16;
+    uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
+    int wf_batch = 4;
     int next_slot = 0;
     cudaEvent_t ev_start = nullptr, last_film = nullptr;
     bool timing_open = false;
@@ -633,11 +644,102 @@ const DevScene<R>& scene_of(const sst_gpu_ctx* ctx) {
 
 constexpr uint64_t kChunkPaths = 1ull << 24;  // radiance scratch per launch
 
+// Carves the wavefront pool of `cap` slots out of the slot's device buffer.
+template <class R>
+WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
+    const size_t n = cap;
+    const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
+                            n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
+                            kQCount * 4, 8, n * 4, n * 4};
+    size_t off[18], total = 0;
+    int k = 0;
+    for (size_t b : sizes) {
+        off[k++] = total;
+        total += (b + 255) & ~size_t(255);
+    }
+    sl.wf.reserve(total);
+    char* base = sl.wf.as<char>();
+    WfPool<R> q{};
+    q.cap = cap;
+    q.xl = reinterpret_cast<Q4<R>*>(base + off[0]);
+    q.wr = reinterpret_cast<Q4<R>*>(base + off[1]);
+    q.rng = reinterpret_cast<uint64_t*>(base + off[2]);
+    q.meta = reinterpret_cast<uint4*>(base + off[3]);
+    q.tpend = reinterpret_cast<R*>(base + off[4]);
+    q.thit = reinterpret_cast<R*>(base + off[5]);
+    q.hinfo = reinterpret_cast<uint2*>(base + off[6]);
+    q.nee_p = reinterpret_cast<Q4<R>*>(base + off[7]);
+    q.nee_w = reinterpret_cast<Q4<R>*>(base + off[8]);
+    q.q_trace = reinterpret_cast<uint32_t*>(base + off[9]);
+    q.q_sphere = reinterpret_cast<uint32_t*>(base + off[10]);
+    q.q_shadow = reinterpret_cast<uint32_t*>(base + off[11]);
+    q.q_live = reinterpret_cast<uint32_t*>(base + off[12]);
+    q.counts = reinterpret_cast<uint32_t*>(base + off[13]);
+    q.resume_work = reinterpret_cast<unsigned long long*>(base + off[14]);
+    q.q_la = reinterpret_cast<uint32_t*>(base + off[15]);
+    q.q_lb = reinterpret_cast<uint32_t*>(base + off[16]);
+    return q;
+}
+
+// Wavefront render of one launch's paths (wavefront.cuh): iterations of
+// logic -> trace -> sphere -> shadow over a pool of path slots until the live slots
+// drop to min(pool/8, wf_tail), then the megakernel finishes the tail. The host checks
+// the live count of batch k-1 while batch k runs (no bubble).
+template <class R>
+void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_keys, sst_gpu_ctx::Slot& sl,
+                   cudaStream_t stream) {
+    const uint32_t cap = static_cast<uint32_t>(std::max<uint64_t>(32, std::min<uint64_t>(a.n_paths, ctx->wf_pool)));
+    a.pool = carve_pool<R>(sl, cap);
+    if (!sl.wf_host) {
+        CK(cudaMallocHost(&sl.wf_host, 2 * kQCount * sizeof(uint32_t)));
+        for (auto& e : sl.wf_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_init(a, stream));
+    else CK(f64::launch_wf_init(a, stream));
+    const uint32_t thresh = std::max<uint32_t>(1, std::min<uint32_t>(cap / 8, ctx->wf_tail));
+    const int batch = std::max(1, ctx->wf_batch);
+    uint64_t it = 0;
+    int out_last[2] = {kQLiveA, kQLiveA};
+    const bool wf_trace = std::getenv("SST_WF_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    for (uint64_t k = 0;; ++k) {
+        for (int b = 0; b < batch; ++b, ++it) {
+            const bool even = (it & 1) == 0;  // live lists ping-pong: A -> B -> A ...
+            a.pool.q_in = even ? a.pool.q_la : a.pool.q_lb;
+            a.pool.q_out = even ? a.pool.q_lb : a.pool.q_la;
+            a.pool.cnt_in = even ? kQLiveA : kQLiveB;
+            a.pool.cnt_out = even ? kQLiveB : kQLiveA;
+            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_iteration(a, st, explicit_keys, stream));
+            else CK(f64::launch_wf_iteration(a, st, explicit_keys, stream));
+        }
+        out_last[k & 1] = a.pool.cnt_out;
+        uint32_t* h = sl.wf_host + (k & 1) * kQCount;
+        CK(cudaMemcpyAsync(h, a.pool.counts, kQCount * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+        CK(cudaEventRecord(sl.wf_ev[k & 1], stream));
+        if (k == 0) continue;
+        CK(cudaEventSynchronize(sl.wf_ev[(k - 1) & 1]));
+        // live slots after the last logic pass of batch k-1; K_logic refills every empty
+        // slot while path ids remain, so live <= thresh < cap means the supply is exhausted
+        const uint32_t live = sl.wf_host[((k - 1) & 1) * kQCount + out_last[(k - 1) & 1]];
+        if (wf_trace) {
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[wf] batch %llu live %u trace %u sphere %u shadow %u t %.3f ms\n",
+                         static_cast<unsigned long long>(k - 1), live, sl.wf_host[((k - 1) & 1) * kQCount + kQTrace],
+                         sl.wf_host[((k - 1) & 1) * kQCount + kQSphere], sl.wf_host[((k - 1) & 1) * kQCount + kQShadow],
+                         std::chrono::duration<double, std::milli>(now - t_start).count());
+        }
+        if (live <= thresh) break;
+    }
+    if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, explicit_keys, stream));
+    else CK(f64::launch_wf_finish(a, st, explicit_keys, stream));
+}
+
 template <class R>
 void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_keys, int nee,
                uint64_t seed, uint64_t n_paths, uint32_t n_pix, uint32_t sample_begin,
                const uint32_t* pix, const uint32_t* smp, const uint8_t* ch, R* radiance,
-               uint32_t* segments, unsigned long long* work, cudaStream_t stream) {
+               uint32_t* segments, unsigned long long* work, cudaStream_t stream,
+               sst_gpu_ctx::Slot* wf) {
     TraceArgs<R> a{};
     a.sc = sc;
     a.nee = nee;
@@ -655,16 +757,23 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.sphere_batch = ctx->sphere_batch;
     a.trace_batch = ctx->trace_batch;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
+    if (wf && ctx->wavefront && n_paths < (1ull << 32) && ctx->desc.n_objects < 250) {
+        run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream);
+        return;
+    }
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
     else CK(f64::launch_trace(a, st, explicit_keys, stream));
 }
 
 void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
-    unsigned long long v[kStCount];
-    CK(cudaMemcpyAsync(v, ctx->stats.p, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long all[kStCopies * kStCount];
+    CK(cudaMemcpyAsync(all, ctx->stats.p, sizeof all, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    unsigned long long v[kStCount] = {};
+    for (int c = 0; c < kStCopies; ++c)
+        for (int k = 0; k < kStCount; ++k) v[k] += all[c * kStCount + k];
     if (v[kStErrors]) {
-        CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+        CK(cudaMemsetAsync(ctx->stats.p, 0, sizeof all, ctx->stream));
         // the reference throws std::runtime_error (scatter.cpp:56)
         if (out) {
             out->errors += v[kStErrors];
@@ -706,8 +815,8 @@ void ensure_pipeline(sst_gpu_ctx* ctx) {
     CK(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
-    ctx->stats.reserve(kStCount * sizeof(unsigned long long));
-    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+    ctx->stats.reserve(kStCopies * kStCount * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCopies * kStCount * sizeof(unsigned long long), ctx->stream));
 }
 
 // Makes ctx->stream wait for every render slot (no host synchronisation).
@@ -730,7 +839,7 @@ void collect_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
     }
     if (out) out->device_ms += ms;
     read_stats(ctx, out);
-    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCount * sizeof(unsigned long long), ctx->stream));
+    CK(cudaMemsetAsync(ctx->stats.p, 0, kStCopies * kStCount * sizeof(unsigned long long), ctx->stream));
 }
 
 template <class R>
@@ -746,6 +855,9 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
     // the next ones on the pipeline slots
     uint64_t target = std::min<uint64_t>(kChunkPaths, std::max<uint64_t>(per_sample * n_samples / 8, 1ull << 20));
     if (const char* e = std::getenv("SST_CHUNK_PATHS")) target = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+    // wavefront: one pool drain per chunk, so chunks are as large as the radiance
+    // scratch allows (2^28 paths = 1 GiB FP32): the long-path tail is paid once
+    if (ctx->wavefront) target = ctx->wf_chunk;
     uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, target / per_sample));
     if (chunk > n_samples) chunk = n_samples;
     ensure_pipeline(ctx);
@@ -772,7 +884,8 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         sl.rad.reserve(per_sample * chunk * sizeof(R));
         CK(cudaStreamWaitEvent(sl.s, ctx->ev_start, 0));
         run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, false, nee, seed, per_sample * ns, n_pix, s,
-                     nullptr, nullptr, nullptr, sl.rad.as<R>(), nullptr, sl.work.as<unsigned long long>(), sl.s);
+                     nullptr, nullptr, nullptr, sl.rad.as<R>(), nullptr, sl.work.as<unsigned long long>(), sl.s,
+                     &sl);
         if (ctx->last_film) CK(cudaStreamWaitEvent(sl.s, ctx->last_film, 0));
         if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
         else CK(f64::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
@@ -820,7 +933,7 @@ void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, 
     run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, true, nee, seed, n, n_pix, 0,
                  ctx->keys_pix.as<uint32_t>(), ctx->keys_smp.as<uint32_t>(), ctx->keys_ch.as<uint8_t>(),
                  ctx->radiance.as<R>(), ctx->segments.as<uint32_t>(), ctx->work.as<unsigned long long>(),
-                 ctx->stream);
+                 ctx->stream, &ctx->slots[0]);
     std::vector<R> rad(n);
     CK(cudaMemcpyAsync(rad.data(), ctx->radiance.p, n * sizeof(R), cudaMemcpyDeviceToHost, ctx->stream));
     if (segments) CK(cudaMemcpyAsync(segments, ctx->segments.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -863,6 +976,11 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         ctx->serial = ++g_serial;
         if (const char* e = std::getenv("SST_SPHERE_BATCH")) ctx->sphere_batch = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SST_TRACE_BATCH")) ctx->trace_batch = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("SST_WAVEFRONT")) ctx->wavefront = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SST_WF_POOL")) ctx->wf_pool = static_cast<uint32_t>(std::max(32, std::atoi(e)));
+        if (const char* e = std::getenv("SST_WF_TAIL")) ctx->wf_tail = static_cast<uint32_t>(std::max(1, std::atoi(e)));
+        if (const char* e = std::getenv("SST_WF_BATCH")) ctx->wf_batch = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("SST_WF_CHUNK")) ctx->wf_chunk = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
         *out = ctx.release();
     });
 }
@@ -889,6 +1007,10 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         if (sl.s) cudaStreamSynchronize(sl.s);
         sl.rad.release();
         sl.work.release();
+        sl.wf.release();
+        if (sl.wf_host) cudaFreeHost(sl.wf_host);
+        for (auto& e : sl.wf_ev)
+            if (e) cudaEventDestroy(e);
         if (sl.film_done) cudaEventDestroy(sl.film_done);
         if (sl.s) cudaStreamDestroy(sl.s);
     }

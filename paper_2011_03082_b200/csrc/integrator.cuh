@@ -228,6 +228,7 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             }
         }
     }
+    else if (active) p.tpend = false;  // resumed wavefront slot: its queued traversal runs now
     const bool proceed = active && !p.tpend;  // this lane's flight is resolved this iteration
     bool hit = false;
     R t_hit = R(0);
@@ -363,6 +364,10 @@ SST_D T warp_sum(T v) {
     return v;
 }
 
+// Wavefront slot -> path state (wavefront.cuh).
+template <class R>
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase);
+
 template <class R, bool ST, bool EXPLICIT>
 SST_D void trace_persistent(const TraceArgs<R>& a) {
     const unsigned lane = threadIdx.x & 31u;
@@ -378,7 +383,15 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
             base = __shfl_sync(0xffffffffu, base, leader);
             if (!alive && !exhausted) {
                 const uint64_t my = base + __popc(need & ((1u << lane) - 1u));
-                if (my < a.n_paths) {
+                if (a.resume) {  // hand-off of the wavefront pool's live slots
+                    if (my < a.pool.counts[kQResume]) {
+                        uint32_t phase;
+                        load_slot(a.pool, a.pool.q_live[my], p, &phase);
+                        alive = true;
+                    } else {
+                        exhausted = true;
+                    }
+                } else if (my < a.n_paths) {
                     path_init<R, EXPLICIT>(a, my, p);
                     alive = true;
                 } else {
@@ -405,10 +418,11 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
     unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
                                       st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow,
                                       st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters};
+    unsigned long long* dst = a.stats + static_cast<size_t>(blockIdx.x % kStCopies) * kStCount;
 #pragma unroll
     for (int k = 0; k < kStCount; ++k) {
         const unsigned long long s = warp_sum(v[k]);
-        if (lane == 0 && s) atomicAdd(a.stats + k, s);
+        if (lane == 0 && s) atomicAdd(dst + k, s);
     }
 }
 

@@ -5,6 +5,7 @@
 
 #include "dataset.cuh"
 #include "integrator.cuh"
+#include "wavefront.cuh"
 #include "launch.h"
 
 namespace sstg {
@@ -78,6 +79,19 @@ __global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_M
 }
 
 // ---------------------------------------------------------------------------
+// Wavefront integrator kernels (wavefront.cuh). Persistent grid-stride kernels sized
+// to the resident capacity (SM count x blocks per SM) so per-block stat flushes stay few.
+constexpr int kWfBlock = 256;
+template <bool ST, bool EX>
+__global__ void __launch_bounds__(kWfBlock) k_wf_logic(TraceArgs<R> a) { wf_logic<R, ST, EX>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock) k_wf_trace(TraceArgs<R> a) { wf_trace<R>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock, 2) k_wf_sphere(TraceArgs<R> a) { wf_sphere<R>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock) k_wf_compact(TraceArgs<R> a) { wf_compact<R>(a.pool); }
+__global__ void __launch_bounds__(kWfBlock) k_wf_init(TraceArgs<R> a) { wf_init<R>(a.pool); }
+__global__ void k_wf_reset(TraceArgs<R> a) { wf_reset<R>(a.pool); }
+
+// ---------------------------------------------------------------------------
 // Config 4: training-data generation (persistent, one sample per lane).
 __global__ void __launch_bounds__(kTraceBlock) k_dataset(DatasetArgs a) { dataset_persistent<R>(a); }
 
@@ -144,6 +158,65 @@ static cudaError_t launch_trace_t(const TraceArgs<R>& a, cudaStream_t s) {
     if (grid < 1) grid = 1;
     k_trace<ST, EX><<<static_cast<unsigned>(grid), kTraceBlock, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+template <class K>
+static unsigned wf_grid(K kernel, uint32_t items) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWfBlock, 0);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t g = static_cast<uint64_t>(sm_count()) * per_sm;
+    const uint64_t need = (static_cast<uint64_t>(items) + kWfBlock - 1) / kWfBlock;
+    if (g > need) g = need;
+    return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {
+    k_wf_init<<<wf_grid(k_wf_init, a.pool.cap), kWfBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// One wavefront iteration (a.pool.q_in/q_out set by the caller; queue counters cleared first).
+cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {
+    static unsigned g_logic[2][2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
+    static uint32_t cap_seen = 0;
+    if (cap_seen != a.pool.cap) {  // grids depend on the pool size only
+        cap_seen = a.pool.cap;
+        g_logic[0][0] = wf_grid(k_wf_logic<false, false>, a.pool.cap);
+        g_logic[0][1] = wf_grid(k_wf_logic<false, true>, a.pool.cap);
+        g_logic[1][0] = wf_grid(k_wf_logic<true, false>, a.pool.cap);
+        g_logic[1][1] = wf_grid(k_wf_logic<true, true>, a.pool.cap);
+        g_trace = wf_grid(k_wf_trace, a.pool.cap);
+        g_sphere = wf_grid(k_wf_sphere, a.pool.cap);
+        g_shadow = wf_grid(k_wf_shadow, a.pool.cap);
+    }
+    k_wf_reset<<<1, 32, 0, s>>>(a);
+    const unsigned gl = g_logic[st][explicit_keys];
+    if (st) {
+        if (explicit_keys) k_wf_logic<true, true><<<gl, kWfBlock, 0, s>>>(a);
+        else k_wf_logic<true, false><<<gl, kWfBlock, 0, s>>>(a);
+    } else {
+        if (explicit_keys) k_wf_logic<false, true><<<gl, kWfBlock, 0, s>>>(a);
+        else k_wf_logic<false, false><<<gl, kWfBlock, 0, s>>>(a);
+    }
+    k_wf_trace<<<g_trace, kWfBlock, 0, s>>>(a);
+    if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s>>>(a);
+    if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Hand-off: compact the live slots and finish them in the megakernel.
+cudaError_t launch_wf_finish(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(a.pool.counts + kQResume, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    k_wf_compact<<<wf_grid(k_wf_compact, a.pool.cap), kWfBlock, 0, s>>>(a);
+    e = cudaMemsetAsync(a.pool.resume_work, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    TraceArgs<R> r = a;
+    r.resume = 1;
+    r.work = a.pool.resume_work;
+    r.n_paths = a.pool.cap;  // upper bound on live slots: sizes the grid
+    return launch_trace(r, st, explicit_keys, s);
 }
 
 cudaError_t launch_trace(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {

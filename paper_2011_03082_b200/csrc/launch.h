@@ -15,6 +15,11 @@ constexpr int kTraceBlock = 32;  // one warp per block: a long-path tail strands
     cudaError_t launch_step_batch(const StepBatchArgs& a, cudaStream_t s);                      \
     cudaError_t launch_trace(const TraceArgs<REAL>& a, bool st, bool explicit_keys,             \
                              cudaStream_t s);                                                   \
+    cudaError_t launch_wf_init(const TraceArgs<REAL>& a, cudaStream_t s);                       \
+    cudaError_t launch_wf_iteration(const TraceArgs<REAL>& a, bool st, bool explicit_keys,      \
+                                    cudaStream_t s);                                            \
+    cudaError_t launch_wf_finish(const TraceArgs<REAL>& a, bool st, bool explicit_keys,         \
+                                 cudaStream_t s);                                               \
     cudaError_t launch_film(const REAL* radiance, uint64_t stride, uint32_t n_samples,          \
                             double* sum, double* sumsq, cudaStream_t s);                        \
     cudaError_t launch_dataset(const DatasetArgs& a, cudaStream_t s);                           \

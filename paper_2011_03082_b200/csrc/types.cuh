@@ -103,6 +103,39 @@ enum : int {
     kStTraversals, kStNodes, kStTriTests, kStLaneIters, kStWarpIters, kStCount
 };
 
+// Stats are kept in kStCopies interleaved copies ([copy][kStCount]) so the per-block
+// flushes of the short wavefront kernels do not serialise on one address.
+constexpr int kStCopies = 64;
+
+// Wavefront path pool (wavefront.cuh): per-slot path state as structure-of-arrays of
+// 16-byte vectors (FP32; 32 bytes for FP64), plus the per-operation slot queues.
+template <class R>
+struct alignas(4 * sizeof(R)) Q4 {
+    R x, y, z, w;
+};
+// counts[]: queue lengths, the two ping-pong live-slot lists, the hand-off list.
+enum : int { kQTrace = 0, kQSphere = 1, kQShadow = 2, kQLiveA = 3, kQLiveB = 4, kQResume = 5, kQCount = 8 };
+template <class R>
+struct WfPool {
+    uint32_t cap;     // slots
+    Q4<R>* xl;        // position, radiance
+    Q4<R>* wr;        // direction, SDF radius at the position
+    uint64_t* rng;    // RandomStream state
+    uint4* meta;      // path id, segments, skip triangle, packed obj/channel/flags/phase/cull
+    R* tpend;         // free-flight length of the queued traversal
+    R* thit;          // traversal result: distance
+    uint2* hinfo;     // traversal result: triangle, object | found << 31
+    Q4<R>* nee_p;     // NEE record: point, weight
+    Q4<R>* nee_w;     // NEE record: direction
+    uint32_t *q_trace, *q_sphere, *q_shadow, *q_live;
+    uint32_t *q_la, *q_lb;  // ping-pong lists of live slots (logic input / output)
+    uint32_t* q_in;         // this iteration's input list (q_la or q_lb), count counts[cnt_in]
+    uint32_t* q_out;        // output list, count counts[cnt_out]
+    int cnt_in, cnt_out;
+    uint32_t* counts;  // [kQCount]
+    unsigned long long* resume_work;  // path counter of the megakernel hand-off
+};
+
 template <class R>
 struct TraceArgs {
     DevScene<R> sc;
@@ -120,6 +153,8 @@ struct TraceArgs {
     unsigned long long* stats;  // [kStCount]
     int sphere_batch;           // warp regrouping threshold for sphere steps (lanes)
     int trace_batch;            // warp regrouping threshold for BVH traversals (0 = off)
+    WfPool<R> pool;             // wavefront pool (wavefront.cuh)
+    int resume;                 // megakernel resumes the pool's live slots (q_live) instead of new ids
 };
 
 // TrainingSample (dataset.hpp:17-27): the SSWK record, 52 bytes, no padding.

@@ -1,0 +1,467 @@
+// wavefront.cuh -- the per-path loop of integrator.cuh as a wavefront over a pool of
+// path slots whose state lives in HBM/L2 as structure-of-arrays (16-byte vectors,
+// coalesced 128-bit loads and stores), with one stream-compacted queue per
+// expensive operation:
+//
+//   k_wf_logic   every slot: resolve the last traversal, collision (delta-tracking
+//                event / sphere-step request), path end + regeneration from the
+//                path-id counter, next free flight; pushes the slot onto AT MOST ONE
+//                of the queues below (block-aggregated atomics)
+//   k_wf_trace   trace queue: nearest-hit BVH traversal (medium entry / free flight)
+//   k_wf_sphere  sphere queue: the CVAE sphere step (ST); survivors push NEE
+//   k_wf_shadow  shadow queue: NEE shadow ray (light grid) + radiance update
+//
+// Every kernel runs its operation on full warps drawn from the whole pool, instead of
+// the 5-10 lanes per warp that reach the same phase of the megakernel's loop
+// (ncu: 7.3 threads/instruction, 40% of lane-iterations waiting for a sphere batch).
+// The per-path operation sequence -- and therefore every RNG draw and every result --
+// is exactly the megakernel's (integrator.cuh path_advance): paths are keyed, so the
+// iteration structure does not matter. When the pool has drained below a threshold
+// (the long-path tail) the remaining slots are handed to the register-resident
+// megakernel (trace_persistent in resume mode), which finishes them without
+// per-iteration launch costs.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "integrator.cuh"
+
+namespace sstg {
+
+namespace cg = cooperative_groups;
+
+// Slot phases (meta.w bits 11-12).
+enum : uint32_t { kPhEmpty = 0, kPhFlight = 1, kPhTrace = 2, kPhSphere = 3 };
+// meta.w packing: obj+1 (bits 0-7), channel (8-9), r_valid (10), phase (11-12),
+// cull+1 (16-23).
+SST_D uint32_t pack_meta(int obj, int c, bool r_valid, uint32_t phase, int cull) {
+    return static_cast<uint32_t>(obj + 1) | (static_cast<uint32_t>(c) << 8) |
+           (static_cast<uint32_t>(r_valid) << 10) | (phase << 11) | (static_cast<uint32_t>(cull + 1) << 16);
+}
+SST_D uint32_t meta_phase(uint32_t m) { return (m >> 11) & 3u; }
+SST_D int meta_obj(uint32_t m) { return static_cast<int>(m & 0xffu) - 1; }
+SST_D int meta_c(uint32_t m) { return static_cast<int>((m >> 8) & 3u); }
+
+template <class R>
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase) {
+    const Q4<R> xl = q.xl[s], wr = q.wr[s];
+    const uint4 m = q.meta[s];
+    p.x = mk<R>(xl.x, xl.y, xl.z);
+    p.L = xl.w;
+    p.w = mk<R>(wr.x, wr.y, wr.z);
+    p.r_here = wr.w;
+    p.rng.s = q.rng[s];
+    p.id = m.x;
+    p.seg = m.y;
+    p.skip = static_cast<int>(m.z);
+    p.obj = meta_obj(m.w);
+    p.c = static_cast<uint8_t>(meta_c(m.w));
+    p.r_valid = (m.w >> 10) & 1u;
+    *phase = meta_phase(m.w);
+    p.cull = static_cast<int>((m.w >> 16) & 0xffu) - 1;
+    p.t_pend = q.tpend[s];
+    p.pending = *phase == kPhSphere;
+    p.tpend = *phase == kPhTrace;
+    p.waited = 0;
+    p.twaited = 0;
+    p.pixel = 0;
+}
+
+template <class R>
+SST_D void store_slot(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p, uint32_t phase) {
+    q.xl[s] = Q4<R>{p.x.x, p.x.y, p.x.z, p.L};
+    q.wr[s] = Q4<R>{p.w.x, p.w.y, p.w.z, p.r_here};
+    q.rng[s] = p.rng.s;
+    q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), p.seg, static_cast<uint32_t>(p.skip),
+                           pack_meta(p.obj, p.c, p.r_valid, phase, p.cull));
+    q.tpend[s] = p.t_pend;
+}
+
+SST_D void set_phase(uint4* meta, uint32_t s, uint32_t phase) {
+    uint32_t w = meta[s].w;
+    w = (w & ~(3u << 11)) | (phase << 11);
+    meta[s].w = w;
+}
+
+// Per-thread counters flushed once per thread block (warp sums -> shared -> one
+// atomic per counter per block, spread over kStCopies copies of the stats array).
+template <int N>
+SST_D void flush_counts(unsigned long long* stats, const unsigned long long (&v)[N]) {
+    __shared__ unsigned long long sh[kStCount];
+    for (int k = threadIdx.x; k < kStCount; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const unsigned long long s = warp_sum(v[k]);
+        if ((threadIdx.x & 31u) == 0 && s) atomicAdd(&sh[k], s);
+    }
+    __syncthreads();
+    unsigned long long* dst = stats + static_cast<size_t>(blockIdx.x % kStCopies) * kStCount;
+    for (int k = threadIdx.x; k < N; k += blockDim.x)
+        if (sh[k]) atomicAdd(dst + k, sh[k]);
+}
+
+SST_D void flush_lane_stats(unsigned long long* stats, const LaneStats& st) {
+    const unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
+                                            st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow,
+                                            st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters};
+    flush_counts<kStCount>(stats, v);
+}
+
+// Path end: the radiance (and segment count) of path p.id, end statistics.
+template <class R>
+SST_D void finish_path(const TraceArgs<R>& a, const PathLocal<R>& p, int end, LaneStats& st) {
+    a.radiance[p.id] = p.L;
+    if (a.segments) a.segments[p.id] = p.seg;
+    ++st.paths;
+    st.seg += p.seg;
+    st.escaped += end == kEndEscaped;
+    st.absorbed += end == kEndAbsorbed;
+    st.capped += end == kEndCapped;
+    st.errors += end == kEndError;
+}
+
+// Block-aggregated queue append: every thread of the block calls it (uniformly);
+// threads with `want` get consecutive positions. One global atomic per block.
+SST_D void block_push(bool want, uint32_t value, uint32_t* counter, uint32_t* queue) {
+    __shared__ uint32_t wcount[32];
+    __shared__ uint32_t base;
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned nw = (blockDim.x + 31u) >> 5;
+    const unsigned b = __ballot_sync(0xffffffffu, want);
+    if (lane == 0) wcount[warp] = __popc(b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (unsigned i = 0; i < nw; ++i) {
+            const uint32_t c = wcount[i];
+            wcount[i] = tot;
+            tot += c;
+        }
+        base = tot ? atomicAdd(counter, tot) : 0u;
+    }
+    __syncthreads();
+    if (want) queue[base + wcount[warp] + __popc(b & ((1u << lane) - 1u))] = value;
+    __syncthreads();  // wcount/base are reused by the next call
+}
+
+// Warp-aggregated append from divergent code.
+SST_D void warp_push(uint32_t value, uint32_t* counter, uint32_t* queue) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    uint32_t base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(counter, g.size());
+    base = g.shfl(base, 0);
+    queue[base + g.thread_rank()] = value;
+}
+
+SST_D uint64_t fetch_path_id(unsigned long long* work, uint64_t n_paths) {
+    if (*reinterpret_cast<volatile unsigned long long*>(work) >= n_paths) return n_paths;
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(work, static_cast<unsigned long long>(g.size()));
+    base = g.shfl(base, 0);
+    return base + g.thread_rank();
+}
+
+enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3 };
+
+// ------------------------------------------------------------------ k_wf_logic
+// The non-traversal part of path_advance for one slot, run until the slot needs a
+// traversal, a sphere step or a shadow ray (at most one per iteration), or the
+// path-id supply is exhausted. Operation order per path is path_advance's.
+template <class R, bool ST, bool EX>
+SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, LaneStats& st,
+                        bool* live) {
+    const DevScene<R>& sc = a.sc;
+    PathLocal<R> p;
+    uint32_t phase = meta_phase(q.meta[s].w);
+    if (phase == kPhEmpty) {
+        const uint64_t my = fetch_path_id(a.work, a.n_paths);
+        if (my >= a.n_paths) {
+            *live = false;
+            return kEmitNone;
+        }
+        path_init<R, EX>(a, my, p);
+        phase = kPhFlight;
+    } else {
+        load_slot(q, s, p, &phase);
+    }
+    ++st.lane_iters;
+    int emit = kEmitNone;
+#pragma unroll 1
+    for (int guard = 0; guard < 8; ++guard) {
+        int end = -1;
+        bool collide = false;
+        R t_free = Real<R>::kInf;
+        if (phase == kPhFlight) {
+            // ---- flight start (path_advance phase 1)
+            bool inside = p.obj >= 0;
+            bool trace = true;
+            if (inside) {
+                const ObjK<R>& ob = sc.objs[p.obj];
+                if (!p.r_valid) {
+                    bool in_grid;
+                    const R v = sdf_raw(ob, p.x, &in_grid);
+                    p.r_here = v < R(0) ? -v : R(0);
+                    p.r_valid = true;
+                    if (leaked(ob, v, in_grid)) {
+                        recover_leak(p, ob);
+                        inside = false;
+                    }
+                }
+                if (inside) {
+                    const MediumK<R>& m = ob.med[p.c];
+                    if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
+                        const R u = p.rng.template uniform<R>();
+                        if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
+                        else t_free = -Real<R>::div_(Real<R>::log_(R(1) - u), m.sigma_t);
+                    }
+                    trace = !(t_free < p.r_here);
+                    if (trace) trace = !(t_free < skip_radius(ob, p.x));
+                }
+            }
+            if (trace) {
+                p.t_pend = t_free;
+                phase = kPhTrace;
+                emit = kEmitTrace;
+                break;
+            }
+            collide = true;  // the flight stays inside: collision without traversal
+        } else if (phase == kPhTrace) {
+            // ---- resolve (path_advance phase 2) with the traversal result
+            const uint2 hi = q.hinfo[s];
+            const bool hit = (hi.y >> 31) != 0u;
+            const R t_hit = q.thit[s];
+            if (p.obj < 0) {
+                if (!hit) {
+                    p.L += sc.bg[p.c];
+                    end = kEndEscaped;
+                } else {  // medium entry (index-matched boundary)
+                    p.x = p.x + p.w * t_hit;
+                    p.obj = static_cast<int>(hi.y & 0x7fffffffu);
+                    p.cull = -1;
+                    p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
+                    p.r_valid = false;
+                    phase = kPhFlight;
+                    continue;
+                }
+            } else if (hit) {  // leaves the medium
+                p.x = p.x + p.w * t_hit;
+                p.cull = sc.objs[p.obj].convex ? p.obj : -1;
+                p.obj = -1;
+                p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
+                phase = kPhFlight;
+                continue;
+            } else {
+                t_free = p.t_pend;
+                collide = true;
+            }
+        }
+        if (collide) {
+            // ---- collision (path_advance phases 2-3)
+            const ObjK<R>& ob = sc.objs[p.obj];
+            p.skip = -1;
+            p.x = p.x + p.w * t_free;
+            p.r_valid = false;
+            if (p.seg >= (ST ? sc.cap_st : sc.cap_pt)) {
+                p.L = R(0);  // dropped
+                end = kEndCapped;
+            } else {
+                ++p.seg;
+                bool event = true;
+                phase = kPhFlight;
+                if (ST) {
+                    bool in_grid;
+                    const R v = sdf_raw(ob, p.x, &in_grid);
+                    p.r_here = v < R(0) ? -v : R(0);
+                    p.r_valid = true;
+                    if (leaked(ob, v, in_grid)) {
+                        recover_leak(p, ob);
+                        event = false;
+                    }
+                    if (p.r_here > ob.med[p.c].r_min) {
+                        phase = kPhSphere;
+                        emit = kEmitSphere;
+                        break;
+                    }
+                }
+                if (!event) continue;
+                ++st.events;
+                const MediumK<R>& m = ob.med[p.c];
+                if (!((p.rng.next() >> 11) < m.survive_below)) {  // u < phi, bit-exact
+                    end = kEndAbsorbed;
+                } else {
+                    if (a.nee) {  // NEE with the incoming direction (no draws)
+                        q.nee_p[s] = Q4<R>{p.x.x, p.x.y, p.x.z, R(1)};
+                        q.nee_w[s] = Q4<R>{p.w.x, p.w.y, p.w.z, R(0)};
+                        emit = kEmitShadow;
+                    }
+                    const R u1 = p.rng.template uniform<R>();
+                    const R u2 = p.rng.template uniform<R>();
+                    p.w = hg_sample(m.g, p.w, u1, u2);
+                    break;  // one event per iteration
+                }
+            }
+        }
+        if (end >= 0) {
+            finish_path(a, p, end, st);
+            const uint64_t my = fetch_path_id(a.work, a.n_paths);
+            if (my >= a.n_paths) {
+                q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+                *live = false;
+                return kEmitNone;
+            }
+            path_init<R, EX>(a, my, p);
+            phase = kPhFlight;
+        }
+    }
+    store_slot(q, s, p, phase);
+    *live = true;
+    return emit;
+}
+
+// Processes the input list of live slots (all slots on the first iteration); slots
+// still live afterwards form the output list (stream compaction), so drained slots
+// cost nothing in later iterations.
+template <class R, bool ST, bool EX>
+SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
+    LaneStats st;
+    const uint32_t n_in = q.counts[q.cnt_in];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += stride) {  // block-uniform
+        const uint32_t i = base + threadIdx.x;
+        int emit = kEmitNone;
+        bool live = false;
+        const uint32_t s = i < n_in ? q.q_in[i] : 0u;
+        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, st, &live);
+        block_push(live, s, q.counts + q.cnt_out, q.q_out);
+        block_push(emit == kEmitTrace, s, q.counts + kQTrace, q.q_trace);
+        if (ST) block_push(emit == kEmitSphere, s, q.counts + kQSphere, q.q_sphere);
+        block_push(emit == kEmitShadow, s, q.counts + kQShadow, q.q_shadow);
+    }
+    flush_lane_stats(a.stats, st);
+}
+
+// Pool start: every slot empty and on the first input list.
+template <class R>
+SST_D void wf_init(const WfPool<R>& q) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < q.cap; s += gridDim.x * blockDim.x) {
+        q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+        q.q_la[s] = s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < kQCount) q.counts[threadIdx.x] = threadIdx.x == kQLiveA ? q.cap : 0u;
+}
+
+// Iteration start: queue lengths and the output live count to zero.
+template <class R>
+SST_D void wf_reset(const WfPool<R>& q) {
+    if (threadIdx.x < 3) q.counts[threadIdx.x] = 0u;
+    if (threadIdx.x == 3) q.counts[q.cnt_out] = 0u;
+}
+
+// ------------------------------------------------------------------ k_wf_trace
+template <class R>
+SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
+    const DevScene<R>& sc = a.sc;
+    uint64_t nodes = 0, tris = 0, trav = 0;
+    const uint32_t n = q.counts[kQTrace];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t s = q.q_trace[i];
+        const Q4<R> xl = q.xl[s], wr = q.wr[s];
+        const uint4 m = q.meta[s];
+        const int obj = meta_obj(m.w);
+        const int skip = static_cast<int>(m.z);
+        const int cull = static_cast<int>((m.w >> 16) & 0xffu) - 1;
+        const bool inside = obj >= 0;
+        const R t_max = inside ? q.tpend[s] : Real<R>::kInf;
+        const RayK<R> ray = make_ray(mk<R>(xl.x, xl.y, xl.z), mk<R>(wr.x, wr.y, wr.z));
+        const int want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
+        R t_hit;
+        Hit h{0, 0};
+        const bool hit = intersect_nearest(sc, ray, skip >= 0 ? sc.surf_eps : sc.t_min, t_max, skip, cull, want,
+                                           &t_hit, &h, nodes, tris);
+        ++trav;
+        q.thit[s] = t_hit;
+        q.hinfo[s] = make_uint2(h.tri, h.obj | (hit ? 0x80000000u : 0u));
+    }
+    unsigned long long v[kStCount] = {};
+    v[kStTraversals] = trav;
+    v[kStNodes] = nodes;
+    v[kStTriTests] = tris;
+    flush_counts<kStCount>(a.stats, v);
+}
+
+// ------------------------------------------------------------------ k_wf_sphere
+template <class R>
+SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
+    const DevScene<R>& sc = a.sc;
+    LaneStats st;
+    const uint32_t n = q.counts[kQSphere];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t s = q.q_sphere[i];
+        PathLocal<R> p;
+        uint32_t phase;
+        load_slot(q, s, p, &phase);
+        ++st.sphere;
+        StepOut<R> o;
+        const MediumK<R>& m = sc.objs[p.obj].med[p.c];
+        int end = -1;
+        if (!sphere_step(m, p.w, p.x, p.r_here, a.nee != 0, p.rng, o, st.dc)) {
+            p.L = R(0);
+            end = kEndError;
+        } else if (o.absorbed) {
+            end = kEndAbsorbed;
+        } else {
+            if (a.nee) {
+                q.nee_p[s] = Q4<R>{o.rep_pos.x, o.rep_pos.y, o.rep_pos.z, o.lambda};
+                q.nee_w[s] = Q4<R>{o.rep_dir.x, o.rep_dir.y, o.rep_dir.z, R(0)};
+                warp_push(s, q.counts + kQShadow, q.q_shadow);
+            }
+            p.x = o.exit_pos;
+            p.w = o.exit_dir;
+            p.r_valid = false;
+        }
+        if (end >= 0) {
+            finish_path(a, p, end, st);
+            q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+        } else {
+            store_slot(q, s, p, kPhFlight);
+        }
+    }
+    flush_lane_stats(a.stats, st);
+}
+
+// ------------------------------------------------------------------ k_wf_shadow
+template <class R>
+SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
+    const DevScene<R>& sc = a.sc;
+    uint64_t tris = 0, shadow = 0;
+    const uint32_t n = q.counts[kQShadow];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t s = q.q_shadow[i];
+        const uint32_t mw = q.meta[s].w;
+        const int obj = meta_obj(mw), c = meta_c(mw);
+        const Q4<R> np = q.nee_p[s], nw = q.nee_w[s];
+        const R add = nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w,
+                               tris);
+        q.xl[s].w += add;
+        ++shadow;
+    }
+    unsigned long long v[kStCount] = {};
+    v[kStShadow] = shadow;
+    v[kStTriTests] = tris;
+    flush_counts<kStCount>(a.stats, v);
+}
+
+// Live slots (phase != empty) -> q_live, count in counts[kQResume] (hand-off list).
+template <class R>
+SST_D void wf_compact(const WfPool<R>& q) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < q.cap; base += stride) {
+        const uint32_t s = base + threadIdx.x;
+        const bool live = s < q.cap && meta_phase(q.meta[s].w) != kPhEmpty;
+        block_push(live, s, q.counts + kQResume, q.q_live);
+    }
+}
+
+}  // namespace sstg
