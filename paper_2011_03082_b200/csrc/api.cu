@@ -165,8 +165,8 @@ struct sst_gpu_ctx {
     // Wavefront integrator (SST_WAVEFRONT=0: megakernel only). Pool slots per launch,
     // hand-off when live slots <= min(pool / 8, wf_tail), iterations per host check.
     bool wavefront = true;
-    uint32_t wf_pool = 1u << 21;
-    uint32_t wf_tail = 1u << 16;
+    uint32_t wf_pool = 1u << 23;
+    uint32_t wf_tail = 1u << 17;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
     int next_slot = 0;
@@ -650,7 +650,7 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     const size_t n = cap;
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
                             n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
-                            kQCount * 4, 8, n * 4, n * 4};
+                            kQCount * 4, 8, n * 4, n * 4, n * 4};
     size_t off[18], total = 0;
     int k = 0;
     for (size_t b : sizes) {
@@ -678,6 +678,7 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.resume_work = reinterpret_cast<unsigned long long*>(base + off[14]);
     q.q_la = reinterpret_cast<uint32_t*>(base + off[15]);
     q.q_lb = reinterpret_cast<uint32_t*>(base + off[16]);
+    q.q_free = reinterpret_cast<uint32_t*>(base + off[17]);
     return q;
 }
 
@@ -699,13 +700,14 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
     const uint32_t thresh = std::max<uint32_t>(1, std::min<uint32_t>(cap / 8, ctx->wf_tail));
     const int batch = std::max(1, ctx->wf_batch);
     uint64_t it = 0;
+    bool full = true;  // pool full (path supply left): logic walks all slots in order
     int out_last[2] = {kQLiveA, kQLiveA};
     const bool wf_trace = std::getenv("SST_WF_TRACE") != nullptr;
     const auto t_start = std::chrono::steady_clock::now();
     for (uint64_t k = 0;; ++k) {
         for (int b = 0; b < batch; ++b, ++it) {
             const bool even = (it & 1) == 0;  // live lists ping-pong: A -> B -> A ...
-            a.pool.q_in = even ? a.pool.q_la : a.pool.q_lb;
+            a.pool.q_in = full ? nullptr : (even ? a.pool.q_la : a.pool.q_lb);
             a.pool.q_out = even ? a.pool.q_lb : a.pool.q_la;
             a.pool.cnt_in = even ? kQLiveA : kQLiveB;
             a.pool.cnt_out = even ? kQLiveB : kQLiveA;
@@ -728,6 +730,7 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
                          sl.wf_host[((k - 1) & 1) * kQCount + kQSphere], sl.wf_host[((k - 1) & 1) * kQCount + kQShadow],
                          std::chrono::duration<double, std::milli>(now - t_start).count());
         }
+        if (live < cap) full = false;  // generation refills every free slot while ids remain
         if (live <= thresh) break;
     }
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, explicit_keys, stream));

@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_M
 constexpr int kWfBlock = 256;
 template <bool ST, bool EX>
 __global__ void __launch_bounds__(kWfBlock) k_wf_logic(TraceArgs<R> a) { wf_logic<R, ST, EX>(a, a.pool); }
+template <bool EX>
+__global__ void __launch_bounds__(kWfBlock) k_wf_gen(TraceArgs<R> a) { wf_gen<R, EX>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_trace(TraceArgs<R> a) { wf_trace<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock, 2) k_wf_sphere(TraceArgs<R> a) { wf_sphere<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
@@ -178,7 +180,7 @@ cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {
 
 // One wavefront iteration (a.pool.q_in/q_out set by the caller; queue counters cleared first).
 cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {
-    static unsigned g_logic[2][2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
+    static unsigned g_logic[2][2] = {}, g_gen[2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
     static uint32_t cap_seen = 0;
     if (cap_seen != a.pool.cap) {  // grids depend on the pool size only
         cap_seen = a.pool.cap;
@@ -186,6 +188,8 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
         g_logic[0][1] = wf_grid(k_wf_logic<false, true>, a.pool.cap);
         g_logic[1][0] = wf_grid(k_wf_logic<true, false>, a.pool.cap);
         g_logic[1][1] = wf_grid(k_wf_logic<true, true>, a.pool.cap);
+        g_gen[0] = wf_grid(k_wf_gen<false>, a.pool.cap);
+        g_gen[1] = wf_grid(k_wf_gen<true>, a.pool.cap);
         g_trace = wf_grid(k_wf_trace, a.pool.cap);
         g_sphere = wf_grid(k_wf_sphere, a.pool.cap);
         g_shadow = wf_grid(k_wf_shadow, a.pool.cap);
@@ -199,6 +203,8 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
         if (explicit_keys) k_wf_logic<false, true><<<gl, kWfBlock, 0, s>>>(a);
         else k_wf_logic<false, false><<<gl, kWfBlock, 0, s>>>(a);
     }
+    if (explicit_keys) k_wf_gen<true><<<g_gen[1], kWfBlock, 0, s>>>(a);
+    else k_wf_gen<false><<<g_gen[0], kWfBlock, 0, s>>>(a);
     k_wf_trace<<<g_trace, kWfBlock, 0, s>>>(a);
     if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s>>>(a);
     if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s>>>(a);

@@ -114,7 +114,14 @@ struct alignas(4 * sizeof(R)) Q4 {
     R x, y, z, w;
 };
 // counts[]: queue lengths, the two ping-pong live-slot lists, the hand-off list.
-enum : int { kQTrace = 0, kQSphere = 1, kQShadow = 2, kQLiveA = 3, kQLiveB = 4, kQResume = 5, kQCount = 8 };
+// kQFetch*: work-stealing cursors of the trace / sphere / shadow kernels.
+enum : int {
+    kQTrace = 0, kQSphere = 1, kQShadow = 2, kQLiveA = 3, kQLiveB = 4, kQResume = 5,
+    kQFetchTrace = 6, kQFetchSphere = 7, kQFetchShadow = 8,
+    kQFree = 9,     // slots whose path ended (generation input)
+    kQTicket = 10,  // last-block detection of the generation kernel
+    kQCount = 12
+};
 template <class R>
 struct WfPool {
     uint32_t cap;     // slots
@@ -129,6 +136,7 @@ struct WfPool {
     Q4<R>* nee_w;     // NEE record: direction
     uint32_t *q_trace, *q_sphere, *q_shadow, *q_live;
     uint32_t *q_la, *q_lb;  // ping-pong lists of live slots (logic input / output)
+    uint32_t* q_free;       // free slots (path ended), refilled by the generation kernel
     uint32_t* q_in;         // this iteration's input list (q_la or q_lb), count counts[cnt_in]
     uint32_t* q_out;        // output list, count counts[cnt_out]
     int cnt_in, cnt_out;

@@ -3,10 +3,12 @@
 // coalesced 128-bit loads and stores), with one stream-compacted queue per
 // expensive operation:
 //
-//   k_wf_logic   every slot: resolve the last traversal, collision (delta-tracking
-//                event / sphere-step request), path end + regeneration from the
-//                path-id counter, next free flight; pushes the slot onto AT MOST ONE
-//                of the queues below (block-aggregated atomics)
+//   k_wf_logic   every live slot: resolve the last traversal, collision (delta-
+//                tracking event / sphere-step request), path end (slot -> free queue),
+//                next free flight; pushes the slot onto AT MOST ONE of the queues
+//                below (block-aggregated atomics)
+//   k_wf_gen     free queue: new paths (camera ray + RNG key) with consecutive ids,
+//                straight onto the trace queue
 //   k_wf_trace   trace queue: nearest-hit BVH traversal (medium entry / free flight)
 //   k_wf_sphere  sphere queue: the CVAE sphere step (ST); survivors push NEE
 //   k_wf_shadow  shadow queue: NEE shadow ray (light grid) + radiance update
@@ -145,6 +147,48 @@ SST_D void block_push(bool want, uint32_t value, uint32_t* counter, uint32_t* qu
     __syncthreads();  // wcount/base are reused by the next call
 }
 
+// N block-aggregated appends in one pass (2 barriers, one global atomic per
+// non-empty queue per block): queue j receives `value` from the threads with want[j].
+template <int N>
+SST_D void block_pushn(const bool (&want)[N], uint32_t value, uint32_t* const (&counter)[N],
+                       uint32_t* const (&queue)[N]) {
+    __shared__ uint32_t wc[8][33];
+    __shared__ uint32_t qbase[8];
+    static_assert(N <= 8, "queues");
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned nw = (blockDim.x + 31u) >> 5;
+    unsigned b[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        b[j] = __ballot_sync(0xffffffffu, want[j]);
+        if (lane == 0) wc[j][warp] = __popc(b[j]);
+    }
+    __syncthreads();
+    if (threadIdx.x < N && counter[threadIdx.x]) {
+        const int j = threadIdx.x;
+        uint32_t tot = 0;
+        for (unsigned i = 0; i < nw; ++i) {
+            const uint32_t c = wc[j][i];
+            wc[j][i] = tot;
+            tot += c;
+        }
+        qbase[j] = tot ? atomicAdd(counter[j], tot) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+        if (want[j]) queue[j][qbase[j] + wc[j][warp] + __popc(b[j] & ((1u << lane) - 1u))] = value;
+    __syncthreads();
+}
+
+// Warp-granular work stealing over a queue of n items: returns the next item index
+// for this lane (>= n when the queue is exhausted for the whole warp).
+SST_D uint32_t warp_fetch(uint32_t* cursor) {
+    uint32_t base = 0;
+    if ((threadIdx.x & 31u) == 0) base = atomicAdd(cursor, 32u);
+    return __shfl_sync(0xffffffffu, base, 0) + (threadIdx.x & 31u);
+}
+
 // Warp-aggregated append from divergent code.
 SST_D void warp_push(uint32_t value, uint32_t* counter, uint32_t* queue) {
     cg::coalesced_group g = cg::coalesced_threads();
@@ -154,38 +198,21 @@ SST_D void warp_push(uint32_t value, uint32_t* counter, uint32_t* queue) {
     queue[base + g.thread_rank()] = value;
 }
 
-SST_D uint64_t fetch_path_id(unsigned long long* work, uint64_t n_paths) {
-    if (*reinterpret_cast<volatile unsigned long long*>(work) >= n_paths) return n_paths;
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned long long base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(work, static_cast<unsigned long long>(g.size()));
-    base = g.shfl(base, 0);
-    return base + g.thread_rank();
-}
-
-enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3 };
+enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3, kEmitFree = 4 };
 
 // ------------------------------------------------------------------ k_wf_logic
 // The non-traversal part of path_advance for one slot, run until the slot needs a
-// traversal, a sphere step or a shadow ray (at most one per iteration), or the
-// path-id supply is exhausted. Operation order per path is path_advance's.
+// traversal, a sphere step or a shadow ray (at most one per iteration), or its path
+// ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
 SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, LaneStats& st,
                         bool* live) {
     const DevScene<R>& sc = a.sc;
     PathLocal<R> p;
     uint32_t phase = meta_phase(q.meta[s].w);
-    if (phase == kPhEmpty) {
-        const uint64_t my = fetch_path_id(a.work, a.n_paths);
-        if (my >= a.n_paths) {
-            *live = false;
-            return kEmitNone;
-        }
-        path_init<R, EX>(a, my, p);
-        phase = kPhFlight;
-    } else {
-        load_slot(q, s, p, &phase);
-    }
+    *live = false;
+    if (phase == kPhEmpty) return kEmitNone;  // ended in k_wf_sphere (already on the free queue)
+    load_slot(q, s, p, &phase);
     ++st.lane_iters;
     int emit = kEmitNone;
 #pragma unroll 1
@@ -305,14 +332,8 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
         }
         if (end >= 0) {
             finish_path(a, p, end, st);
-            const uint64_t my = fetch_path_id(a.work, a.n_paths);
-            if (my >= a.n_paths) {
-                q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
-                *live = false;
-                return kEmitNone;
-            }
-            path_init<R, EX>(a, my, p);
-            phase = kPhFlight;
+            q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+            return kEmitFree;
         }
     }
     store_slot(q, s, p, phase);
@@ -326,36 +347,80 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
 template <class R, bool ST, bool EX>
 SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
     LaneStats st;
-    const uint32_t n_in = q.counts[q.cnt_in];
+    // q_in == null: every slot in slot order (while the pool is full: coalesced SoA
+    // accesses); otherwise the compacted list of the previous iteration (drain)
+    const uint32_t n_in = q.q_in ? q.counts[q.cnt_in] : q.cap;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += stride) {  // block-uniform
         const uint32_t i = base + threadIdx.x;
         int emit = kEmitNone;
         bool live = false;
-        const uint32_t s = i < n_in ? q.q_in[i] : 0u;
+        const uint32_t s = i < n_in ? (q.q_in ? q.q_in[i] : i) : 0u;
         if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, st, &live);
-        block_push(live, s, q.counts + q.cnt_out, q.q_out);
-        block_push(emit == kEmitTrace, s, q.counts + kQTrace, q.q_trace);
-        if (ST) block_push(emit == kEmitSphere, s, q.counts + kQSphere, q.q_sphere);
-        block_push(emit == kEmitShadow, s, q.counts + kQShadow, q.q_shadow);
+        const bool want[5] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitShadow, emit == kEmitFree};
+        uint32_t* const ctr[5] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
+                                  q.counts + kQShadow, q.counts + kQFree};
+        uint32_t* const qs[5] = {q.q_out, q.q_trace, q.q_sphere, q.q_shadow, q.q_free};
+        block_pushn<5>(want, s, ctr, qs);
     }
     flush_lane_stats(a.stats, st);
 }
 
-// Pool start: every slot empty and on the first input list.
+// ------------------------------------------------------------------ k_wf_gen
+// New paths into the free slots: entry i of the free queue gets path id work + i
+// (no per-path atomics), the camera ray is set up (path_init) and queued for its
+// first traversal. The last block to finish advances the path counter and empties
+// the free queue (slots left over once the ids run out stay empty).
+template <class R, bool EX>
+SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
+    const uint32_t n_free = q.counts[kQFree];
+    const uint64_t base = *a.work;
+    const uint64_t left = base < a.n_paths ? a.n_paths - base : 0;
+    const uint32_t n_new = static_cast<uint32_t>(left < n_free ? left : n_free);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n_new; b0 += stride) {  // block-uniform
+        const uint32_t i = b0 + threadIdx.x;
+        const bool ok = i < n_new;
+        const uint32_t s = ok ? q.q_free[i] : 0u;
+        if (ok) {
+            PathLocal<R> p;
+            path_init<R, EX>(a, base + i, p);
+            p.t_pend = Real<R>::kInf;  // outside: the first flight is the camera ray
+            store_slot(q, s, p, kPhTrace);
+        }
+        const bool want[2] = {ok, ok};
+        uint32_t* const ctr[2] = {q.counts + q.cnt_out, q.counts + kQTrace};
+        uint32_t* const qs[2] = {q.q_out, q.q_trace};
+        block_pushn<2>(want, s, ctr, qs);
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(q.counts + kQTicket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        *a.work = base + n_new;
+        q.counts[kQFree] = 0u;
+        q.counts[kQTicket] = 0u;
+    }
+}
+
+// Pool start: every slot empty and on the free queue.
 template <class R>
 SST_D void wf_init(const WfPool<R>& q) {
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < q.cap; s += gridDim.x * blockDim.x) {
         q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
-        q.q_la[s] = s;
+        q.q_free[s] = s;
     }
-    if (blockIdx.x == 0 && threadIdx.x < kQCount) q.counts[threadIdx.x] = threadIdx.x == kQLiveA ? q.cap : 0u;
+    if (blockIdx.x == 0 && threadIdx.x < kQCount) q.counts[threadIdx.x] = threadIdx.x == kQFree ? q.cap : 0u;
 }
 
 // Iteration start: queue lengths and the output live count to zero.
 template <class R>
 SST_D void wf_reset(const WfPool<R>& q) {
-    if (threadIdx.x < 3) q.counts[threadIdx.x] = 0u;
+    if (threadIdx.x < 3 || (threadIdx.x >= kQFetchTrace && threadIdx.x <= kQFetchShadow)) q.counts[threadIdx.x] = 0u;
     if (threadIdx.x == 3) q.counts[q.cnt_out] = 0u;
 }
 
@@ -365,7 +430,10 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
     const DevScene<R>& sc = a.sc;
     uint64_t nodes = 0, tris = 0, trav = 0;
     const uint32_t n = q.counts[kQTrace];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (;;) {
+        const uint32_t i = warp_fetch(q.counts + kQFetchTrace);
+        if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
+        if (i >= n) continue;
         const uint32_t s = q.q_trace[i];
         const Q4<R> xl = q.xl[s], wr = q.wr[s];
         const uint4 m = q.meta[s];
@@ -397,7 +465,10 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
     const DevScene<R>& sc = a.sc;
     LaneStats st;
     const uint32_t n = q.counts[kQSphere];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (;;) {
+        const uint32_t i = warp_fetch(q.counts + kQFetchSphere);
+        if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
+        if (i >= n) continue;
         const uint32_t s = q.q_sphere[i];
         PathLocal<R> p;
         uint32_t phase;
@@ -424,6 +495,7 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
         if (end >= 0) {
             finish_path(a, p, end, st);
             q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+            warp_push(s, q.counts + kQFree, q.q_free);
         } else {
             store_slot(q, s, p, kPhFlight);
         }
@@ -437,7 +509,10 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
     const DevScene<R>& sc = a.sc;
     uint64_t tris = 0, shadow = 0;
     const uint32_t n = q.counts[kQShadow];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (;;) {
+        const uint32_t i = warp_fetch(q.counts + kQFetchShadow);
+        if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
+        if (i >= n) continue;
         const uint32_t s = q.q_shadow[i];
         const uint32_t mw = q.meta[s].w;
         const int obj = meta_obj(mw), c = meta_c(mw);
