@@ -1,0 +1,140 @@
+"""The wavefront integrator (csrc/wavefront.cuh) against the register-resident
+megakernel (csrc/integrator.cuh) it restructures.
+
+Both run the same per-path operation sequence on keyed RNG streams, so every path
+must come out identical -- radiance, segment count and every result counter --
+whatever the pool size, the hand-off threshold or the iteration batching:
+  FP64: bit-identical radiance and segments (the parity mode, -fmad=false).
+  FP32: bit-identical on >= 99.9% of paths (the two kernels are separate
+        compilations; FMA contraction may differ in a few expressions) and radiance
+        within 1e-5 relative elsewhere.
+Small pools (SST_WF_POOL) force many slot recycles, the drain and the megakernel
+hand-off (SST_WF_TAIL) on small workloads.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ENV_KEYS = ("SST_WAVEFRONT", "SST_WF_POOL", "SST_WF_TAIL", "SST_WF_BATCH")
+
+
+def _renderer(models_dir, precision, **env):
+    from paper_2011_03082_b200 import Renderer
+    saved = {k: os.environ.get(k) for k in ENV_KEYS}
+    try:
+        for k in ENV_KEYS:
+            os.environ.pop(k, None)
+        os.environ.update({k: str(v) for k, v in env.items()})
+        r = Renderer(0, precision)  # the knobs are read when the context is created
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    r.load_models_dir(models_dir)
+    return r
+
+
+def _keys(n_pix, n, seed=3):
+    rng = np.random.default_rng(seed)
+    return (rng.integers(0, n_pix, n).astype(np.uint32), rng.integers(0, 5000, n).astype(np.uint32),
+            rng.integers(0, 3, n).astype(np.uint8))
+
+
+# Result counters. The work counters (traversals, node visits, triangle tests) may
+# differ: a slot handed to the megakernel with its traversal done re-runs it there.
+STAT_FIELDS = ("paths", "segments", "sphere_steps", "pt_events", "decodes_length", "decodes_path",
+               "decodes_event", "absorbed", "escaped", "capped", "errors", "shadow_rays")
+
+
+@pytest.fixture(scope="module")
+def scenes():
+    from paper_2011_03082_b200 import make_icosphere
+    from paper_2011_03082_b200.scene import c1_scene, c5_scene
+    mesh = make_icosphere(3, 1.0)
+    return {"c1": c1_scene(mesh, 64, 64), "c5": c5_scene(mesh, 192, 108)}
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("scene_name", ["c1", "c5"])
+def test_wavefront_paths_identical_to_megakernel(models_dir, scenes, precision, scene_name):
+    from paper_2011_03082_b200 import abi
+    scene = scenes[scene_name]
+    n = 40000 if precision == "f64" else 200000
+    pix, smp, ch = _keys(scene.n_pixels, n)
+    mk = _renderer(models_dir, precision, SST_WAVEFRONT=0)
+    configs = [dict(SST_WAVEFRONT=1),  # default pool: drain + hand-off
+               dict(SST_WAVEFRONT=1, SST_WF_POOL=2048, SST_WF_TAIL=64, SST_WF_BATCH=1)]  # many recycles
+    wfs = [_renderer(models_dir, precision, **c) for c in configs]
+    try:
+        for r in [mk] + wfs:
+            r.upload_scene(scene)
+        for integ in (0, 1):
+            for nee in (0, 1):
+                s0 = abi.PathStats()
+                r0, g0 = mk.trace_paths(integ, nee, 7, pix, smp, ch, stats=s0)
+                for cfg, wf in zip(configs, wfs):
+                    s1 = abi.PathStats()
+                    r1, g1 = wf.trace_paths(integ, nee, 7, pix, smp, ch, stats=s1)
+                    tag = (scene_name, precision, integ, nee, cfg)
+                    if precision == "f64":
+                        assert (g0 == g1).all(), tag
+                        assert (r0 == r1).all(), tag
+                        for f in STAT_FIELDS:
+                            assert getattr(s0, f) == getattr(s1, f), (tag, f)
+                    else:
+                        same = (g0 == g1) & (r0 == r1)
+                        assert same.mean() >= 0.999, (tag, same.mean())
+                        close = np.abs(r0 - r1) <= 1e-7 + 1e-5 * np.abs(r0)
+                        assert close.mean() >= 0.999, tag
+                    assert s1.paths == n and s1.errors == 0, tag
+    finally:
+        for r in [mk] + wfs:
+            r.close()
+
+
+def test_wavefront_film_identical_to_megakernel(models_dir, scenes):
+    """Render path (device film sums, several chunks): identical FP64 films."""
+    from paper_2011_03082_b200 import PT, ST, abi
+    scene = scenes["c5"]
+    mk = _renderer(models_dir, "f64", SST_WAVEFRONT=0)
+    wf = _renderer(models_dir, "f64", SST_WAVEFRONT=1, SST_WF_POOL=8192, SST_WF_TAIL=256)
+    try:
+        for r in (mk, wf):
+            r.upload_scene(scene)
+        for integ in (ST, PT):
+            f0, f1 = abi.PathStats(), abi.PathStats()
+            img0, _ = mk.render_film(integ, 64, 5, True, 0, 3, stats=f0)
+            img1, _ = wf.render_film(integ, 64, 5, True, 0, 3, stats=f1)
+            assert (img0.sum == img1.sum).all() and (img0.sumsq == img1.sumsq).all(), integ
+            for f in STAT_FIELDS:
+                assert getattr(f0, f) == getattr(f1, f), (integ, f)
+    finally:
+        mk.close()
+        wf.close()
+
+
+def test_wavefront_async_slabs_match_one_call(models_dir, scenes):
+    """Consecutive asynchronous device-pointer slabs (the bench's pattern) sum to the
+    same film as one synchronous call over the same samples."""
+    import torch
+    from paper_2011_03082_b200 import ST
+    scene = scenes["c1"]
+    r = _renderer(models_dir, "f32", SST_WAVEFRONT=1, SST_WF_POOL=65536, SST_WF_TAIL=1024)
+    try:
+        r.upload_scene(scene)
+        n = 3 * scene.n_pixels
+        fs = torch.zeros(n, dtype=torch.float64, device="cuda")
+        fq = torch.zeros(n, dtype=torch.float64, device="cuda")
+        for k in range(4):
+            r.render_device(ST, 64, 2 * k, 2 * k + 2, 9, True, fs.data_ptr(), fq.data_ptr(), asynchronous=True)
+        r.read_stats()
+        one, _ = r.render_film(ST, 64, 9, True, 0, 8)
+        assert np.allclose(fs.cpu().numpy(), one.sum, rtol=1e-12, atol=1e-12)
+        assert np.allclose(fq.cpu().numpy(), one.sumsq, rtol=1e-12, atol=1e-12)
+    finally:
+        r.close()
