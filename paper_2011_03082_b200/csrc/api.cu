@@ -358,6 +358,7 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     CK(cudaMemcpyAsync(objs.p, ok.data(), ok.size() * sizeof(ObjK<R>), cudaMemcpyHostToDevice, ctx->stream));
     sc.nodes = nodes.p;
     sc.tris = tris.p;
+    sc.bvh_depth = ctx->scene_cache.bvh.max_depth;
     sc.objs = objs.as<ObjK<R>>();
     sc.n_objects = static_cast<uint32_t>(ok.size());
     // Camera basis in double (DESIGN.md camera model), then rounded.
@@ -580,6 +581,8 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     if (!cached) {
         ctx->scene_cache = sst_gpu_ctx::SceneCache{};
         ctx->scene_cache.bvh = build_bvh(tv, tobj);
+        if (ctx->scene_cache.bvh.max_depth + 1 > static_cast<uint32_t>(kStack))
+            throw InvalidArgument("BVH deeper than the traversal stack (" + std::to_string(kStack) + ")");
         build_light_grid(ctx, d, tv, ctx->scene_cache.bvh);
         ctx->scene_cache.fp = sfp;
     } else {  // copy the cached light grid to the device (inputs travel every upload)

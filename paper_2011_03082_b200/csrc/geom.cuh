@@ -68,6 +68,7 @@ SST_D R skip_radius(const ObjK<R>& o, V3<R> p) {
 template <class R>
 struct RayK {
     V3<R> o, d, inv;
+    V3<R> oi;  // FP32: o * inv, so each slab plane is one FFMA (t = lo * inv - oi)
 };
 
 template <class R>
@@ -77,24 +78,46 @@ SST_D RayK<R> make_ray(V3<R> o, V3<R> d) {
     r.d = d;
     if (Real<R>::kIsDouble) {  // bvh.cpp:91 computes 1/dir per axis (inf allowed)
         r.inv = mk<R>(R(1) / d.x, R(1) / d.y, R(1) / d.z);
+        r.oi = r.o;
     } else {
         const float e = 1e-20f;
         r.inv = mk<R>(__fdividef(1.0f, fabsf(d.x) > e ? d.x : copysignf(e, d.x)),
                       __fdividef(1.0f, fabsf(d.y) > e ? d.y : copysignf(e, d.y)),
                       __fdividef(1.0f, fabsf(d.z) > e ? d.z : copysignf(e, d.z)));
+        r.oi = mk<R>(o.x * r.inv.x, o.y * r.inv.y, o.z * r.inv.z);
     }
     return r;
 }
+
+// Traversal stacks: registers/local memory (megakernel), or shared memory with a
+// per-thread stride (wavefront trace kernel: no local-memory traffic through L2).
+template <class R, int N>
+struct LocalStack {
+    int n[N];
+    R t[N];
+    SST_D int& node(int i) { return n[i]; }
+    SST_D R& dist(int i) { return t[i]; }
+};
+template <class R>
+struct SharedStack {
+    int* n;
+    R* t;
+    int stride;
+    SST_D int& node(int i) { return n[i * stride]; }
+    SST_D R& dist(int i) { return t[i * stride]; }
+};
 
 // slab_hit (bvh.cpp:88-101) returning the entry distance.
 template <class R>
 SST_D bool slab(const RayK<R>& r, R lox, R hix, R loy, R hiy, R loz, R hiz, R t_min, R t_max,
                 R* t_enter) {
     R t0 = t_min, t1 = t_max;
-    if constexpr (!Real<R>::kIsDouble) {  // FP32: branch-free min/max (inv is finite, no NaN)
-        const R nx = (lox - r.o.x) * r.inv.x, fx = (hix - r.o.x) * r.inv.x;
-        const R ny = (loy - r.o.y) * r.inv.y, fy = (hiy - r.o.y) * r.inv.y;
-        const R nz = (loz - r.o.z) * r.inv.z, fz = (hiz - r.o.z) * r.inv.z;
+    if constexpr (!Real<R>::kIsDouble) {  // FP32: branch-free min/max (inv is finite, no NaN);
+        // one FFMA per plane -- its rounding (<= 1 ulp of t) is covered by the outward
+        // box padding of the FP32 nodes (host.cpp down/up, ~2e-7 relative)
+        const R nx = fmaf(lox, r.inv.x, -r.oi.x), fx = fmaf(hix, r.inv.x, -r.oi.x);
+        const R ny = fmaf(loy, r.inv.y, -r.oi.y), fy = fmaf(hiy, r.inv.y, -r.oi.y);
+        const R nz = fmaf(loz, r.inv.z, -r.oi.z), fz = fmaf(hiz, r.inv.z, -r.oi.z);
         t0 = fmaxf(fmaxf(t0, fminf(nx, fx)), fmaxf(fminf(ny, fy), fminf(nz, fz)));
         t1 = fminf(fminf(t1, fmaxf(nx, fx)), fminf(fmaxf(ny, fy), fmaxf(nz, fz)));
         *t_enter = t0;
@@ -189,7 +212,6 @@ SST_D void load_tri<double>(const void* tris, uint32_t i, V3<double>& v0, V3<dou
     id = t->id;
 }
 
-constexpr int kStack = 48;
 
 // Nearest hit with t in (t_min, t_max), ignoring triangle `skip` (FP32
 // self-intersection guard for rays leaving a surface; -1 = none).
@@ -204,12 +226,10 @@ constexpr int kDone = 0x7fffffff;
 // 0 any. FP32 rays use it (a ray outside every medium can only enter, a flight
 // inside can only leave): with outward-wound meshes this rejects the spurious
 // re-hits of neighbouring triangles that FP32 rounding produces at surfaces.
-template <class R>
-SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
-                             int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
-                             uint64_t& n_tris) {
-    int stack_n[kStack];
-    R stack_t[kStack];
+template <class R, class Stack>
+SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
+                               int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
+                               uint64_t& n_tris, Stack& stk) {
     int sp = 0;
     int node = 0;   // interior (>= 0), leaf (< 0) or kDone
     int leaf = 0;   // postponed leaf (< 0) or 0 = none
@@ -218,7 +238,7 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
     auto pop = [&]() -> int {
         while (sp > 0) {
             --sp;
-            if (stack_t[sp] <= t_best) return stack_n[sp];
+            if (stk.dist(sp) <= t_best) return stk.node(sp);
         }
         return kDone;
     };
@@ -236,8 +256,8 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
                             (cull_obj < 0 || o1 != cull_obj);
             if (h0 && h1) {
                 const bool first0 = t0 <= t1;
-                stack_n[sp] = first0 ? c1 : c0;
-                stack_t[sp] = first0 ? t1 : t0;
+                stk.node(sp) = first0 ? c1 : c0;
+                stk.dist(sp) = first0 ? t1 : t0;
                 ++sp;
                 node = first0 ? c0 : c1;
             } else if (h0) {
@@ -281,6 +301,14 @@ SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min,
     }
     *t_hit = t_best;
     return found;
+}
+
+template <class R>
+SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
+                             int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
+                             uint64_t& n_tris) {
+    LocalStack<R, kStack> stk;
+    return intersect_nearest_s(sc, ray, t_min, t_max, skip, cull_obj, want_sign, t_hit, hit, n_nodes, n_tris, stk);
 }
 
 // Optical depth along [0, t_max] from a point inside a medium (order-free signed sum;

@@ -427,6 +427,14 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
     }
     FlatBvh out;
     out.n_nodes = static_cast<uint32_t>(bld.nodes.size());
+    {  // deepest root-to-leaf path (traversal stacks hold at most one entry per level)
+        std::vector<uint32_t> depth(out.n_nodes, 1);
+        for (uint32_t i = 0; i < out.n_nodes; ++i) {  // parents precede children
+            for (int32_t c : {bld.nodes[i].c0, bld.nodes[i].c1})
+                if (c >= 0) depth[c] = depth[i] + 1;
+            out.max_depth = std::max(out.max_depth, depth[i]);
+        }
+    }
     out.n_tris = n;
     out.order = bld.order;
     // Object id of every child subtree (-1 when mixed): lets a traversal cull the

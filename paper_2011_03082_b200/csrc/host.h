@@ -59,6 +59,7 @@ struct FlatBvh {
     std::vector<uint8_t> nodes_f32, tris_f32;  // NodeF[], TriF[]
     std::vector<uint8_t> nodes_f64, tris_f64;  // NodeD[], TriD[]
     uint32_t n_nodes = 0, n_tris = 0;
+    uint32_t max_depth = 0;       // interior levels on the deepest root-leaf path (stack bound)
     std::vector<uint32_t> order;  // leaf position -> input triangle index
 };
 // tri_vertices: [n][3] corners; tri_obj: object id per triangle.

@@ -163,9 +163,9 @@ static cudaError_t launch_trace_t(const TraceArgs<R>& a, cudaStream_t s) {
 }
 
 template <class K>
-static unsigned wf_grid(K kernel, uint32_t items) {
+static unsigned wf_grid(K kernel, uint32_t items, size_t smem = 0) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWfBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWfBlock, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t g = static_cast<uint64_t>(sm_count()) * per_sm;
     const uint64_t need = (static_cast<uint64_t>(items) + kWfBlock - 1) / kWfBlock;
@@ -181,16 +181,19 @@ cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {
 // One wavefront iteration (a.pool.q_in/q_out set by the caller; queue counters cleared first).
 cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {
     static unsigned g_logic[2][2] = {}, g_gen[2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
-    static uint32_t cap_seen = 0;
-    if (cap_seen != a.pool.cap) {  // grids depend on the pool size only
+    static uint32_t cap_seen = 0, depth_seen = 0;
+    const size_t trace_smem = wf_trace_smem<R>(a.sc.bvh_depth, kWfBlock);
+    if (cap_seen != a.pool.cap || depth_seen != a.sc.bvh_depth) {  // grids depend on pool size and BVH depth
         cap_seen = a.pool.cap;
+        depth_seen = a.sc.bvh_depth;
+        cudaFuncSetAttribute(k_wf_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trace_smem));
         g_logic[0][0] = wf_grid(k_wf_logic<false, false>, a.pool.cap);
         g_logic[0][1] = wf_grid(k_wf_logic<false, true>, a.pool.cap);
         g_logic[1][0] = wf_grid(k_wf_logic<true, false>, a.pool.cap);
         g_logic[1][1] = wf_grid(k_wf_logic<true, true>, a.pool.cap);
         g_gen[0] = wf_grid(k_wf_gen<false>, a.pool.cap);
         g_gen[1] = wf_grid(k_wf_gen<true>, a.pool.cap);
-        g_trace = wf_grid(k_wf_trace, a.pool.cap);
+        g_trace = wf_grid(k_wf_trace, a.pool.cap, trace_smem);
         g_sphere = wf_grid(k_wf_sphere, a.pool.cap);
         g_shadow = wf_grid(k_wf_shadow, a.pool.cap);
     }
@@ -205,7 +208,7 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
     }
     if (explicit_keys) k_wf_gen<true><<<g_gen[1], kWfBlock, 0, s>>>(a);
     else k_wf_gen<false><<<g_gen[0], kWfBlock, 0, s>>>(a);
-    k_wf_trace<<<g_trace, kWfBlock, 0, s>>>(a);
+    k_wf_trace<<<g_trace, kWfBlock, trace_smem, s>>>(a);
     if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s>>>(a);
     if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s>>>(a);
     return cudaGetLastError();

@@ -86,7 +86,11 @@ struct DevScene {
     const uint32_t* grid_off;
     const uint32_t* grid_tri;
     uint32_t grid_res;
+    uint32_t bvh_depth;  // FlatBvh::max_depth (traversal stack bound)
 };
+
+// Traversal stack capacity (entries); scenes whose BVH is deeper are rejected at upload.
+constexpr int kStack = 48;
 
 struct Hit {
     uint32_t tri, obj;

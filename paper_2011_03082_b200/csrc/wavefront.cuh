@@ -425,10 +425,23 @@ SST_D void wf_reset(const WfPool<R>& q) {
 }
 
 // ------------------------------------------------------------------ k_wf_trace
+// Traversal stacks live in dynamic shared memory ([entry][thread], conflict-free),
+// sc.bvh_depth + 1 entries per thread (wf_trace_smem bytes per block).
+template <class R>
+SST_HD size_t wf_trace_smem(uint32_t bvh_depth, int block) {
+    return static_cast<size_t>(bvh_depth + 1) * block * (sizeof(int) + sizeof(R));
+}
+
 template <class R>
 SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
     const DevScene<R>& sc = a.sc;
     uint64_t nodes = 0, tris = 0, trav = 0;
+    extern __shared__ __align__(16) unsigned char wf_smem[];
+    const uint32_t entries = sc.bvh_depth + 1;
+    SharedStack<R> stk{reinterpret_cast<int*>(wf_smem) + threadIdx.x,
+                       reinterpret_cast<R*>(wf_smem + static_cast<size_t>(entries) * blockDim.x * sizeof(int)) +
+                           threadIdx.x,
+                       static_cast<int>(blockDim.x)};
     const uint32_t n = q.counts[kQTrace];
     for (;;) {
         const uint32_t i = warp_fetch(q.counts + kQFetchTrace);
@@ -446,8 +459,8 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
         const int want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
         R t_hit;
         Hit h{0, 0};
-        const bool hit = intersect_nearest(sc, ray, skip >= 0 ? sc.surf_eps : sc.t_min, t_max, skip, cull, want,
-                                           &t_hit, &h, nodes, tris);
+        const bool hit = intersect_nearest_s(sc, ray, skip >= 0 ? sc.surf_eps : sc.t_min, t_max, skip, cull, want,
+                                             &t_hit, &h, nodes, tris, stk);
         ++trav;
         q.thit[s] = t_hit;
         q.hinfo[s] = make_uint2(h.tri, h.obj | (hit ? 0x80000000u : 0u));
