@@ -19,7 +19,6 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
-import math
 import os
 import sys
 import threading
@@ -44,6 +43,19 @@ DATA = ("synthetic: procedural icosphere meshes, GPU-built conservative SDFs (re
 def mlp_flops(dl, dp, de):
     """Algorithmic FLOPs of the decoders: 2 x MACs x decodes."""
     return 2.0 * (112 * dl + 480 * dp + 640 * de)
+
+
+# Algorithmic per-unit work of each wavefront kernel (DESIGN.md §5, counted from the
+# device counters of the measured slab):
+#   wf_logic  HBM: per slot visit the path state it must read (x,L 16 + w,r 16 + rng 8 +
+#             meta 16 + flight 4 + hit 12 = 72 B) and write back (60 B) + 2 queue
+#             entries (8 B); per delta-tracking event a 32 B NEE record.
+#   wf_trace  FP32: per interior node 2 slab tests = 12 FFMA + 12 min/max = 36 FLOP;
+#             per Moller-Trumbore test 51 FLOP (2 cross, 4 dot, rcp, 3 mul, 3 sub).
+#   wf_shadow FP32: 51 FLOP per light-grid triangle test.
+#   wf_sphere FP32: decoder MLP FLOPs 2*(112 nL + 480 nP + 640 nE).
+NODE_FLOP, TRI_FLOP = 36.0, 51.0
+LOGIC_BYTES_PER_SLOT, NEE_RECORD_BYTES = 140.0, 32.0
 
 
 class ClockSampler:
@@ -213,7 +225,7 @@ def bench_ours(args, world, rank, local):
     n_pix = W_FRAME * H_FRAME
     S = args.spp_per_step
     total_steps = args.warmup + args.steps
-    if total_steps * world * S > FRAME_SPP:
+    if (total_steps + 1) * world * S > FRAME_SPP:
         raise SystemExit("spp budget exceeds the 5000-spp frame")
     # FFMA roofline denominator (measured once, before the timed region)
     peak_lib = C.CDLL(os.path.join(ROOT, "paper_2011_03082_b200", "libsst_peak.so"))
@@ -279,10 +291,40 @@ def bench_ours(args, world, rank, local):
     achieved = flops / (dev_ms / 1e3) / 1e12
     traffic = load_traffic()
     hbm_bytes = paths_all * 8.0 + args.steps * world * 3 * n_pix * 32.0
-    per_sample = 3 * n_pix
-    target = min(1 << 24, max(per_sample * S // 8, 1 << 20))
-    chunk = max(1, target // per_sample)
-    launches_per_step = 2 * math.ceil(S / min(chunk, S))
+
+    # ---- per-kernel roofline: one more slab with every launch bracketed by CUDA events
+    # on its own stream (synchronous per iteration, so outside the timed region)
+    hbm_peak = 6551.7
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        pass
+    r.kernel_timing(True)
+    kst = abi.PathStats()
+    s0k = (args.warmup + args.steps) * world * S + rank * S
+    r.render_device(sb.ST, FRAME_SPP, s0k, s0k + S, 1, True, fsum.data_ptr(), fsq.data_ptr(), stats=kst)
+    kt = r.kernel_timing(False)
+    tri_trace = kst.triangle_tests - kst.shadow_triangle_tests
+    kdef = {
+        "wf_logic": ("hbm", (LOGIC_BYTES_PER_SLOT * kst.wavefront_slot_visits + NEE_RECORD_BYTES * kst.pt_events) / 1e9,
+                     hbm_peak, "GB/s"),
+        "wf_trace": ("fp32", (NODE_FLOP * kst.node_visits + TRI_FLOP * tri_trace) / 1e12, fp32_peak, "TFLOP/s"),
+        "wf_shadow": ("fp32", TRI_FLOP * kst.shadow_triangle_tests / 1e12, fp32_peak, "TFLOP/s"),
+        "wf_sphere": ("fp32", mlp_flops(kst.decodes_length, kst.decodes_path, kst.decodes_event) / 1e12,
+                      fp32_peak, "TFLOP/s"),
+    }
+    tot_ms = sum(v[0] for v in kt.values())
+    kernels = {}
+    for k, (ms_k, n_k) in kt.items():
+        if n_k == 0:
+            continue
+        e = {"ms": ms_k, "launches": n_k, "avg_us": 1e3 * ms_k / n_k, "share": ms_k / tot_ms if tot_ms else None}
+        if k in kdef and ms_k > 0:
+            bound, work, peak, unit = kdef[k]
+            ach = work / (ms_k / 1e3)
+            e.update({"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak})
+        kernels[k] = e
+    dominant = max((k for k in kernels if k in kdef), key=lambda k: kernels[k]["ms"], default=None)
 
     # ---- e2e: the public host-buffer API per step (scene upload + render + film D2H)
     e2e = None
@@ -389,20 +431,30 @@ def bench_ours(args, world, rank, local):
                 "paths_per_s": paths_all / (ms / 1e3),
             },
             "roofline": {
-                "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak if fp32_peak > 0 else None,
-                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                "kernel": "k_trace<ST> persistent megakernel",
-                "achieved_def": "decoder MLP FLOPs 2*(112 nL + 480 nP + 640 nE) from device decode counters / "
-                                "CUDA-event time of the render launches on the context stream",
-                "peak_source": "measured FFMA throughput (csrc/peak.cu) on this GPU; MEASURED_PEAKS.json has no FP32 figure",
-                "hbm": {"algorithmic_bytes_per_s": hbm_bytes / (ms / 1e3),
-                        "frac_of_measured": hbm_bytes / (ms / 1e3) / 6551.7e9,
-                        "def": "per path 4 B radiance write + 4 B film read; film 2x8 B RMW per pixel-channel per slab"},
+                "bound": kernels[dominant]["bound"] if dominant else None,
+                "achieved": kernels[dominant]["achieved"] if dominant else None,
+                "peak": kernels[dominant]["peak"] if dominant else None,
+                "unit": kernels[dominant]["unit"] if dominant else None,
+                "frac": kernels[dominant]["frac"] if dominant else None,
+                "traffic": (traffic or {}).get("kernels", {}).get(dominant, {}).get("dram_bytes_per_launch"),
+                "kernel": f"k_{dominant} (wavefront)" if dominant else None,
+                "share_of_kernel_time": kernels[dominant]["share"] if dominant else None,
+                "achieved_def": "algorithmic work of the measured slab (device counters; bench.py NODE_FLOP/TRI_FLOP/"
+                                "LOGIC_BYTES_PER_SLOT) / summed CUDA-event duration of that kernel's launches on "
+                                "their stream (one extra slab after the timed region)",
+                "peak_source": f"HBM: MEASURED_PEAKS.json hbm_gbs; FP32: measured FFMA throughput (csrc/peak.cu) "
+                               f"{fp32_peak:.1f} TFLOP/s on this GPU (MEASURED_PEAKS.json has no FP32 figure)",
+                "kernels": kernels,
+                "decoder_flops": {"achieved": achieved, "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
+                                  "def": "decoder MLP FLOPs only / whole render device time (SURVEY §8d)"},
+                "hbm_film": {"algorithmic_bytes_per_s": hbm_bytes / (ms / 1e3),
+                             "frac_of_measured": hbm_bytes / (ms / 1e3) / (hbm_peak * 1e9),
+                             "def": "per path 4 B radiance write + 4 B film read; film 2x8 B RMW per pixel-channel per slab"},
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": sum(n for _, n in kt.values()) * args.steps,
+            "gpu_launches_def": "kernel launches of one slab (counted by the library's per-kernel timing pass) x steps",
             "extra": extra,
             "clocks": clocks.summary(),
         }

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SST_GPU_ABI_VERSION 1
+#define SST_GPU_ABI_VERSION 2
 
 enum {
     SST_OK = 0,
@@ -229,6 +229,9 @@ typedef struct {
     /* work counters: nearest-hit traversals, BVH interior nodes visited, triangle
      * tests (nearest + shadow), live-lane loop iterations, warp loop iterations */
     uint64_t traversals, node_visits, triangle_tests, lane_iterations, warp_iterations;
+    /* triangle tests of NEE shadow rays (part of triangle_tests); path-slot visits of
+     * the wavefront logic pass */
+    uint64_t shadow_triangle_tests, wavefront_slot_visits;
     double device_ms;        /* kernel time of the render call */
 } sst_path_stats;
 
@@ -250,6 +253,19 @@ int sst_gpu_render(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total
 /* Waits for all enqueued work, adds the counters accumulated since the last read
  * (and their device time) into *stats and resets them. */
 int sst_gpu_read_stats(sst_gpu_ctx* ctx, sst_path_stats* stats);
+
+/* Per-kernel device time (measurement aid for the roofline): with enable = 1 the
+ * render / trace calls bracket every kernel launch with CUDA events on its own
+ * stream and synchronise after each wavefront iteration (slower; for measurement
+ * passes only); ms[k] / launches[k] accumulate per kernel kind k (SST_KT_*).
+ * enable = 1 resets the accumulators, 0 stops; both first copy the current values
+ * (after synchronising) into ms / launches when those are non-NULL. */
+enum {
+    SST_KT_WF_LOGIC = 0, SST_KT_WF_GEN = 1, SST_KT_WF_TRACE = 2, SST_KT_WF_SPHERE = 3,
+    SST_KT_WF_SHADOW = 4, SST_KT_WF_RESET = 5, SST_KT_WF_TAIL = 6, SST_KT_MEGAKERNEL = 7,
+    SST_KT_FILM = 8, SST_KT_COUNT = 9
+};
+int sst_gpu_kernel_timing(sst_gpu_ctx* ctx, int enable, double* ms, uint64_t* launches);
 
 /* Per-path parity entry: traces n explicit (pixel, sample, channel) paths and
  * returns their radiance and segment counts (host pointers). */

@@ -89,7 +89,7 @@ class PathStats(C.Structure):
                 ("absorbed", U64), ("escaped", U64), ("capped", U64), ("errors", U64),
                 ("shadow_rays", U64), ("traversals", U64), ("node_visits", U64),
                 ("triangle_tests", U64), ("lane_iterations", U64), ("warp_iterations", U64),
-                ("device_ms", D)]
+                ("shadow_triangle_tests", U64), ("wavefront_slot_visits", U64), ("device_ms", D)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -139,7 +139,7 @@ EXPORTED = [
     "sst_gpu_set_precision", "sst_gpu_get_device", "sst_gpu_stream", "sst_gpu_synchronize",
     "sst_gpu_upload_models", "sst_gpu_load_models_dir", "sst_rng_init",
     "sst_gpu_sphere_step_batch", "sst_gpu_upload_scene", "sst_gpu_scene_info", "sst_gpu_get_sdf", "sst_gpu_render",
-    "sst_gpu_trace_paths", "sst_gpu_read_stats", "sst_gpu_generate_dataset",
+    "sst_gpu_trace_paths", "sst_gpu_read_stats", "sst_gpu_kernel_timing", "sst_gpu_generate_dataset",
     "sst_train_config_default", "sst_gpu_train_model", "sst_gpu_train_models",
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
@@ -184,6 +184,7 @@ def _declare(L):
     L.sst_gpu_scene_info.argtypes = [P, P, P, P]
     L.sst_gpu_render.argtypes = [P, I, I, U32, U32, U32, U64, P, P, I, C.POINTER(PathStats)]
     L.sst_gpu_read_stats.argtypes = [P, C.POINTER(PathStats)]
+    L.sst_gpu_kernel_timing.argtypes = [P, I, P, P]
     L.sst_gpu_generate_dataset.argtypes = [P, U64, D, D, D, D, I, D, D, U64, U64, P, I,
                                            C.POINTER(DatasetStats)]
     L.sst_train_config_default.argtypes = [P]

@@ -243,6 +243,18 @@ class Renderer:
                                            C.c_void_p(sumsq_ptr), abi.SST_PTR_DEVICE, sp))
         return stats
 
+    KERNEL_KINDS = ("wf_logic", "wf_gen", "wf_trace", "wf_sphere", "wf_shadow", "wf_reset", "wf_tail",
+                    "megakernel", "film")
+
+    def kernel_timing(self, enable: bool):
+        """Per-kernel device time (sst_gpu_kernel_timing): returns {kind: (ms, launches)}
+        accumulated since the last enable, then enables (and resets) or disables timing."""
+        n = len(self.KERNEL_KINDS)
+        ms = np.zeros(n, np.float64)
+        cnt = np.zeros(n, np.uint64)
+        abi.check(abi.lib().sst_gpu_kernel_timing(self.h, int(bool(enable)), _p(ms), _p(cnt)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.KERNEL_KINDS)}
+
     def read_stats(self, stats=None):
         """Waits for enqueued work and returns the counters accumulated since the last read."""
         stats = stats if stats is not None else abi.PathStats()

@@ -162,13 +162,20 @@ struct sst_gpu_ctx {
         uint32_t* wf_host = nullptr;  // [2][kQCount]
         cudaEvent_t wf_ev[2] = {nullptr, nullptr};
     } slots[kSlots];
-    // Wavefront integrator (SST_WAVEFRONT=0: megakernel only). Pool slots per launch,
+    // Wavefront integrator: SST_WAVEFRONT=0 megakernel only, 1 (default) wavefront for
+    // the sphere tracer, 2 also for the delta-tracking path tracer (whose events are
+    // cheap and whose long paths favour the register-resident megakernel). Pool slots per launch,
     // hand-off when live slots <= min(pool / 8, wf_tail), iterations per host check.
-    bool wavefront = true;
+    int wavefront = 1;
     uint32_t wf_pool = 1u << 23;
     uint32_t wf_tail = 1u << 17;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
+    // per-kernel device timing (sst_gpu_kernel_timing)
+    bool ktime = false;
+    double kt_ms[SST_KT_COUNT] = {};
+    uint64_t kt_n[SST_KT_COUNT] = {};
+    cudaEvent_t kt_ev[8] = {};
     int next_slot = 0;
     cudaEvent_t ev_start = nullptr, last_film = nullptr;
     bool timing_open = false;
@@ -647,6 +654,26 @@ const DevScene<R>& scene_of(const sst_gpu_ctx* ctx) {
 
 constexpr uint64_t kChunkPaths = 1ull << 24;  // radiance scratch per launch
 
+// Kernel timing: events around launches on their own stream (synchronous; only
+// while sst_gpu_kernel_timing is enabled).
+void kt_begin(sst_gpu_ctx* ctx, cudaStream_t s) {
+    if (!ctx->ktime) return;
+    if (!ctx->kt_ev[0])
+        for (auto& e : ctx->kt_ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ctx->kt_ev[0], s));
+}
+void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
+    if (!ctx->ktime) return;
+    CK(cudaEventRecord(ctx->kt_ev[1], s));
+    CK(cudaEventSynchronize(ctx->kt_ev[1]));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, ctx->kt_ev[0], ctx->kt_ev[1]));
+    ctx->kt_ms[kind] += ms;
+    ++ctx->kt_n[kind];
+}
+
+bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
+
 // Carves the wavefront pool of `cap` slots out of the slot's device buffer.
 template <class R>
 WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
@@ -714,8 +741,25 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
             a.pool.q_out = even ? a.pool.q_lb : a.pool.q_la;
             a.pool.cnt_in = even ? kQLiveA : kQLiveB;
             a.pool.cnt_out = even ? kQLiveB : kQLiveA;
-            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_iteration(a, st, explicit_keys, stream));
-            else CK(f64::launch_wf_iteration(a, st, explicit_keys, stream));
+            cudaEvent_t* ev = nullptr;
+            if (ctx->ktime) {
+                if (!ctx->kt_ev[0])
+                    for (auto& e : ctx->kt_ev) CK(cudaEventCreate(&e));
+                ev = ctx->kt_ev;
+            }
+            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_iteration(a, st, explicit_keys, stream, ev));
+            else CK(f64::launch_wf_iteration(a, st, explicit_keys, stream, ev));
+            if (ev) {  // reset | logic | gen | trace | sphere | shadow
+                CK(cudaEventSynchronize(ev[6]));
+                static const int kinds[6] = {SST_KT_WF_RESET, SST_KT_WF_LOGIC, SST_KT_WF_GEN, SST_KT_WF_TRACE,
+                                             SST_KT_WF_SPHERE, SST_KT_WF_SHADOW};
+                for (int j = 0; j < 6; ++j) {
+                    float ms = 0.0f;
+                    CK(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+                    ctx->kt_ms[kinds[j]] += ms;
+                    ++ctx->kt_n[kinds[j]];
+                }
+            }
         }
         out_last[k & 1] = a.pool.cnt_out;
         uint32_t* h = sl.wf_host + (k & 1) * kQCount;
@@ -736,8 +780,10 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
         if (live < cap) full = false;  // generation refills every free slot while ids remain
         if (live <= thresh) break;
     }
+    kt_begin(ctx, stream);
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, explicit_keys, stream));
     else CK(f64::launch_wf_finish(a, st, explicit_keys, stream));
+    kt_end(ctx, stream, SST_KT_WF_TAIL);
 }
 
 template <class R>
@@ -763,12 +809,14 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.sphere_batch = ctx->sphere_batch;
     a.trace_batch = ctx->trace_batch;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
-    if (wf && ctx->wavefront && n_paths < (1ull << 32) && ctx->desc.n_objects < 250) {
+    if (wf && use_wavefront(ctx, st) && n_paths < (1ull << 32) && ctx->desc.n_objects < 250) {
         run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream);
         return;
     }
+    kt_begin(ctx, stream);
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
     else CK(f64::launch_trace(a, st, explicit_keys, stream));
+    kt_end(ctx, stream, SST_KT_MEGAKERNEL);
 }
 
 void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
@@ -803,6 +851,8 @@ void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
     out->triangle_tests += v[kStTriTests];
     out->lane_iterations += v[kStLaneIters];
     out->warp_iterations += v[kStWarpIters];
+    out->shadow_triangle_tests += v[kStShadowTris];
+    out->wavefront_slot_visits += v[kStWfSlots];
 }
 
 void check_render_ready(sst_gpu_ctx* ctx, int integrator) {
@@ -863,7 +913,7 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
     if (const char* e = std::getenv("SST_CHUNK_PATHS")) target = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
     // wavefront: one pool drain per chunk, so chunks are as large as the radiance
     // scratch allows (2^28 paths = 1 GiB FP32): the long-path tail is paid once
-    if (ctx->wavefront) target = ctx->wf_chunk;
+    if (use_wavefront(ctx, integrator == SST_INTEGRATOR_ST)) target = ctx->wf_chunk;
     uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, target / per_sample));
     if (chunk > n_samples) chunk = n_samples;
     ensure_pipeline(ctx);
@@ -893,8 +943,10 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
                      nullptr, nullptr, nullptr, sl.rad.as<R>(), nullptr, sl.work.as<unsigned long long>(), sl.s,
                      &sl);
         if (ctx->last_film) CK(cudaStreamWaitEvent(sl.s, ctx->last_film, 0));
+        kt_begin(ctx, sl.s);
         if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
         else CK(f64::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
+        kt_end(ctx, sl.s, SST_KT_FILM);
         CK(cudaEventRecord(sl.film_done, sl.s));
         ctx->last_film = sl.film_done;
     }
@@ -982,7 +1034,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         ctx->serial = ++g_serial;
         if (const char* e = std::getenv("SST_SPHERE_BATCH")) ctx->sphere_batch = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SST_TRACE_BATCH")) ctx->trace_batch = std::max(0, std::atoi(e));
-        if (const char* e = std::getenv("SST_WAVEFRONT")) ctx->wavefront = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SST_WAVEFRONT")) ctx->wavefront = std::atoi(e);
         if (const char* e = std::getenv("SST_WF_POOL")) ctx->wf_pool = static_cast<uint32_t>(std::max(32, std::atoi(e)));
         if (const char* e = std::getenv("SST_WF_TAIL")) ctx->wf_tail = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("SST_WF_BATCH")) ctx->wf_batch = std::max(1, std::atoi(e));
@@ -1006,6 +1058,8 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         b->release();
     for (auto& b : ctx->sdf_dev) b.release();
     for (auto& b : ctx->skip_dev) b.release();
+    for (auto& e : ctx->kt_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
@@ -1041,6 +1095,25 @@ int sst_gpu_synchronize(sst_gpu_ctx* ctx) {
         require_device(ctx);
         join_slots(ctx);
         CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sst_gpu_kernel_timing(sst_gpu_ctx* ctx, int enable, double* ms, uint64_t* launches) {
+    return guarded([&] {
+        require_device(ctx);
+        join_slots(ctx);
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int k = 0; k < SST_KT_COUNT; ++k) {
+            if (ms) ms[k] = ctx->kt_ms[k];
+            if (launches) launches[k] = ctx->kt_n[k];
+        }
+        if (enable) {
+            for (int k = 0; k < SST_KT_COUNT; ++k) {
+                ctx->kt_ms[k] = 0.0;
+                ctx->kt_n[k] = 0;
+            }
+        }
+        ctx->ktime = enable != 0;
     });
 }
 

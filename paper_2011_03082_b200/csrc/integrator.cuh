@@ -87,7 +87,7 @@ struct PathLocal {
 struct LaneStats {
     uint32_t paths = 0, absorbed = 0, escaped = 0, capped = 0, errors = 0;
     uint64_t seg = 0, sphere = 0, events = 0, shadow = 0;
-    uint64_t traversals = 0, nodes = 0, tris = 0, lane_iters = 0, warp_iters = 0;
+    uint64_t traversals = 0, nodes = 0, tris = 0, lane_iters = 0, warp_iters = 0, shadow_tris = 0, wf_slots = 0;
     DecodeCount dc;
 };
 
@@ -351,7 +351,9 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     }
     // ---- 5. NEE
     if (nee) {
+        const uint64_t t0 = st.tris;
         p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt, st.tris);
+        st.shadow_tris += st.tris - t0;
         ++st.shadow;
     }
     return end;
@@ -417,7 +419,8 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
     }
     unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
                                       st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow,
-                                      st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters};
+                                      st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters,
+                                      st.shadow_tris, st.wf_slots};
     unsigned long long* dst = a.stats + static_cast<size_t>(blockIdx.x % kStCopies) * kStCount;
 #pragma unroll
     for (int k = 0; k < kStCount; ++k) {

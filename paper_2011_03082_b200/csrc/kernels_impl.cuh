@@ -179,7 +179,8 @@ cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {
 }
 
 // One wavefront iteration (a.pool.q_in/q_out set by the caller; queue counters cleared first).
-cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s) {
+cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s,
+                                cudaEvent_t* ev) {
     static unsigned g_logic[2][2] = {}, g_gen[2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
     static uint32_t cap_seen = 0, depth_seen = 0;
     const size_t trace_smem = wf_trace_smem<R>(a.sc.bvh_depth, kWfBlock);
@@ -197,7 +198,13 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
         g_sphere = wf_grid(k_wf_sphere, a.pool.cap);
         g_shadow = wf_grid(k_wf_shadow, a.pool.cap);
     }
+    // ev (optional, 7 events): brackets reset | logic | gen | trace | sphere | shadow
+    auto mark = [&](int k) {
+        if (ev) cudaEventRecord(ev[k], s);
+    };
+    mark(0);
     k_wf_reset<<<1, 32, 0, s>>>(a);
+    mark(1);
     const unsigned gl = g_logic[st][explicit_keys];
     if (st) {
         if (explicit_keys) k_wf_logic<true, true><<<gl, kWfBlock, 0, s>>>(a);
@@ -206,11 +213,16 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
         if (explicit_keys) k_wf_logic<false, true><<<gl, kWfBlock, 0, s>>>(a);
         else k_wf_logic<false, false><<<gl, kWfBlock, 0, s>>>(a);
     }
+    mark(2);
     if (explicit_keys) k_wf_gen<true><<<g_gen[1], kWfBlock, 0, s>>>(a);
     else k_wf_gen<false><<<g_gen[0], kWfBlock, 0, s>>>(a);
+    mark(3);
     k_wf_trace<<<g_trace, kWfBlock, trace_smem, s>>>(a);
+    mark(4);
     if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s>>>(a);
+    mark(5);
     if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s>>>(a);
+    mark(6);
     return cudaGetLastError();
 }
 

@@ -104,7 +104,10 @@ enum : int {
     kStEscaped, kStCapped, kStErrors, kStShadow,
     // work counters (profiling): nearest-hit traversals, interior nodes visited,
     // triangle tests (nearest + shadow), live-lane iterations, warp iterations
-    kStTraversals, kStNodes, kStTriTests, kStLaneIters, kStWarpIters, kStCount
+    kStTraversals, kStNodes, kStTriTests, kStLaneIters, kStWarpIters,
+    kStShadowTris,  // triangle tests of NEE shadow rays (also in kStTriTests)
+    kStWfSlots,     // wavefront logic-pass slot visits
+    kStCount
 };
 
 // Stats are kept in kStCopies interleaved copies ([copy][kStCount]) so the per-block

@@ -106,7 +106,8 @@ SST_D void flush_counts(unsigned long long* stats, const unsigned long long (&v)
 SST_D void flush_lane_stats(unsigned long long* stats, const LaneStats& st) {
     const unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
                                             st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow,
-                                            st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters};
+                                            st.traversals, st.nodes, st.tris, st.lane_iters, st.warp_iters,
+                                            st.shadow_tris, st.wf_slots};
     flush_counts<kStCount>(stats, v);
 }
 
@@ -211,6 +212,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
     PathLocal<R> p;
     uint32_t phase = meta_phase(q.meta[s].w);
     *live = false;
+    ++st.wf_slots;
     if (phase == kPhEmpty) return kEmitNone;  // ended in k_wf_sphere (already on the free queue)
     load_slot(q, s, p, &phase);
     ++st.lane_iters;
@@ -538,6 +540,7 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
     unsigned long long v[kStCount] = {};
     v[kStShadow] = shadow;
     v[kStTriTests] = tris;
+    v[kStShadowTris] = tris;
     flush_counts<kStCount>(a.stats, v);
 }
 

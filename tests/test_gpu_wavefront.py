@@ -67,8 +67,8 @@ def test_wavefront_paths_identical_to_megakernel(models_dir, scenes, precision, 
     n = 40000 if precision == "f64" else 200000
     pix, smp, ch = _keys(scene.n_pixels, n)
     mk = _renderer(models_dir, precision, SST_WAVEFRONT=0)
-    configs = [dict(SST_WAVEFRONT=1),  # default pool: drain + hand-off
-               dict(SST_WAVEFRONT=1, SST_WF_POOL=2048, SST_WF_TAIL=64, SST_WF_BATCH=1)]  # many recycles
+    configs = [dict(SST_WAVEFRONT=2),  # default pool: drain + hand-off
+               dict(SST_WAVEFRONT=2, SST_WF_POOL=2048, SST_WF_TAIL=64, SST_WF_BATCH=1)]  # many recycles
     wfs = [_renderer(models_dir, precision, **c) for c in configs]
     try:
         for r in [mk] + wfs:
@@ -102,7 +102,7 @@ def test_wavefront_film_identical_to_megakernel(models_dir, scenes):
     from paper_2011_03082_b200 import PT, ST, abi
     scene = scenes["c5"]
     mk = _renderer(models_dir, "f64", SST_WAVEFRONT=0)
-    wf = _renderer(models_dir, "f64", SST_WAVEFRONT=1, SST_WF_POOL=8192, SST_WF_TAIL=256)
+    wf = _renderer(models_dir, "f64", SST_WAVEFRONT=2, SST_WF_POOL=8192, SST_WF_TAIL=256)
     try:
         for r in (mk, wf):
             r.upload_scene(scene)

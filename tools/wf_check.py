@@ -23,7 +23,7 @@ MODELS = os.path.join(ROOT, "tests", "golden", "models")
 
 
 def renderer(wf, prec):
-    os.environ["SST_WAVEFRONT"] = "1" if wf else "0"
+    os.environ["SST_WAVEFRONT"] = "2" if wf else "0"
     r = sb.Renderer(0, prec)
     r.load_models_dir(MODELS)
     return r

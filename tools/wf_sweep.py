@@ -16,7 +16,7 @@ for integ, iname in ((sb.ST, "st"), (sb.PT, "pt")):
             os.environ["SST_WAVEFRONT"] = "0"
         else:
             pool, tail, batch = cfg.split(":")
-            os.environ.update(SST_WAVEFRONT="1", SST_WF_POOL=pool, SST_WF_TAIL=tail, SST_WF_BATCH=batch)
+            os.environ.update(SST_WAVEFRONT="2", SST_WF_POOL=pool, SST_WF_TAIL=tail, SST_WF_BATCH=batch)
         r = sb.Renderer(0, "f32")
         r.load_models_dir(os.path.join(ROOT, "tests", "golden", "models"))
         r.upload_scene(scene)
