@@ -226,23 +226,40 @@ constexpr int kDone = 0x7fffffff;
 // 0 any. FP32 rays use it (a ray outside every medium can only enter, a flight
 // inside can only leave): with outward-wound meshes this rejects the spurious
 // re-hits of neighbouring triangles that FP32 rounding produces at surfaces.
-template <class R, class Stack>
-SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
-                               int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
-                               uint64_t& n_tris, Stack& stk) {
-    int sp = 0;
-    int node = 0;   // interior (>= 0), leaf (< 0) or kDone
-    int leaf = 0;   // postponed leaf (< 0) or 0 = none
-    R t_best = t_max;
-    bool found = false;
-    auto pop = [&]() -> int {
+// Traversal state of one ray. round() = one while-while round: interior nodes until
+// this lane holds a leaf and every active lane does (or is done), then the parked
+// leaf (and a leaf the traversal sits on). The wavefront trace kernel drives rounds
+// directly so that lanes whose ray finished take a new ray between rounds.
+template <class R>
+struct Trav {
+    int node;    // interior (>= 0), leaf (< 0) or kDone
+    int leaf;    // postponed leaf (< 0) or 0 = none
+    int sp;
+    R t_best;
+    bool found;
+    Hit hit;
+    SST_D void init(R t_max, int root = 0) {
+        node = root;
+        leaf = 0;
+        sp = 0;
+        t_best = t_max;
+        found = false;
+        hit = Hit{0, 0};
+    }
+    SST_D bool done() const { return node == kDone && leaf == 0; }
+
+    template <class Stack>
+    SST_D int pop(Stack& stk) {
         while (sp > 0) {
             --sp;
             if (stk.dist(sp) <= t_best) return stk.node(sp);
         }
         return kDone;
-    };
-    while (node != kDone || leaf != 0) {
+    }
+
+    template <class Stack>
+    SST_D void round(const DevScene<R>& sc, const RayK<R>& ray, R t_min, int skip, int cull_obj, int want_sign,
+                     uint64_t& n_nodes, uint64_t& n_tris, Stack& stk) {
         // interior nodes until this lane holds a leaf and all lanes do
         while (node != kDone && node >= 0) {
             R b[12];
@@ -265,11 +282,11 @@ SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_mi
             } else if (h1) {
                 node = c1;
             } else {
-                node = pop();
+                node = pop(stk);
             }
             if (node < 0 && leaf == 0) {  // park the leaf, keep descending
                 leaf = node;
-                node = pop();
+                node = pop(stk);
             }
             if (!__any_sync(__activemask(), leaf == 0)) break;
         }
@@ -287,20 +304,30 @@ SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_mi
                 const bool orient = want_sign == 0 || (want_sign > 0 ? det > R(0) : det < R(0));
                 if (t >= R(0) && static_cast<int>(id) != skip && orient) {
                     t_best = t;
-                    hit->tri = id;
-                    hit->obj = obj;
+                    hit.tri = id;
+                    hit.obj = obj;
                     found = true;
                 }
             }
             leaf = 0;
             if (node != kDone && node < 0) {
                 leaf = node;
-                node = pop();
+                node = pop(stk);
             }
         }
     }
-    *t_hit = t_best;
-    return found;
+};
+
+template <class R, class Stack>
+SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
+                               int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
+                               uint64_t& n_tris, Stack& stk) {
+    Trav<R> tr;
+    tr.init(t_max);
+    while (!tr.done()) tr.round(sc, ray, t_min, skip, cull_obj, want_sign, n_nodes, n_tris, stk);
+    *t_hit = tr.t_best;
+    if (tr.found) *hit = tr.hit;
+    return tr.found;
 }
 
 template <class R>

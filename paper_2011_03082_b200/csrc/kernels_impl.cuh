@@ -82,12 +82,22 @@ __global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_M
 // Wavefront integrator kernels (wavefront.cuh). Persistent grid-stride kernels sized
 // to the resident capacity (SM count x blocks per SM) so per-block stat flushes stay few.
 constexpr int kWfBlock = 256;
+// Minimum resident blocks per SM (register caps) of the wavefront kernels; tuning knobs.
+#ifndef SST_WF_LOGIC_BLOCKS
+#define SST_WF_LOGIC_BLOCKS 5
+#endif
+#ifndef SST_WF_TRACE_BLOCKS
+#define SST_WF_TRACE_BLOCKS 1
+#endif
+#ifndef SST_WF_SPHERE_BLOCKS
+#define SST_WF_SPHERE_BLOCKS 2
+#endif
 template <bool ST, bool EX>
-__global__ void __launch_bounds__(kWfBlock) k_wf_logic(TraceArgs<R> a) { wf_logic<R, ST, EX>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock, SST_WF_LOGIC_BLOCKS) k_wf_logic(TraceArgs<R> a) { wf_logic<R, ST, EX>(a, a.pool); }
 template <bool EX>
 __global__ void __launch_bounds__(kWfBlock) k_wf_gen(TraceArgs<R> a) { wf_gen<R, EX>(a, a.pool); }
-__global__ void __launch_bounds__(kWfBlock) k_wf_trace(TraceArgs<R> a) { wf_trace<R>(a, a.pool); }
-__global__ void __launch_bounds__(kWfBlock, 2) k_wf_sphere(TraceArgs<R> a) { wf_sphere<R>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock, SST_WF_TRACE_BLOCKS) k_wf_trace(TraceArgs<R> a) { wf_trace<R>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock, SST_WF_SPHERE_BLOCKS) k_wf_sphere(TraceArgs<R> a) { wf_sphere<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_compact(TraceArgs<R> a) { wf_compact<R>(a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_init(TraceArgs<R> a) { wf_init<R>(a.pool); }

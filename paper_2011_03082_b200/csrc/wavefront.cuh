@@ -444,28 +444,61 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
                        reinterpret_cast<R*>(wf_smem + static_cast<size_t>(entries) * blockDim.x * sizeof(int)) +
                            threadIdx.x,
                        static_cast<int>(blockDim.x)};
+    // Persistent lanes with ray refill (Aila & Laine): rays run while-while rounds;
+    // when at least kTraceRefill lanes of the warp have finished their ray (or all
+    // have), they take new rays from the queue together, so a warp never idles until
+    // its slowest ray is done.
+    constexpr int kTraceRefill = 8;
     const uint32_t n = q.counts[kQTrace];
+    const unsigned lane = threadIdx.x & 31u;
+    bool have = false, exhausted = false;
+    uint32_t s = 0;
+    int skip = -1, cull = -1, want = 0;
+    R t_min = R(0);
+    RayK<R> ray;
+    Trav<R> tr;
+    tr.init(R(0));
+    tr.node = kDone;
     for (;;) {
-        const uint32_t i = warp_fetch(q.counts + kQFetchTrace);
-        if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
-        if (i >= n) continue;
-        const uint32_t s = q.q_trace[i];
-        const Q4<R> xl = q.xl[s], wr = q.wr[s];
-        const uint4 m = q.meta[s];
-        const int obj = meta_obj(m.w);
-        const int skip = static_cast<int>(m.z);
-        const int cull = static_cast<int>((m.w >> 16) & 0xffu) - 1;
-        const bool inside = obj >= 0;
-        const R t_max = inside ? q.tpend[s] : Real<R>::kInf;
-        const RayK<R> ray = make_ray(mk<R>(xl.x, xl.y, xl.z), mk<R>(wr.x, wr.y, wr.z));
-        const int want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
-        R t_hit;
-        Hit h{0, 0};
-        const bool hit = intersect_nearest_s(sc, ray, skip >= 0 ? sc.surf_eps : sc.t_min, t_max, skip, cull, want,
-                                             &t_hit, &h, nodes, tris, stk);
-        ++trav;
-        q.thit[s] = t_hit;
-        q.hinfo[s] = make_uint2(h.tri, h.obj | (hit ? 0x80000000u : 0u));
+        const unsigned idle = __ballot_sync(0xffffffffu, !have);
+        if (!exhausted && (__popc(idle) >= kTraceRefill || idle == 0xffffffffu)) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(q.counts + kQFetchTrace, static_cast<uint32_t>(__popc(idle)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= n) {
+                exhausted = true;
+            } else if (!have) {
+                const uint32_t i = base + __popc(idle & ((1u << lane) - 1u));
+                if (i < n) {
+                    s = q.q_trace[i];
+                    const Q4<R> xl = q.xl[s], wr = q.wr[s];
+                    const uint4 m = q.meta[s];
+                    const int obj = meta_obj(m.w);
+                    skip = static_cast<int>(m.z);
+                    cull = static_cast<int>((m.w >> 16) & 0xffu) - 1;
+                    const bool inside = obj >= 0;
+                    ray = make_ray(mk<R>(xl.x, xl.y, xl.z), mk<R>(wr.x, wr.y, wr.z));
+                    want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
+                    t_min = skip >= 0 ? sc.surf_eps : sc.t_min;
+                    tr.init(inside ? q.tpend[s] : Real<R>::kInf);
+                    have = true;
+                }
+            }
+        }
+        if (__ballot_sync(0xffffffffu, have) == 0u) {
+            if (exhausted) break;
+            continue;
+        }
+        if (have) {
+            tr.round(sc, ray, t_min, skip, cull, want, nodes, tris, stk);
+            if (tr.done()) {
+                q.thit[s] = tr.t_best;
+                q.hinfo[s] = make_uint2(tr.found ? tr.hit.tri : 0u,
+                                        (tr.found ? tr.hit.obj : 0u) | (tr.found ? 0x80000000u : 0u));
+                ++trav;
+                have = false;
+            }
+        }
     }
     unsigned long long v[kStCount] = {};
     v[kStTraversals] = trav;
