@@ -448,7 +448,10 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
     // when at least kTraceRefill lanes of the warp have finished their ray (or all
     // have), they take new rays from the queue together, so a warp never idles until
     // its slowest ray is done.
-    constexpr int kTraceRefill = 8;
+#ifndef SST_TRACE_REFILL
+#define SST_TRACE_REFILL 16
+#endif
+    constexpr int kTraceRefill = SST_TRACE_REFILL;
     const uint32_t n = q.counts[kQTrace];
     const unsigned lane = threadIdx.x & 31u;
     bool have = false, exhausted = false;
