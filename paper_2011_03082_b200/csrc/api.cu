@@ -12,6 +12,9 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <functional>
+#include <thread>
 #include <fstream>
 #include <map>
 #include <memory>
@@ -109,6 +112,20 @@ struct ObjectHost {
 
 }  // namespace
 
+namespace sstg {
+// A wavefront render launch in flight (api.cu WfJob): the host drives its iterations
+// in batches; render calls return while a job drains so consecutive calls overlap.
+struct WfJobBase {
+    virtual ~WfJobBase() = default;
+    // Reads completed batches and keeps two in flight; the oldest job may finish (hand-
+    // off + film). block: wait for this job's oldest batch. Returns 2 finished, 1
+    // progressed, 0 idle.
+    virtual int advance(bool may_finish, bool block) = 0;
+    virtual bool supply_done() const = 0;
+    const void* slot = nullptr;
+};
+}  // namespace sstg
+
 struct sst_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -171,6 +188,7 @@ struct sst_gpu_ctx {
     uint32_t wf_tail = 1u << 17;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
+    std::deque<std::unique_ptr<WfJobBase>> jobs;  // FIFO: finishes (and films) in launch order
     // per-kernel device timing (sst_gpu_kernel_timing)
     bool ktime = false;
     double kt_ms[SST_KT_COUNT] = {};
@@ -214,7 +232,10 @@ void ensure_constants(sst_gpu_ctx* ctx) {
     g_const_owner[ctx->device] = {ctx, ctx->model_gen};
 }
 
+void join_slots(sst_gpu_ctx* ctx);
+
 void set_models(sst_gpu_ctx* ctx, const HostModel (&m)[3]) {
+    join_slots(ctx);  // in-flight renders read the decoder constants
     std::vector<double> w;
     double norms[6];
     pack_models(m, w, norms);
@@ -712,29 +733,31 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     return q;
 }
 
-// Wavefront render of one launch's paths (wavefront.cuh): iterations of
-// logic -> trace -> sphere -> shadow over a pool of path slots until the live slots
-// drop to min(pool/8, wf_tail), then the megakernel finishes the tail. The host checks
-// the live count of batch k-1 while batch k runs (no bubble).
+// Wavefront render of one launch's paths (wavefront.cuh): batches of iterations of
+// reset -> logic -> gen -> trace -> sphere -> shadow over a pool of path slots until
+// the live slots drop to min(pool/8, wf_tail), then the megakernel finishes the tail
+// and on_finish (the film accumulation) is enqueued. The host keeps two batches in
+// flight and reads the live count of each as it completes (no bubble).
 template <class R>
-void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_keys, sst_gpu_ctx::Slot& sl,
-                   cudaStream_t stream) {
-    const uint32_t cap = static_cast<uint32_t>(std::max<uint64_t>(32, std::min<uint64_t>(a.n_paths, ctx->wf_pool)));
-    a.pool = carve_pool<R>(sl, cap);
-    if (!sl.wf_host) {
-        CK(cudaMallocHost(&sl.wf_host, 2 * kQCount * sizeof(uint32_t)));
-        for (auto& e : sl.wf_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_init(a, stream));
-    else CK(f64::launch_wf_init(a, stream));
-    const uint32_t thresh = std::max<uint32_t>(1, std::min<uint32_t>(cap / 8, ctx->wf_tail));
-    const int batch = std::max(1, ctx->wf_batch);
-    uint64_t it = 0;
-    bool full = true;  // pool full (path supply left): logic walks all slots in order
+struct WfJob final : WfJobBase {
+    sst_gpu_ctx* ctx;
+    sst_gpu_ctx::Slot* sl;
+    TraceArgs<R> a;
+    bool st, ex;
+    cudaStream_t stream;
+    uint32_t cap = 0, thresh = 0;
+    int batch = 1;
+    uint64_t it = 0, k = 0, nread = 0;  // iterations and batches launched, batches read
+    bool full = true;                   // pool full (path supply left): logic walks all slots in order
+    bool supply = false, done = false;
     int out_last[2] = {kQLiveA, kQLiveA};
-    const bool wf_trace = std::getenv("SST_WF_TRACE") != nullptr;
-    const auto t_start = std::chrono::steady_clock::now();
-    for (uint64_t k = 0;; ++k) {
+    std::function<void()> on_finish;
+    bool log = false;
+    std::chrono::steady_clock::time_point t0;
+
+    bool supply_done() const override { return supply; }
+
+    void launch_batch() {
         for (int b = 0; b < batch; ++b, ++it) {
             const bool even = (it & 1) == 0;  // live lists ping-pong: A -> B -> A ...
             a.pool.q_in = full ? nullptr : (even ? a.pool.q_la : a.pool.q_lb);
@@ -747,8 +770,8 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
                     for (auto& e : ctx->kt_ev) CK(cudaEventCreate(&e));
                 ev = ctx->kt_ev;
             }
-            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_iteration(a, st, explicit_keys, stream, ev));
-            else CK(f64::launch_wf_iteration(a, st, explicit_keys, stream, ev));
+            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_iteration(a, st, ex, stream, ev));
+            else CK(f64::launch_wf_iteration(a, st, ex, stream, ev));
             if (ev) {  // reset | logic | gen | trace | sphere | shadow
                 CK(cudaEventSynchronize(ev[6]));
                 static const int kinds[6] = {SST_KT_WF_RESET, SST_KT_WF_LOGIC, SST_KT_WF_GEN, SST_KT_WF_TRACE,
@@ -762,28 +785,122 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
             }
         }
         out_last[k & 1] = a.pool.cnt_out;
-        uint32_t* h = sl.wf_host + (k & 1) * kQCount;
-        CK(cudaMemcpyAsync(h, a.pool.counts, kQCount * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
-        CK(cudaEventRecord(sl.wf_ev[k & 1], stream));
-        if (k == 0) continue;
-        CK(cudaEventSynchronize(sl.wf_ev[(k - 1) & 1]));
-        // live slots after the last logic pass of batch k-1; K_logic refills every empty
-        // slot while path ids remain, so live <= thresh < cap means the supply is exhausted
-        const uint32_t live = sl.wf_host[((k - 1) & 1) * kQCount + out_last[(k - 1) & 1]];
-        if (wf_trace) {
-            const auto now = std::chrono::steady_clock::now();
-            std::fprintf(stderr, "[wf] batch %llu live %u trace %u sphere %u shadow %u t %.3f ms\n",
-                         static_cast<unsigned long long>(k - 1), live, sl.wf_host[((k - 1) & 1) * kQCount + kQTrace],
-                         sl.wf_host[((k - 1) & 1) * kQCount + kQSphere], sl.wf_host[((k - 1) & 1) * kQCount + kQShadow],
-                         std::chrono::duration<double, std::milli>(now - t_start).count());
-        }
-        if (live < cap) full = false;  // generation refills every free slot while ids remain
-        if (live <= thresh) break;
+        CK(cudaMemcpyAsync(sl->wf_host + (k & 1) * kQCount, a.pool.counts, kQCount * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaEventRecord(sl->wf_ev[k & 1], stream));
+        ++k;
     }
-    kt_begin(ctx, stream);
-    if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, explicit_keys, stream));
-    else CK(f64::launch_wf_finish(a, st, explicit_keys, stream));
-    kt_end(ctx, stream, SST_KT_WF_TAIL);
+
+    int advance(bool may_finish, bool block) override {
+        bool progressed = false;
+        while (nread < k && !done) {
+            const cudaEvent_t e = sl->wf_ev[nread & 1];
+            if (block && !progressed) {
+                CK(cudaEventSynchronize(e));
+            } else {
+                const cudaError_t q = cudaEventQuery(e);
+                if (q == cudaErrorNotReady) break;
+                CK(q);
+            }
+            const uint32_t* h = sl->wf_host + (nread & 1) * kQCount;
+            const uint32_t live = h[out_last[nread & 1]];
+            if (log)
+                std::fprintf(stderr, "[wf] batch %llu live %u trace %u sphere %u shadow %u t %.3f ms\n",
+                             static_cast<unsigned long long>(nread), live, h[kQTrace], h[kQSphere], h[kQShadow],
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+            ++nread;
+            progressed = true;
+            // generation refills every free slot while ids remain: live < cap means the
+            // supply is exhausted (the pool drains from here)
+            if (live < cap) full = false, supply = true;
+            if (live <= thresh) done = true;
+        }
+        if (done) {
+            if (!may_finish) return progressed ? 1 : 0;
+            kt_begin(ctx, stream);
+            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, ex, stream));
+            else CK(f64::launch_wf_finish(a, st, ex, stream));
+            kt_end(ctx, stream, SST_KT_WF_TAIL);
+            if (on_finish) on_finish();
+            return 2;
+        }
+        while (k - nread < 2) {  // two batches in flight (the pinned count buffers are double)
+            launch_batch();
+            progressed = true;
+        }
+        return progressed ? 1 : 0;
+    }
+};
+
+// Advances every active job (only the oldest may finish). block: wait on the oldest.
+bool pump_jobs(sst_gpu_ctx* ctx, bool block) {
+    bool any = false;
+    for (size_t i = 0; i < ctx->jobs.size();) {
+        const int r = ctx->jobs[i]->advance(i == 0, block && i == 0);
+        if (r == 2) {  // only the front finishes
+            ctx->jobs.pop_front();
+            any = true;
+            continue;  // the next job is the front now
+        }
+        any |= r != 0;
+        ++i;
+    }
+    return any;
+}
+
+// Drives every job to completion (sync points: stats, host films, uploads, destroy).
+void drain_jobs(sst_gpu_ctx* ctx) {
+    while (!ctx->jobs.empty()) pump_jobs(ctx, true);
+}
+
+// Waits until no job uses render slot sl (slots are reused round robin).
+void wait_slot(sst_gpu_ctx* ctx, const sst_gpu_ctx::Slot* sl) {
+    for (;;) {
+        bool busy = false;
+        for (const auto& j : ctx->jobs) busy |= j->slot == sl;
+        if (!busy) return;
+        if (!pump_jobs(ctx, false)) pump_jobs(ctx, true);
+    }
+}
+
+template <class R>
+void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_keys, sst_gpu_ctx::Slot& sl,
+                   cudaStream_t stream, std::function<void()> on_finish, bool sync) {
+    auto job = std::make_unique<WfJob<R>>();
+    WfJob<R>& j = *job;
+    j.ctx = ctx;
+    j.sl = &sl;
+    j.slot = &sl;
+    j.st = st;
+    j.ex = explicit_keys;
+    j.stream = stream;
+    j.cap = static_cast<uint32_t>(std::max<uint64_t>(32, std::min<uint64_t>(a.n_paths, ctx->wf_pool)));
+    a.pool = carve_pool<R>(sl, j.cap);
+    j.a = a;
+    if (!sl.wf_host) {
+        CK(cudaMallocHost(&sl.wf_host, 2 * kQCount * sizeof(uint32_t)));
+        for (auto& e : sl.wf_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_init(j.a, stream));
+    else CK(f64::launch_wf_init(j.a, stream));
+    j.thresh = std::max<uint32_t>(1, std::min<uint32_t>(j.cap / 8, ctx->wf_tail));
+    j.batch = std::max(1, ctx->wf_batch);
+    j.on_finish = std::move(on_finish);
+    j.log = std::getenv("SST_WF_TRACE") != nullptr;
+    j.t0 = std::chrono::steady_clock::now();
+    ctx->jobs.push_back(std::move(job));
+    if (sync) {
+        drain_jobs(ctx);
+        return;
+    }
+    // asynchronous call: drive every job until this one's path supply is exhausted;
+    // its drain continues under later calls (overlapping their launches) or a sync point
+    for (;;) {
+        bool mine = false;
+        for (const auto& q : ctx->jobs) mine |= q.get() == &j;
+        if (!mine || j.supply) return;
+        if (!pump_jobs(ctx, false)) std::this_thread::yield();
+    }
 }
 
 template <class R>
@@ -791,7 +908,7 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
                uint64_t seed, uint64_t n_paths, uint32_t n_pix, uint32_t sample_begin,
                const uint32_t* pix, const uint32_t* smp, const uint8_t* ch, R* radiance,
                uint32_t* segments, unsigned long long* work, cudaStream_t stream,
-               sst_gpu_ctx::Slot* wf) {
+               sst_gpu_ctx::Slot* wf, std::function<void()> on_finish, bool sync) {
     TraceArgs<R> a{};
     a.sc = sc;
     a.nee = nee;
@@ -810,13 +927,14 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.trace_batch = ctx->trace_batch;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
     if (wf && use_wavefront(ctx, st) && n_paths < (1ull << 32) && ctx->desc.n_objects < 250) {
-        run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream);
+        run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream, std::move(on_finish), sync);
         return;
     }
     kt_begin(ctx, stream);
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
     else CK(f64::launch_trace(a, st, explicit_keys, stream));
     kt_end(ctx, stream, SST_KT_MEGAKERNEL);
+    if (on_finish) on_finish();
 }
 
 void read_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
@@ -877,6 +995,7 @@ void ensure_pipeline(sst_gpu_ctx* ctx) {
 
 // Makes ctx->stream wait for every render slot (no host synchronisation).
 void join_slots(sst_gpu_ctx* ctx) {
+    drain_jobs(ctx);
     if (!ctx->ev_start) return;
     for (auto& sl : ctx->slots) CK(cudaStreamWaitEvent(ctx->stream, sl.film_done, 0));
 }
@@ -937,18 +1056,23 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         const uint32_t ns = std::min(chunk, s1 - s);
         auto& sl = ctx->slots[ctx->next_slot];
         ctx->next_slot = (ctx->next_slot + 1) % sst_gpu_ctx::kSlots;
+        wait_slot(ctx, &sl);  // a job still draining on this slot owns its buffers
         sl.rad.reserve(per_sample * chunk * sizeof(R));
         CK(cudaStreamWaitEvent(sl.s, ctx->ev_start, 0));
+        // film accumulation of this chunk, enqueued once its paths are done; films
+        // chain in chunk order (jobs finish FIFO) -> deterministic sums
+        auto film = [ctx, &sl, per_sample, ns, dsum, dsq]() {
+            if (ctx->last_film) CK(cudaStreamWaitEvent(sl.s, ctx->last_film, 0));
+            kt_begin(ctx, sl.s);
+            if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
+            else CK(f64::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
+            kt_end(ctx, sl.s, SST_KT_FILM);
+            CK(cudaEventRecord(sl.film_done, sl.s));
+            ctx->last_film = sl.film_done;
+        };
         run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, false, nee, seed, per_sample * ns, n_pix, s,
                      nullptr, nullptr, nullptr, sl.rad.as<R>(), nullptr, sl.work.as<unsigned long long>(), sl.s,
-                     &sl);
-        if (ctx->last_film) CK(cudaStreamWaitEvent(sl.s, ctx->last_film, 0));
-        kt_begin(ctx, sl.s);
-        if constexpr (std::is_same<R, float>::value) CK(f32::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
-        else CK(f64::launch_film(sl.rad.as<R>(), per_sample, ns, dsum, dsq, sl.s));
-        kt_end(ctx, sl.s, SST_KT_FILM);
-        CK(cudaEventRecord(sl.film_done, sl.s));
-        ctx->last_film = sl.film_done;
+                     &sl, film, sync);
     }
     if (!sync) return;  // asynchronous device-pointer call: sst_gpu_read_stats collects
     join_slots(ctx);
@@ -991,7 +1115,7 @@ void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, 
     run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, true, nee, seed, n, n_pix, 0,
                  ctx->keys_pix.as<uint32_t>(), ctx->keys_smp.as<uint32_t>(), ctx->keys_ch.as<uint8_t>(),
                  ctx->radiance.as<R>(), ctx->segments.as<uint32_t>(), ctx->work.as<unsigned long long>(),
-                 ctx->stream, &ctx->slots[0]);
+                 ctx->stream, &ctx->slots[0], nullptr, true);
     std::vector<R> rad(n);
     CK(cudaMemcpyAsync(rad.data(), ctx->radiance.p, n * sizeof(R), cudaMemcpyDeviceToHost, ctx->stream));
     if (segments) CK(cudaMemcpyAsync(segments, ctx->segments.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1046,6 +1170,11 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
 void sst_gpu_destroy(sst_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    try {
+        drain_jobs(ctx);
+    } catch (...) {
+        ctx->jobs.clear();
+    }
     cudaStreamSynchronize(ctx->stream);
     {
         std::lock_guard<std::mutex> lk(g_const_mu);
