@@ -701,8 +701,9 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     const size_t n = cap;
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
                             n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
-                            kQCount * 4, 8, n * 4, n * 4, n * 4};
-    size_t off[18], total = 0;
+                            kQCount * 4, 8, n * 4, n * 4, n * 4,
+                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4};
+    size_t off[21], total = 0;
     int k = 0;
     for (size_t b : sizes) {
         off[k++] = total;
@@ -721,7 +722,7 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.hinfo = reinterpret_cast<uint2*>(base + off[6]);
     q.nee_p = reinterpret_cast<Q4<R>*>(base + off[7]);
     q.nee_w = reinterpret_cast<Q4<R>*>(base + off[8]);
-    q.q_trace = reinterpret_cast<uint32_t*>(base + off[9]);
+    q.tq = reinterpret_cast<uint32_t*>(base + off[9]);
     q.q_sphere = reinterpret_cast<uint32_t*>(base + off[10]);
     q.q_shadow = reinterpret_cast<uint32_t*>(base + off[11]);
     q.q_live = reinterpret_cast<uint32_t*>(base + off[12]);
@@ -730,6 +731,9 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.q_la = reinterpret_cast<uint32_t*>(base + off[15]);
     q.q_lb = reinterpret_cast<uint32_t*>(base + off[16]);
     q.q_free = reinterpret_cast<uint32_t*>(base + off[17]);
+    q.tr_o = reinterpret_cast<Q4<R>*>(base + off[18]);
+    q.tr_d = reinterpret_cast<Q4<R>*>(base + off[19]);
+    q.tr_f = reinterpret_cast<uint32_t*>(base + off[20]);
     return q;
 }
 

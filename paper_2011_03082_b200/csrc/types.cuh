@@ -137,11 +137,19 @@ struct WfPool {
     uint64_t* rng;    // RandomStream state
     uint4* meta;      // path id, segments, skip triangle, packed obj/channel/flags/phase/cull
     R* tpend;         // free-flight length of the queued traversal
+    uint32_t* tq;     // trace-queue position of the slot's queued traversal
+    // Trace queue as contiguous ray records (indexed by queue position, written by
+    // the logic / generation kernels, read coalesced by k_wf_trace), and the
+    // traversal results at the same positions (read by the next logic pass).
+    Q4<R>* tr_o;      // origin, t_max
+    Q4<R>* tr_d;      // direction, skip triangle (int bits)
+    uint32_t* tr_f;   // (cull + 1) | inside << 8
     R* thit;          // traversal result: distance
     uint2* hinfo;     // traversal result: triangle, object | found << 31
+    // Shadow queue records (indexed by queue position): slot in q_shadow.
     Q4<R>* nee_p;     // NEE record: point, weight
-    Q4<R>* nee_w;     // NEE record: direction
-    uint32_t *q_trace, *q_sphere, *q_shadow, *q_live;
+    Q4<R>* nee_w;     // NEE record: direction, obj | channel << 8 (int bits)
+    uint32_t *q_sphere, *q_shadow, *q_live;
     uint32_t *q_la, *q_lb;  // ping-pong lists of live slots (logic input / output)
     uint32_t* q_free;       // free slots (path ended), refilled by the generation kernel
     uint32_t* q_in;         // this iteration's input list (q_la or q_lb), count counts[cnt_in]

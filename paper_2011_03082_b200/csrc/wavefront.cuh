@@ -41,6 +41,17 @@ SST_D uint32_t pack_meta(int obj, int c, bool r_valid, uint32_t phase, int cull)
            (static_cast<uint32_t>(r_valid) << 10) | (phase << 11) | (static_cast<uint32_t>(cull + 1) << 16);
 }
 SST_D uint32_t meta_phase(uint32_t m) { return (m >> 11) & 3u; }
+// Integer payloads carried in the spare lane of a record vector.
+template <class R>
+SST_D R int_bits(int v) {
+    if constexpr (sizeof(R) == 4) return __int_as_float(v);
+    else return __longlong_as_double(static_cast<long long>(v));
+}
+template <class R>
+SST_D int bits_int(R v) {
+    if constexpr (sizeof(R) == 4) return __float_as_int(v);
+    else return static_cast<int>(__double_as_longlong(v));
+}
 SST_D int meta_obj(uint32_t m) { return static_cast<int>(m & 0xffu) - 1; }
 SST_D int meta_c(uint32_t m) { return static_cast<int>((m >> 8) & 3u); }
 
@@ -152,7 +163,7 @@ SST_D void block_push(bool want, uint32_t value, uint32_t* counter, uint32_t* qu
 // non-empty queue per block): queue j receives `value` from the threads with want[j].
 template <int N>
 SST_D void block_pushn(const bool (&want)[N], uint32_t value, uint32_t* const (&counter)[N],
-                       uint32_t* const (&queue)[N]) {
+                       uint32_t* const (&queue)[N], uint32_t (&pos)[N]) {
     __shared__ uint32_t wc[8][33];
     __shared__ uint32_t qbase[8];
     static_assert(N <= 8, "queues");
@@ -177,8 +188,10 @@ SST_D void block_pushn(const bool (&want)[N], uint32_t value, uint32_t* const (&
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < N; ++j)
-        if (want[j]) queue[j][qbase[j] + wc[j][warp] + __popc(b[j] & ((1u << lane) - 1u))] = value;
+    for (int j = 0; j < N; ++j) {
+        pos[j] = qbase[j] + wc[j][warp] + __popc(b[j] & ((1u << lane) - 1u));
+        if (want[j] && queue[j]) queue[j][pos[j]] = value;
+    }
     __syncthreads();
 }
 
@@ -191,12 +204,37 @@ SST_D uint32_t warp_fetch(uint32_t* cursor) {
 }
 
 // Warp-aggregated append from divergent code.
-SST_D void warp_push(uint32_t value, uint32_t* counter, uint32_t* queue) {
+SST_D uint32_t warp_push(uint32_t value, uint32_t* counter, uint32_t* queue) {
     cg::coalesced_group g = cg::coalesced_threads();
     uint32_t base = 0;
     if (g.thread_rank() == 0) base = atomicAdd(counter, g.size());
     base = g.shfl(base, 0);
     queue[base + g.thread_rank()] = value;
+    return base + g.thread_rank();
+}
+
+// Queue record written after the block push (the position is known only then):
+// trace -- a = origin, b = direction, t = t_max, u = skip, v = (cull + 1) | inside << 8;
+// shadow -- a = point, b = direction, t = weight, u = obj | channel << 8.
+template <class R>
+struct WfRec {
+    V3<R> a, b;
+    R t;
+    int u;
+    uint32_t v;
+};
+
+template <class R>
+SST_D void put_trace(const WfPool<R>& q, uint32_t j, const WfRec<R>& r) {
+    q.tr_o[j] = Q4<R>{r.a.x, r.a.y, r.a.z, r.t};
+    q.tr_d[j] = Q4<R>{r.b.x, r.b.y, r.b.z, int_bits<R>(r.u)};
+    q.tr_f[j] = r.v;
+}
+
+template <class R>
+SST_D void put_shadow(const WfPool<R>& q, uint32_t j, const WfRec<R>& r) {
+    q.nee_p[j] = Q4<R>{r.a.x, r.a.y, r.a.z, r.t};
+    q.nee_w[j] = Q4<R>{r.b.x, r.b.y, r.b.z, int_bits<R>(r.u)};
 }
 
 enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3, kEmitFree = 4 };
@@ -207,7 +245,7 @@ enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3, kE
 // ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
 SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, LaneStats& st,
-                        bool* live) {
+                        bool* live, WfRec<R>& rec) {
     const DevScene<R>& sc = a.sc;
     PathLocal<R> p;
     uint32_t phase = meta_phase(q.meta[s].w);
@@ -253,14 +291,20 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
                 p.t_pend = t_free;
                 phase = kPhTrace;
                 emit = kEmitTrace;
+                rec.a = p.x;
+                rec.b = p.w;
+                rec.t = t_free;
+                rec.u = p.skip;
+                rec.v = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8);
                 break;
             }
             collide = true;  // the flight stays inside: collision without traversal
         } else if (phase == kPhTrace) {
             // ---- resolve (path_advance phase 2) with the traversal result
-            const uint2 hi = q.hinfo[s];
+            const uint32_t j = q.tq[s];  // this slot's position in the last trace queue
+            const uint2 hi = q.hinfo[j];
             const bool hit = (hi.y >> 31) != 0u;
-            const R t_hit = q.thit[s];
+            const R t_hit = q.thit[j];
             if (p.obj < 0) {
                 if (!hit) {
                     p.L += sc.bg[p.c];
@@ -321,8 +365,10 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
                     end = kEndAbsorbed;
                 } else {
                     if (a.nee) {  // NEE with the incoming direction (no draws)
-                        q.nee_p[s] = Q4<R>{p.x.x, p.x.y, p.x.z, R(1)};
-                        q.nee_w[s] = Q4<R>{p.w.x, p.w.y, p.w.z, R(0)};
+                        rec.a = p.x;
+                        rec.b = p.w;
+                        rec.t = R(1);
+                        rec.u = p.obj | (static_cast<int>(p.c) << 8);
                         emit = kEmitShadow;
                     }
                     const R u1 = p.rng.template uniform<R>();
@@ -357,13 +403,21 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
         const uint32_t i = base + threadIdx.x;
         int emit = kEmitNone;
         bool live = false;
+        WfRec<R> rec;
         const uint32_t s = i < n_in ? (q.q_in ? q.q_in[i] : i) : 0u;
-        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, st, &live);
+        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, st, &live, rec);
         const bool want[5] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitShadow, emit == kEmitFree};
         uint32_t* const ctr[5] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
                                   q.counts + kQShadow, q.counts + kQFree};
-        uint32_t* const qs[5] = {q.q_out, q.q_trace, q.q_sphere, q.q_shadow, q.q_free};
-        block_pushn<5>(want, s, ctr, qs);
+        uint32_t* const qs[5] = {q.q_out, nullptr, q.q_sphere, q.q_shadow, q.q_free};
+        uint32_t pos[5];
+        block_pushn<5>(want, s, ctr, qs, pos);
+        if (emit == kEmitTrace) {
+            put_trace(q, pos[1], rec);
+            q.tq[s] = pos[1];
+        } else if (emit == kEmitShadow) {
+            put_shadow(q, pos[3], rec);
+        }
     }
     flush_lane_stats(a.stats, st);
 }
@@ -384,16 +438,27 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
         const uint32_t i = b0 + threadIdx.x;
         const bool ok = i < n_new;
         const uint32_t s = ok ? q.q_free[i] : 0u;
+        WfRec<R> rec;
         if (ok) {
             PathLocal<R> p;
             path_init<R, EX>(a, base + i, p);
             p.t_pend = Real<R>::kInf;  // outside: the first flight is the camera ray
             store_slot(q, s, p, kPhTrace);
+            rec.a = p.x;
+            rec.b = p.w;
+            rec.t = Real<R>::kInf;
+            rec.u = -1;
+            rec.v = 0u;  // no cull, outside
         }
         const bool want[2] = {ok, ok};
         uint32_t* const ctr[2] = {q.counts + q.cnt_out, q.counts + kQTrace};
-        uint32_t* const qs[2] = {q.q_out, q.q_trace};
-        block_pushn<2>(want, s, ctr, qs);
+        uint32_t* const qs[2] = {q.q_out, nullptr};
+        uint32_t pos[2];
+        block_pushn<2>(want, s, ctr, qs, pos);
+        if (ok) {
+            put_trace(q, pos[1], rec);
+            q.tq[s] = pos[1];
+        }
     }
     __shared__ bool last;
     __syncthreads();
@@ -473,17 +538,16 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
             } else if (!have) {
                 const uint32_t i = base + __popc(idle & ((1u << lane) - 1u));
                 if (i < n) {
-                    s = q.q_trace[i];
-                    const Q4<R> xl = q.xl[s], wr = q.wr[s];
-                    const uint4 m = q.meta[s];
-                    const int obj = meta_obj(m.w);
-                    skip = static_cast<int>(m.z);
-                    cull = static_cast<int>((m.w >> 16) & 0xffu) - 1;
-                    const bool inside = obj >= 0;
-                    ray = make_ray(mk<R>(xl.x, xl.y, xl.z), mk<R>(wr.x, wr.y, wr.z));
+                    s = i;  // results go to the record's queue position
+                    const Q4<R> o = q.tr_o[i], d = q.tr_d[i];
+                    const uint32_t f = q.tr_f[i];
+                    skip = bits_int<R>(d.w);
+                    cull = static_cast<int>(f & 0xffu) - 1;
+                    const bool inside = (f >> 8) & 1u;
+                    ray = make_ray(mk<R>(o.x, o.y, o.z), mk<R>(d.x, d.y, d.z));
                     want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
                     t_min = skip >= 0 ? sc.surf_eps : sc.t_min;
-                    tr.init(inside ? q.tpend[s] : Real<R>::kInf);
+                    tr.init(o.w);
                     have = true;
                 }
             }
@@ -535,9 +599,9 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
             end = kEndAbsorbed;
         } else {
             if (a.nee) {
-                q.nee_p[s] = Q4<R>{o.rep_pos.x, o.rep_pos.y, o.rep_pos.z, o.lambda};
-                q.nee_w[s] = Q4<R>{o.rep_dir.x, o.rep_dir.y, o.rep_dir.z, R(0)};
-                warp_push(s, q.counts + kQShadow, q.q_shadow);
+                const uint32_t j = warp_push(s, q.counts + kQShadow, q.q_shadow);
+                q.nee_p[j] = Q4<R>{o.rep_pos.x, o.rep_pos.y, o.rep_pos.z, o.lambda};
+                q.nee_w[j] = Q4<R>{o.rep_dir.x, o.rep_dir.y, o.rep_dir.z, int_bits<R>(p.obj | (static_cast<int>(p.c) << 8))};
             }
             p.x = o.exit_pos;
             p.w = o.exit_dir;
@@ -565,12 +629,13 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
         if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
         if (i >= n) continue;
         const uint32_t s = q.q_shadow[i];
-        const uint32_t mw = q.meta[s].w;
-        const int obj = meta_obj(mw), c = meta_c(mw);
-        const Q4<R> np = q.nee_p[s], nw = q.nee_w[s];
+        const Q4<R> np = q.nee_p[i], nw = q.nee_w[i];
+        const R L0 = q.xl[s].w;  // issued early: the radiance update is the last use
+        const int oc = bits_int<R>(nw.w);
+        const int obj = oc & 0xff, c = oc >> 8;
         const R add = nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w,
                                tris);
-        q.xl[s].w += add;
+        q.xl[s].w = L0 + add;
         ++shadow;
     }
     unsigned long long v[kStCount] = {};
