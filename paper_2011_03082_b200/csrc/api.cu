@@ -141,10 +141,12 @@ struct sst_gpu_ctx {
 
     bool scene = false;
     uint64_t scene_bytes = 0, scene_bytes_grid = 0;
+    uint64_t grid_list_n = 0;  // light-grid list entries
     uint32_t n_nodes = 0, n_tris = 0;
     std::vector<ObjectHost> objects;
     sst_scene_desc desc{};
     DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri;
+    DevBuf grid_tris32;  // FP32 triangle records in light-grid list order (grid_tri gathered)
     uint32_t grid_res = 0;
     std::vector<DevBuf> sdf_dev, skip_dev;
     DevScene<float> sc32{};
@@ -430,6 +432,7 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     const bool use_grid = ctx->grid_res && !(no_grid && no_grid[0] == '1');
     sc.grid_off = use_grid ? ctx->grid_off.as<uint32_t>() : nullptr;
     sc.grid_tri = use_grid ? ctx->grid_tri.as<uint32_t>() : nullptr;
+    sc.grid_tris = use_grid && std::is_same<R, float>::value ? ctx->grid_tris32.p : nullptr;
     sc.grid_res = ctx->grid_res;
 }
 
@@ -440,7 +443,8 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
 void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
                       const std::vector<std::array<std::array<double, 3>, 3>>& tv, const FlatBvh& bvh) {
     const uint32_t n = bvh.n_tris;
-    const uint32_t res = n <= 4096 ? 128u : 256u;
+    uint32_t res = n <= 4096 ? 256u : 512u;
+    if (const char* e = std::getenv("SST_LIGHT_GRID_RES")) res = static_cast<uint32_t>(std::max(8, std::atoi(e)));
     const double pad = 2e-5;
     std::vector<double> caps(static_cast<size_t>(kCapStride) * n);
     for (uint32_t k = 0; k < n; ++k) {
@@ -518,6 +522,7 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
     ctx->scene_cache.grid_res = res;
     ctx->grid_res = res;
     ctx->scene_bytes_grid = offsets.size() * sizeof(uint32_t) + total * sizeof(uint32_t);
+    ctx->grid_list_n = total;
 }
 
 void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
@@ -624,6 +629,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
                                cudaMemcpyHostToDevice, ctx->stream));
         ctx->grid_res = sc.grid_res;
         ctx->scene_bytes_grid = (sc.grid_off.size() + sc.grid_tri.size()) * sizeof(uint32_t);
+        ctx->grid_list_n = sc.grid_tri.size();
     }
     const FlatBvh& bvh = ctx->scene_cache.bvh;
     lap(cached ? "bvh+grid(hit)" : "bvh+grid(build)");
@@ -660,6 +666,15 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     ctx->n_nodes = bvh.n_nodes;
     ctx->n_tris = bvh.n_tris;
     lap("copies queued");
+    {  // FP32 shadow rays read each light-grid cell's triangles contiguously (no index hop)
+        const uint64_t n_list = ctx->grid_res ? ctx->grid_list_n : 0;
+        ctx->grid_tris32.reserve(std::max<uint64_t>(n_list, 1) * sizeof(TriF));
+        if (n_list)
+            CK(launch_gather_tris(ctx->grid_tri.as<uint32_t>(), ctx->tris32.as<TriF>(), n_list,
+                                  ctx->grid_tris32.as<TriF>(), ctx->stream));
+        bytes += n_list * sizeof(TriF);
+        ctx->scene_bytes = bytes;
+    }
     fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
     fill_devscene<double>(ctx, ctx->sc64, ctx->nodes64, ctx->tris64, ctx->objs64);
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1185,7 +1200,7 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         auto it = g_const_owner.find(ctx->device);
         if (it != g_const_owner.end() && it->second.first == ctx) g_const_owner.erase(it);
     }
-    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri,
+    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri, &ctx->grid_tris32,
                       &ctx->radiance, &ctx->segments, &ctx->work, &ctx->stats, &ctx->error, &ctx->film_sum,
                       &ctx->film_sq, &ctx->keys_pix, &ctx->keys_smp, &ctx->keys_ch, &ctx->step_in, &ctx->step_out})
         b->release();

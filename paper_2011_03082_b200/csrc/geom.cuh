@@ -418,11 +418,12 @@ SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R
     const uint32_t b = __ldg(sc.grid_off + cell), e = __ldg(sc.grid_off + cell + 1);
     n_tris += e - b;
     R tau = R(0);
+    const bool direct = !Real<R>::kIsDouble && sc.grid_tris;  // cell's triangles stored contiguously
     for (uint32_t k = b; k < e; ++k) {
-        const uint32_t i = __ldg(sc.grid_tri + k);
+        const uint32_t i = direct ? k : __ldg(sc.grid_tri + k);
         V3<R> v0, e1, e2;
         uint32_t obj, id;
-        load_tri<R>(sc.tris, i, v0, e1, e2, obj, id);
+        load_tri<R>(direct ? sc.grid_tris : sc.tris, i, v0, e1, e2, obj, id);
         R det;
         const R t = ray_tri(ray, v0, e1, e2, t_min, t_max, &det);
         if (t >= R(0)) {

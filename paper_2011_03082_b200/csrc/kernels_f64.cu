@@ -271,7 +271,20 @@ __global__ void __launch_bounds__(128) k_light_grid(LightGridArgs a) {
     if (active && !a.fill) a.counts[cell] = count;
 }
 
+__global__ void k_gather_tris(const uint32_t* __restrict__ idx, const TriF* __restrict__ tris, uint64_t n,
+                              TriF* __restrict__ out) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[k] = tris[idx[k]];
+}
+
 }  // namespace
+
+cudaError_t launch_gather_tris(const uint32_t* idx, const TriF* tris, uint64_t n, TriF* out, cudaStream_t s) {
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_gather_tris<<<static_cast<unsigned>(blocks), 256, 0, s>>>(idx, tris, n, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_skip_build(const SkipBuildArgs& a, cudaStream_t s) {
     const uint64_t nvox = static_cast<uint64_t>(a.dims[0]) * a.dims[1] * a.dims[2];

@@ -98,7 +98,10 @@ template <bool EX>
 __global__ void __launch_bounds__(kWfBlock) k_wf_gen(TraceArgs<R> a) { wf_gen<R, EX>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock, SST_WF_TRACE_BLOCKS) k_wf_trace(TraceArgs<R> a) { wf_trace<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock, SST_WF_SPHERE_BLOCKS) k_wf_sphere(TraceArgs<R> a) { wf_sphere<R>(a, a.pool); }
-__global__ void __launch_bounds__(kWfBlock) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
+#ifndef SST_WF_SHADOW_BLOCKS
+#define SST_WF_SHADOW_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kWfBlock, SST_WF_SHADOW_BLOCKS) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_compact(TraceArgs<R> a) { wf_compact<R>(a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_init(TraceArgs<R> a) { wf_init<R>(a.pool); }
 __global__ void k_wf_reset(TraceArgs<R> a) { wf_reset<R>(a.pool); }

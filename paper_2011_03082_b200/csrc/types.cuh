@@ -85,6 +85,7 @@ struct DevScene {
     // footprint overlaps it: grid_tri[grid_off[c] .. grid_off[c+1]). Null = use the BVH.
     const uint32_t* grid_off;
     const uint32_t* grid_tri;
+    const void* grid_tris;  // FP32: TriF records in list order (grid_tri gathered); null in FP64
     uint32_t grid_res;
     uint32_t bvh_depth;  // FlatBvh::max_depth (traversal stack bound)
 };
