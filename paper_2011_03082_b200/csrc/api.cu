@@ -153,6 +153,10 @@ struct sst_gpu_ctx {
     DevScene<double> sc64{};
 
     DevBuf radiance, segments, work, stats, error, film_sum, film_sq, keys_pix, keys_smp, keys_ch;
+    // pinned staging for host-film readback (grow-only; cudaFreeHost on destroy)
+    double* film_pin = nullptr;
+    size_t film_pin_n = 0;
+    cudaEvent_t film_pin_ev[8] = {};
     DevBuf step_in, step_out;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -187,7 +191,7 @@ struct sst_gpu_ctx {
     // hand-off when live slots <= min(pool / 8, wf_tail), iterations per host check.
     int wavefront = 1;
     uint32_t wf_pool = 1u << 23;
-    uint32_t wf_tail = 1u << 17;
+    uint32_t wf_tail = 1u << 20;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
     std::deque<std::unique_ptr<WfJobBase>> jobs;  // FIFO: finishes (and films) in launch order
@@ -1036,6 +1040,9 @@ void collect_stats(sst_gpu_ctx* ctx, sst_path_stats* out) {
     CK(cudaMemsetAsync(ctx->stats.p, 0, kStCopies * kStCount * sizeof(unsigned long long), ctx->stream));
 }
 
+void readback_films(sst_gpu_ctx* ctx, const double* dsum, const double* dsq, uint64_t n, double* film_sum,
+                    double* film_sq);
+
 template <class R>
 void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, uint32_t s0, uint32_t s1,
                  uint64_t seed, double* film_sum, double* film_sq, int ptr_kind, sst_path_stats* stats) {
@@ -1095,17 +1102,58 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
     }
     if (!sync) return;  // asynchronous device-pointer call: sst_gpu_read_stats collects
     join_slots(ctx);
-    if (ptr_kind == SST_PTR_HOST) {
-        std::vector<double> hs(per_sample), hq(per_sample);
-        CK(cudaMemcpyAsync(hs.data(), dsum, per_sample * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(hq.data(), dsq, per_sample * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        for (uint64_t i = 0; i < per_sample; ++i) {
-            film_sum[i] += hs[i];
-            film_sq[i] += hq[i];
-        }
-    }
+    if (ptr_kind == SST_PTR_HOST) readback_films(ctx, dsum, dsq, per_sample, film_sum, film_sq);
     collect_stats(ctx, stats);
+}
+
+// Host films accumulate the call's device sums: the D2H copies go through a pinned
+// staging buffer in pieces, and each piece is added (by a few host threads) while the
+// next one is in flight.
+void readback_films(sst_gpu_ctx* ctx, const double* dsum, const double* dsq, uint64_t n, double* film_sum,
+                    double* film_sq) {
+    if (ctx->film_pin_n < 2 * n) {
+        if (ctx->film_pin) CK(cudaFreeHost(ctx->film_pin));
+        ctx->film_pin = nullptr;
+        ctx->film_pin_n = 0;
+        CK(cudaMallocHost(&ctx->film_pin, 2 * n * sizeof(double)));
+        ctx->film_pin_n = 2 * n;
+    }
+    if (!ctx->film_pin_ev[0])
+        for (auto& e : ctx->film_pin_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    constexpr int kPieces = 8;
+    const uint64_t piece = (n + kPieces - 1) / kPieces;
+    double* hs = ctx->film_pin;
+    double* hq = ctx->film_pin + n;
+    for (int k = 0; k < kPieces; ++k) {
+        const uint64_t b = std::min<uint64_t>(n, k * piece), e = std::min<uint64_t>(n, b + piece);
+        if (e > b) {
+            CK(cudaMemcpyAsync(hs + b, dsum + b, (e - b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(hq + b, dsq + b, (e - b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CK(cudaEventRecord(ctx->film_pin_ev[k], ctx->stream));
+    }
+    const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    for (int k = 0; k < kPieces; ++k) {
+        CK(cudaEventSynchronize(ctx->film_pin_ev[k]));
+        const uint64_t b = std::min<uint64_t>(n, k * piece), e = std::min<uint64_t>(n, b + piece);
+        auto add = [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t i = lo; i < hi; ++i) {
+                film_sum[i] += hs[i];
+                film_sq[i] += hq[i];
+            }
+        };
+        if (e - b < (1u << 16) || nt == 1) {
+            add(b, e);
+            continue;
+        }
+        std::vector<std::thread> th;
+        const uint64_t part = (e - b + nt - 1) / nt;
+        for (unsigned t = 0; t < nt; ++t) {
+            const uint64_t lo = b + std::min<uint64_t>(e - b, t * part), hi = b + std::min<uint64_t>(e - b, (t + 1) * part);
+            if (hi > lo) th.emplace_back(add, lo, hi);
+        }
+        for (auto& t : th) t.join();
+    }
 }
 
 template <class R>
@@ -1208,6 +1256,9 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
     for (auto& b : ctx->skip_dev) b.release();
     for (auto& e : ctx->kt_ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->film_pin_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->film_pin) cudaFreeHost(ctx->film_pin);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);

@@ -96,6 +96,39 @@ SST_D void set_phase(uint4* meta, uint32_t s, uint32_t phase) {
     meta[s].w = w;
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (no registers, no completion to wait
+// for): the pool's SoA streams are read a known distance ahead.
+SST_D void l2_prefetch(const void* p, size_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+    if (e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(e - a))
+                     : "memory");
+}
+
+// Records [j, j + n) of a trace / shadow queue (bounded by the queue length).
+#ifndef SST_WF_PREFETCH_AHEAD
+#define SST_WF_PREFETCH_AHEAD 32768
+#endif
+template <class R>
+SST_D void prefetch_trace(const WfPool<R>& q, uint32_t j, uint32_t n, uint32_t len) {
+    j += SST_WF_PREFETCH_AHEAD;
+    if (j >= len) return;
+    if (n > len - j) n = len - j;
+    l2_prefetch(q.tr_o + j, n * sizeof(Q4<R>));
+    l2_prefetch(q.tr_d + j, n * sizeof(Q4<R>));
+    l2_prefetch(q.tr_f + j, n * sizeof(uint32_t));
+}
+template <class R>
+SST_D void prefetch_shadow(const WfPool<R>& q, uint32_t j, uint32_t n, uint32_t len) {
+    j += SST_WF_PREFETCH_AHEAD;
+    if (j >= len) return;
+    if (n > len - j) n = len - j;
+    l2_prefetch(q.nee_p + j, n * sizeof(Q4<R>));
+    l2_prefetch(q.nee_w + j, n * sizeof(Q4<R>));
+    l2_prefetch(q.q_shadow + j, n * sizeof(uint32_t));
+}
+
 // Per-thread counters flushed once per thread block (warp sums -> shared -> one
 // atomic per counter per block, spread over kStCopies copies of the stats array).
 template <int N>
@@ -401,6 +434,17 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += stride) {  // block-uniform
         const uint32_t i = base + threadIdx.x;
+#ifndef SST_WF_NO_PREFETCH
+        if (!q.q_in && threadIdx.x == 0 && base + stride < n_in) {  // slot order: this block's next chunk
+            const uint32_t nb = base + stride, cnt = min(blockDim.x, n_in - nb);
+            l2_prefetch(q.meta + nb, cnt * sizeof(uint4));
+            l2_prefetch(q.xl + nb, cnt * sizeof(Q4<R>));
+            l2_prefetch(q.wr + nb, cnt * sizeof(Q4<R>));
+            l2_prefetch(q.rng + nb, cnt * sizeof(uint64_t));
+            l2_prefetch(q.tpend + nb, cnt * sizeof(R));
+            l2_prefetch(q.tq + nb, cnt * sizeof(uint32_t));
+        }
+#endif
         int emit = kEmitNone;
         bool live = false;
         WfRec<R> rec;
@@ -531,7 +575,12 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
         const unsigned idle = __ballot_sync(0xffffffffu, !have);
         if (!exhausted && (__popc(idle) >= kTraceRefill || idle == 0xffffffffu)) {
             uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(q.counts + kQFetchTrace, static_cast<uint32_t>(__popc(idle)));
+            if (lane == 0) {
+                base = atomicAdd(q.counts + kQFetchTrace, static_cast<uint32_t>(__popc(idle)));
+#ifndef SST_WF_NO_PREFETCH
+                prefetch_trace(q, base, static_cast<uint32_t>(__popc(idle)), n);
+#endif
+            }
             base = __shfl_sync(0xffffffffu, base, 0);
             if (base >= n) {
                 exhausted = true;
@@ -626,6 +675,9 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
     const uint32_t n = q.counts[kQShadow];
     for (;;) {
         const uint32_t i = warp_fetch(q.counts + kQFetchShadow);
+#ifndef SST_WF_NO_PREFETCH
+        if ((threadIdx.x & 31u) == 0) prefetch_shadow(q, i, 32u, n);
+#endif
         if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
         if (i >= n) continue;
         const uint32_t s = q.q_shadow[i];
