@@ -98,7 +98,12 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
         pixel = a.pixel[id];
         sample = a.sample[id];
         c = a.channel[id];
-    } else {  // id = (s_local * n_pix + pixel) * 3 + c
+    } else if (id <= 0xffffffffull) {  // id = (s_local * n_pix + pixel) * 3 + c (32-bit divisions)
+        const uint32_t id32 = static_cast<uint32_t>(id), rest = id32 / 3u;
+        c = id32 - 3u * rest;
+        pixel = rest % a.n_pix;
+        sample = a.sample_begin + rest / a.n_pix;
+    } else {
         c = static_cast<uint32_t>(id % 3);
         const uint64_t rest = id / 3;
         pixel = static_cast<uint32_t>(rest % a.n_pix);

@@ -467,42 +467,35 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
 }
 
 // ------------------------------------------------------------------ k_wf_gen
-// New paths into the free slots: entry i of the free queue gets path id work + i
-// (no per-path atomics), the camera ray is set up (path_init) and queued for its
-// first traversal. The last block to finish advances the path counter and empties
-// the free queue (slots left over once the ids run out stay empty).
+// New paths into the free slots: entry i of the free queue gets path id work + i, the
+// camera ray is set up (path_init) and queued for its first traversal at trace
+// position T + i and live-list position L + i (T, L = the logic pass's final counts):
+// every position is known up front, so there are no atomics and no barriers. The last
+// block to finish advances the path counter and the two queue counts and empties the
+// free queue (slots left over once the ids run out stay empty).
 template <class R, bool EX>
 SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     const uint32_t n_free = q.counts[kQFree];
     const uint64_t base = *a.work;
     const uint64_t left = base < a.n_paths ? a.n_paths - base : 0;
     const uint32_t n_new = static_cast<uint32_t>(left < n_free ? left : n_free);
+    const uint32_t t0 = q.counts[kQTrace], l0 = q.counts[q.cnt_out];
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n_new; b0 += stride) {  // block-uniform
-        const uint32_t i = b0 + threadIdx.x;
-        const bool ok = i < n_new;
-        const uint32_t s = ok ? q.q_free[i] : 0u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += stride) {
+        const uint32_t s = q.q_free[i];
+        PathLocal<R> p;
+        path_init<R, EX>(a, base + i, p);
+        p.t_pend = Real<R>::kInf;  // outside: the first flight is the camera ray
+        store_slot(q, s, p, kPhTrace);
         WfRec<R> rec;
-        if (ok) {
-            PathLocal<R> p;
-            path_init<R, EX>(a, base + i, p);
-            p.t_pend = Real<R>::kInf;  // outside: the first flight is the camera ray
-            store_slot(q, s, p, kPhTrace);
-            rec.a = p.x;
-            rec.b = p.w;
-            rec.t = Real<R>::kInf;
-            rec.u = -1;
-            rec.v = 0u;  // no cull, outside
-        }
-        const bool want[2] = {ok, ok};
-        uint32_t* const ctr[2] = {q.counts + q.cnt_out, q.counts + kQTrace};
-        uint32_t* const qs[2] = {q.q_out, nullptr};
-        uint32_t pos[2];
-        block_pushn<2>(want, s, ctr, qs, pos);
-        if (ok) {
-            put_trace(q, pos[1], rec);
-            q.tq[s] = pos[1];
-        }
+        rec.a = p.x;
+        rec.b = p.w;
+        rec.t = Real<R>::kInf;
+        rec.u = -1;
+        rec.v = 0u;  // no cull, outside
+        put_trace(q, t0 + i, rec);
+        q.tq[s] = t0 + i;
+        q.q_out[l0 + i] = s;
     }
     __shared__ bool last;
     __syncthreads();
@@ -513,6 +506,8 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     __syncthreads();
     if (last && threadIdx.x == 0) {
         *a.work = base + n_new;
+        q.counts[kQTrace] = t0 + n_new;
+        q.counts[q.cnt_out] = l0 + n_new;
         q.counts[kQFree] = 0u;
         q.counts[kQTicket] = 0u;
     }
