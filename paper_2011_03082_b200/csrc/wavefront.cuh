@@ -293,8 +293,39 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
         int end = -1;
         bool collide = false;
         R t_free = Real<R>::kInf;
-        if (phase == kPhFlight) {
-            // ---- flight start (path_advance phase 1)
+        if (phase == kPhTrace) {
+            // ---- resolve (path_advance phase 2) with the traversal result
+            const uint32_t j = q.tq[s];  // this slot's position in the last trace queue
+            const uint2 hi = q.hinfo[j];
+            const bool hit = (hi.y >> 31) != 0u;
+            const R t_hit = q.thit[j];
+            if (p.obj < 0) {
+                if (!hit) {
+                    p.L += sc.bg[p.c];
+                    end = kEndEscaped;
+                } else {  // medium entry (index-matched boundary)
+                    p.x = p.x + p.w * t_hit;
+                    p.obj = static_cast<int>(hi.y & 0x7fffffffu);
+                    p.cull = -1;
+                    p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
+                    p.r_valid = false;
+                    phase = kPhFlight;
+                }
+            } else if (hit) {  // leaves the medium
+                p.x = p.x + p.w * t_hit;
+                p.cull = sc.objs[p.obj].convex ? p.obj : -1;
+                p.obj = -1;
+                p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
+                phase = kPhFlight;
+            } else {
+                t_free = p.t_pend;
+                collide = true;
+            }
+        }
+        if (end < 0 && !collide && phase == kPhFlight) {
+            // ---- flight start (path_advance phase 1); a path that just crossed a
+            // boundary starts its next flight in the same pass as the others
+            // (one warp pass over resolve -> flight start -> collision)
             bool inside = p.obj >= 0;
             bool trace = true;
             if (inside) {
@@ -332,36 +363,6 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
                 break;
             }
             collide = true;  // the flight stays inside: collision without traversal
-        } else if (phase == kPhTrace) {
-            // ---- resolve (path_advance phase 2) with the traversal result
-            const uint32_t j = q.tq[s];  // this slot's position in the last trace queue
-            const uint2 hi = q.hinfo[j];
-            const bool hit = (hi.y >> 31) != 0u;
-            const R t_hit = q.thit[j];
-            if (p.obj < 0) {
-                if (!hit) {
-                    p.L += sc.bg[p.c];
-                    end = kEndEscaped;
-                } else {  // medium entry (index-matched boundary)
-                    p.x = p.x + p.w * t_hit;
-                    p.obj = static_cast<int>(hi.y & 0x7fffffffu);
-                    p.cull = -1;
-                    p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
-                    p.r_valid = false;
-                    phase = kPhFlight;
-                    continue;
-                }
-            } else if (hit) {  // leaves the medium
-                p.x = p.x + p.w * t_hit;
-                p.cull = sc.objs[p.obj].convex ? p.obj : -1;
-                p.obj = -1;
-                p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
-                phase = kPhFlight;
-                continue;
-            } else {
-                t_free = p.t_pend;
-                collide = true;
-            }
         }
         if (collide) {
             // ---- collision (path_advance phases 2-3)
