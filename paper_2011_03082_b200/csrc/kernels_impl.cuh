@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_M
 constexpr int kWfBlock = 256;
 // Minimum resident blocks per SM (register caps) of the wavefront kernels; tuning knobs.
 #ifndef SST_WF_LOGIC_BLOCKS
-#define SST_WF_LOGIC_BLOCKS 5
+#define SST_WF_LOGIC_BLOCKS 4
 #endif
 #ifndef SST_WF_TRACE_BLOCKS
 #define SST_WF_TRACE_BLOCKS 1

@@ -277,23 +277,30 @@ enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3, kE
 // traversal, a sphere step or a shadow ray (at most one per iteration), or its path
 // ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
-SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, LaneStats& st,
+SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, unsigned m, LaneStats& st,
                         bool* live, WfRec<R>& rec) {
+    // m: the lanes of this warp calling (converged). The loop below has no break /
+    // continue / return inside: every stage is an if-block that all lanes of the warp
+    // reach together, so lanes that got to a collision by different routes (after a
+    // traversal, or after a flight that needed none) run it in ONE warp pass.
     const DevScene<R>& sc = a.sc;
     PathLocal<R> p;
     uint32_t phase = meta_phase(q.meta[s].w);
     *live = false;
     ++st.wf_slots;
+    m = __ballot_sync(m, phase != kPhEmpty);
     if (phase == kPhEmpty) return kEmitNone;  // ended in k_wf_sphere (already on the free queue)
     load_slot(q, s, p, &phase);
     ++st.lane_iters;
     int emit = kEmitNone;
+    int end = -1;
+    bool run = true;
 #pragma unroll 1
     for (int guard = 0; guard < 8; ++guard) {
-        int end = -1;
+        if (!__any_sync(m, run)) break;
         bool collide = false;
         R t_free = Real<R>::kInf;
-        if (phase == kPhTrace) {
+        if (run && phase == kPhTrace) {
             // ---- resolve (path_advance phase 2) with the traversal result
             const uint32_t j = q.tq[s];  // this slot's position in the last trace queue
             const uint2 hi = q.hinfo[j];
@@ -322,10 +329,9 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
                 collide = true;
             }
         }
-        if (end < 0 && !collide && phase == kPhFlight) {
+        if (run && end < 0 && !collide && phase == kPhFlight) {
             // ---- flight start (path_advance phase 1); a path that just crossed a
             // boundary starts its next flight in the same pass as the others
-            // (one warp pass over resolve -> flight start -> collision)
             bool inside = p.obj >= 0;
             bool trace = true;
             if (inside) {
@@ -360,11 +366,13 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
                 rec.t = t_free;
                 rec.u = p.skip;
                 rec.v = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8);
-                break;
+                run = false;
+            } else {
+                collide = true;  // the flight stays inside: collision without traversal
             }
-            collide = true;  // the flight stays inside: collision without traversal
         }
-        if (collide) {
+        __syncwarp(m);
+        if (run && collide) {
             // ---- collision (path_advance phases 2-3)
             const ObjK<R>& ob = sc.objs[p.obj];
             p.skip = -1;
@@ -382,41 +390,44 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, L
                     const R v = sdf_raw(ob, p.x, &in_grid);
                     p.r_here = v < R(0) ? -v : R(0);
                     p.r_valid = true;
-                    if (leaked(ob, v, in_grid)) {
+                    if (leaked(ob, v, in_grid)) {  // not in the medium: next pass flies from here
                         recover_leak(p, ob);
                         event = false;
                     }
                     if (p.r_here > ob.med[p.c].r_min) {
                         phase = kPhSphere;
                         emit = kEmitSphere;
-                        break;
+                        run = false;
+                        event = false;
                     }
                 }
-                if (!event) continue;
-                ++st.events;
-                const MediumK<R>& m = ob.med[p.c];
-                if (!((p.rng.next() >> 11) < m.survive_below)) {  // u < phi, bit-exact
-                    end = kEndAbsorbed;
-                } else {
-                    if (a.nee) {  // NEE with the incoming direction (no draws)
-                        rec.a = p.x;
-                        rec.b = p.w;
-                        rec.t = R(1);
-                        rec.u = p.obj | (static_cast<int>(p.c) << 8);
-                        emit = kEmitShadow;
+                if (event) {
+                    ++st.events;
+                    const MediumK<R>& m = ob.med[p.c];
+                    if (!((p.rng.next() >> 11) < m.survive_below)) {  // u < phi, bit-exact
+                        end = kEndAbsorbed;
+                    } else {
+                        if (a.nee) {  // NEE with the incoming direction (no draws)
+                            rec.a = p.x;
+                            rec.b = p.w;
+                            rec.t = R(1);
+                            rec.u = p.obj | (static_cast<int>(p.c) << 8);
+                            emit = kEmitShadow;
+                        }
+                        const R u1 = p.rng.template uniform<R>();
+                        const R u2 = p.rng.template uniform<R>();
+                        p.w = hg_sample(m.g, p.w, u1, u2);
+                        run = false;  // one event per pass
                     }
-                    const R u1 = p.rng.template uniform<R>();
-                    const R u2 = p.rng.template uniform<R>();
-                    p.w = hg_sample(m.g, p.w, u1, u2);
-                    break;  // one event per iteration
                 }
             }
         }
-        if (end >= 0) {
-            finish_path(a, p, end, st);
-            q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
-            return kEmitFree;
-        }
+        if (end >= 0) run = false;
+    }
+    if (end >= 0) {
+        finish_path(a, p, end, st);
+        q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+        return kEmitFree;
     }
     store_slot(q, s, p, phase);
     *live = true;
@@ -450,7 +461,8 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
         bool live = false;
         WfRec<R> rec;
         const uint32_t s = i < n_in ? (q.q_in ? q.q_in[i] : i) : 0u;
-        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, st, &live, rec);
+        const unsigned m = __ballot_sync(0xffffffffu, i < n_in);
+        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, m, st, &live, rec);
         const bool want[5] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitShadow, emit == kEmitFree};
         uint32_t* const ctr[5] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
                                   q.counts + kQShadow, q.counts + kQFree};
