@@ -41,6 +41,9 @@ SST_D uint32_t pack_meta(int obj, int c, bool r_valid, uint32_t phase, int cull)
            (static_cast<uint32_t>(r_valid) << 10) | (phase << 11) | (static_cast<uint32_t>(cull + 1) << 16);
 }
 SST_D uint32_t meta_phase(uint32_t m) { return (m >> 11) & 3u; }
+// meta.w bit 13: a path fresh from the generation kernel whose position / direction
+// live only in its camera-ray trace record (xl / wr were not written; L = 0).
+constexpr uint32_t kMetaFresh = 1u << 13;
 // Integer payloads carried in the spare lane of a record vector.
 template <class R>
 SST_D R int_bits(int v) {
@@ -56,13 +59,22 @@ SST_D int meta_obj(uint32_t m) { return static_cast<int>(m & 0xffu) - 1; }
 SST_D int meta_c(uint32_t m) { return static_cast<int>((m >> 8) & 3u); }
 
 template <class R>
-SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase) {
+SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLocal<R>& p, uint32_t* phase) {
     const Q4<R> xl = q.xl[s], wr = q.wr[s];
-    const uint4 m = q.meta[s];
     p.x = mk<R>(xl.x, xl.y, xl.z);
     p.L = xl.w;
     p.w = mk<R>(wr.x, wr.y, wr.z);
     p.r_here = wr.w;
+    p.t_pend = q.tpend[s];
+    if (m.w & kMetaFresh) {  // camera ray: the state is in the trace record
+        const uint32_t j = q.tq[s];
+        const Q4<R> o = q.tr_o[j], d = q.tr_d[j];
+        p.x = mk<R>(o.x, o.y, o.z);
+        p.w = mk<R>(d.x, d.y, d.z);
+        p.L = R(0);
+        p.r_here = R(0);
+        p.t_pend = Real<R>::kInf;
+    }
     p.rng.s = q.rng[s];
     p.id = m.x;
     p.seg = m.y;
@@ -72,12 +84,16 @@ SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* 
     p.r_valid = (m.w >> 10) & 1u;
     *phase = meta_phase(m.w);
     p.cull = static_cast<int>((m.w >> 16) & 0xffu) - 1;
-    p.t_pend = q.tpend[s];
     p.pending = *phase == kPhSphere;
     p.tpend = *phase == kPhTrace;
     p.waited = 0;
     p.twaited = 0;
     p.pixel = 0;
+}
+
+template <class R>
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase) {
+    load_slot_from(q, s, q.meta[s], p, phase);
 }
 
 template <class R>
@@ -285,12 +301,22 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
     // traversal, or after a flight that needed none) run it in ONE warp pass.
     const DevScene<R>& sc = a.sc;
     PathLocal<R> p;
-    uint32_t phase = meta_phase(q.meta[s].w);
+    const uint4 mt = q.meta[s];
+    uint32_t phase = meta_phase(mt.w);
     *live = false;
     ++st.wf_slots;
     m = __ballot_sync(m, phase != kPhEmpty);
     if (phase == kPhEmpty) return kEmitNone;  // ended in k_wf_sphere (already on the free queue)
-    load_slot(q, s, p, &phase);
+    // the traversal result (and a fresh path's camera record) at the slot's trace-queue
+    // position, issued with the slot loads
+    uint2 hi = make_uint2(0u, 0u);
+    R t_hit = R(0);
+    if (phase == kPhTrace) {
+        const uint32_t j = q.tq[s];
+        hi = q.hinfo[j];
+        t_hit = q.thit[j];
+    }
+    load_slot_from(q, s, mt, p, &phase);
     ++st.lane_iters;
     int emit = kEmitNone;
     int end = -1;
@@ -302,10 +328,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
         R t_free = Real<R>::kInf;
         if (run && phase == kPhTrace) {
             // ---- resolve (path_advance phase 2) with the traversal result
-            const uint32_t j = q.tq[s];  // this slot's position in the last trace queue
-            const uint2 hi = q.hinfo[j];
             const bool hit = (hi.y >> 31) != 0u;
-            const R t_hit = q.thit[j];
             if (p.obj < 0) {
                 if (!hit) {
                     p.L += sc.bg[p.c];
@@ -498,8 +521,11 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
         const uint32_t s = q.q_free[i];
         PathLocal<R> p;
         path_init<R, EX>(a, base + i, p);
-        p.t_pend = Real<R>::kInf;  // outside: the first flight is the camera ray
-        store_slot(q, s, p, kPhTrace);
+        // only the id/flags and the RNG go to the slot (scattered stores); position and
+        // direction stay in the camera-ray record (kMetaFresh, load_slot)
+        q.rng[s] = p.rng.s;
+        q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), 0u, static_cast<uint32_t>(-1),
+                               pack_meta(-1, p.c, false, kPhTrace, -1) | kMetaFresh);
         WfRec<R> rec;
         rec.a = p.x;
         rec.b = p.w;
