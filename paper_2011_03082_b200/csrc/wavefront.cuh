@@ -516,6 +516,20 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     const uint64_t left = base < a.n_paths ? a.n_paths - base : 0;
     const uint32_t n_new = static_cast<uint32_t>(left < n_free ? left : n_free);
     const uint32_t t0 = q.counts[kQTrace], l0 = q.counts[q.cnt_out];
+    // The three channel paths of a (pixel, sample) share one camera ray (the camera
+    // stream is keyed by pixel and sample only): ids are consecutive, so entry i
+    // (channel c_i = id % 3) shares the record of entry max(i - c_i, 0), and only those
+    // owner entries are traced -- one traversal instead of three, identical results.
+    const uint32_t c0 = EX ? 0u : static_cast<uint32_t>(base % 3), k0 = (3u - c0) % 3u;
+    auto rank = [&](uint32_t i) -> uint32_t {  // trace position of owner entry i
+        if (EX) return i;
+        if (c0 == 0u) return i / 3u;
+        return i == 0u ? 0u : 1u + (i - k0) / 3u;
+    };
+    const uint32_t n_own = EX ? n_new
+                              : (n_new == 0u ? 0u
+                                             : (c0 == 0u ? (n_new + 2u) / 3u
+                                                         : 1u + (n_new > k0 ? (n_new - k0 + 2u) / 3u : 0u)));
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += stride) {
         const uint32_t s = q.q_free[i];
@@ -526,14 +540,19 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
         q.rng[s] = p.rng.s;
         q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), 0u, static_cast<uint32_t>(-1),
                                pack_meta(-1, p.c, false, kPhTrace, -1) | kMetaFresh);
-        WfRec<R> rec;
-        rec.a = p.x;
-        rec.b = p.w;
-        rec.t = Real<R>::kInf;
-        rec.u = -1;
-        rec.v = 0u;  // no cull, outside
-        put_trace(q, t0 + i, rec);
-        q.tq[s] = t0 + i;
+        const uint32_t ci = EX ? 0u : (c0 + i) % 3u;
+        const uint32_t owner = i >= ci ? i - ci : 0u;
+        const uint32_t j = t0 + rank(owner);
+        if (owner == i) {
+            WfRec<R> rec;
+            rec.a = p.x;
+            rec.b = p.w;
+            rec.t = Real<R>::kInf;
+            rec.u = -1;
+            rec.v = 0u;  // no cull, outside
+            put_trace(q, j, rec);
+        }
+        q.tq[s] = j;
         q.q_out[l0 + i] = s;
     }
     __shared__ bool last;
@@ -545,7 +564,7 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     __syncthreads();
     if (last && threadIdx.x == 0) {
         *a.work = base + n_new;
-        q.counts[kQTrace] = t0 + n_new;
+        q.counts[kQTrace] = t0 + n_own;
         q.counts[q.cnt_out] = l0 + n_new;
         q.counts[kQFree] = 0u;
         q.counts[kQTicket] = 0u;
