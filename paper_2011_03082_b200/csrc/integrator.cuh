@@ -57,7 +57,13 @@ SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<
     const R d = Real<R>::sqrt_(d2);
     const R inv_d = Real<R>::div_(R(1), d);  // FP64: IEEE 1/d (the reference divides; see below)
     const V3<R> wl = Real<R>::kIsDouble ? to_l / d : to_l * inv_d;
-    const RayK<R> ray = make_ray(p, wl);
+    RayK<R> ray;  // the light-grid path needs no slab reciprocals
+    if (sc.grid_off) {
+        ray.o = p;
+        ray.d = wl;
+    } else {
+        ray = make_ray(p, wl);
+    }
     const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c, tri_tests)
                               : optical_depth(sc, ray, sc.t_min, d, c);
     const R phase = hg_eval(m.g, dot(w, wl));
