@@ -81,16 +81,19 @@ __global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_M
 // ---------------------------------------------------------------------------
 // Wavefront integrator kernels (wavefront.cuh). Persistent grid-stride kernels sized
 // to the resident capacity (SM count x blocks per SM) so per-block stat flushes stay few.
-constexpr int kWfBlock = 256;
+#ifndef SST_WF_BLOCK
+#define SST_WF_BLOCK 128
+#endif
+constexpr int kWfBlock = SST_WF_BLOCK;
 // Minimum resident blocks per SM (register caps) of the wavefront kernels; tuning knobs.
 #ifndef SST_WF_LOGIC_BLOCKS
-#define SST_WF_LOGIC_BLOCKS 4
+#define SST_WF_LOGIC_BLOCKS 8
 #endif
 #ifndef SST_WF_TRACE_BLOCKS
 #define SST_WF_TRACE_BLOCKS 1
 #endif
 #ifndef SST_WF_SPHERE_BLOCKS
-#define SST_WF_SPHERE_BLOCKS 2
+#define SST_WF_SPHERE_BLOCKS 4
 #endif
 template <bool ST, bool EX>
 __global__ void __launch_bounds__(kWfBlock, SST_WF_LOGIC_BLOCKS) k_wf_logic(TraceArgs<R> a) { wf_logic<R, ST, EX>(a, a.pool); }
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(kWfBlock) k_wf_gen(TraceArgs<R> a) { wf_gen<R,
 __global__ void __launch_bounds__(kWfBlock, SST_WF_TRACE_BLOCKS) k_wf_trace(TraceArgs<R> a) { wf_trace<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock, SST_WF_SPHERE_BLOCKS) k_wf_sphere(TraceArgs<R> a) { wf_sphere<R>(a, a.pool); }
 #ifndef SST_WF_SHADOW_BLOCKS
-#define SST_WF_SHADOW_BLOCKS 5
+#define SST_WF_SHADOW_BLOCKS 10
 #endif
 __global__ void __launch_bounds__(kWfBlock, SST_WF_SHADOW_BLOCKS) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_compact(TraceArgs<R> a) { wf_compact<R>(a.pool); }
