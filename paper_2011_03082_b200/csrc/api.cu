@@ -184,6 +184,9 @@ struct sst_gpu_ctx {
         DevBuf wf;
         uint32_t* wf_host = nullptr;  // [2][kQCount]
         cudaEvent_t wf_ev[2] = {nullptr, nullptr};
+        // concurrent half of a wavefront iteration (sphere + shadow) and its fork/join
+        cudaStream_t side = nullptr;
+        cudaEvent_t wf_fork = nullptr, wf_join = nullptr;
     } slots[kSlots];
     // Wavefront integrator: SST_WAVEFRONT=0 megakernel only, 1 (default) wavefront for
     // the sphere tracer, 2 also for the delta-tracking path tracer (whose events are
@@ -194,6 +197,7 @@ struct sst_gpu_ctx {
     uint32_t wf_tail = 1u << 20;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
+    bool wf_concurrent = true;  // SST_WF_CONCURRENT=0: one stream per iteration
     std::deque<std::unique_ptr<WfJobBase>> jobs;  // FIFO: finishes (and films) in launch order
     // per-kernel device timing (sst_gpu_kernel_timing)
     bool ktime = false;
@@ -714,6 +718,17 @@ void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
 
 bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
 
+// Iteration `it` writes the record buffer it & 1 and reads fresh camera rays from the other.
+template <class R>
+void set_record_parity(WfPool<R>& q, uint64_t it) {
+    const int c = static_cast<int>(it & 1), p = c ^ 1;
+    q.tr_o = q.tr_buf[c][0];
+    q.tr_d = q.tr_buf[c][1];
+    q.tr_f = q.tr_fbuf[c];
+    q.tr_po = q.tr_buf[p][0];
+    q.tr_pd = q.tr_buf[p][1];
+}
+
 // Carves the wavefront pool of `cap` slots out of the slot's device buffer.
 template <class R>
 WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
@@ -721,8 +736,9 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
                             n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
                             kQCount * 4, 8, n * 4, n * 4, n * 4,
+                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4,
                             n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4};
-    size_t off[21], total = 0;
+    size_t off[24], total = 0;
     int k = 0;
     for (size_t b : sizes) {
         off[k++] = total;
@@ -750,9 +766,12 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.q_la = reinterpret_cast<uint32_t*>(base + off[15]);
     q.q_lb = reinterpret_cast<uint32_t*>(base + off[16]);
     q.q_free = reinterpret_cast<uint32_t*>(base + off[17]);
-    q.tr_o = reinterpret_cast<Q4<R>*>(base + off[18]);
-    q.tr_d = reinterpret_cast<Q4<R>*>(base + off[19]);
-    q.tr_f = reinterpret_cast<uint32_t*>(base + off[20]);
+    for (int k = 0; k < 2; ++k) {
+        q.tr_buf[k][0] = reinterpret_cast<Q4<R>*>(base + off[18 + 3 * k]);
+        q.tr_buf[k][1] = reinterpret_cast<Q4<R>*>(base + off[19 + 3 * k]);
+        q.tr_fbuf[k] = reinterpret_cast<uint32_t*>(base + off[20 + 3 * k]);
+    }
+    set_record_parity(q, 0);
     return q;
 }
 
@@ -787,14 +806,17 @@ struct WfJob final : WfJobBase {
             a.pool.q_out = even ? a.pool.q_lb : a.pool.q_la;
             a.pool.cnt_in = even ? kQLiveA : kQLiveB;
             a.pool.cnt_out = even ? kQLiveB : kQLiveA;
+            set_record_parity(a.pool, it);
             cudaEvent_t* ev = nullptr;
             if (ctx->ktime) {
                 if (!ctx->kt_ev[0])
                     for (auto& e : ctx->kt_ev) CK(cudaEventCreate(&e));
                 ev = ctx->kt_ev;
             }
-            if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_iteration(a, st, ex, stream, ev));
-            else CK(f64::launch_wf_iteration(a, st, ex, stream, ev));
+            cudaStream_t side = ctx->wf_concurrent ? sl->side : nullptr;
+            if constexpr (std::is_same<R, float>::value)
+                CK(f32::launch_wf_iteration(a, st, ex, stream, ev, side, sl->wf_fork, sl->wf_join));
+            else CK(f64::launch_wf_iteration(a, st, ex, stream, ev, side, sl->wf_fork, sl->wf_join));
             if (ev) {  // reset | logic | gen | trace | sphere | shadow
                 CK(cudaEventSynchronize(ev[6]));
                 static const int kinds[6] = {SST_KT_WF_RESET, SST_KT_WF_LOGIC, SST_KT_WF_GEN, SST_KT_WF_TRACE,
@@ -840,6 +862,7 @@ struct WfJob final : WfJobBase {
         }
         if (done) {
             if (!may_finish) return progressed ? 1 : 0;
+            set_record_parity(a.pool, it);  // fresh slots read the last iteration's records
             kt_begin(ctx, stream);
             if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, ex, stream));
             else CK(f64::launch_wf_finish(a, st, ex, stream));
@@ -1006,7 +1029,10 @@ void ensure_pipeline(sst_gpu_ctx* ctx) {
     if (ctx->ev_start) return;
     for (auto& sl : ctx->slots) {
         CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&sl.side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&sl.film_done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sl.wf_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sl.wf_join, cudaEventDisableTiming));
         sl.work.reserve(sizeof(unsigned long long));
     }
     CK(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
@@ -1229,6 +1255,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         if (const char* e = std::getenv("SST_WF_POOL")) ctx->wf_pool = static_cast<uint32_t>(std::max(32, std::atoi(e)));
         if (const char* e = std::getenv("SST_WF_TAIL")) ctx->wf_tail = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("SST_WF_BATCH")) ctx->wf_batch = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("SST_WF_CONCURRENT")) ctx->wf_concurrent = std::atoi(e) != 0;
         if (const char* e = std::getenv("SST_WF_CHUNK")) ctx->wf_chunk = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
         *out = ctx.release();
     });
@@ -1271,6 +1298,9 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         for (auto& e : sl.wf_ev)
             if (e) cudaEventDestroy(e);
         if (sl.film_done) cudaEventDestroy(sl.film_done);
+        if (sl.wf_fork) cudaEventDestroy(sl.wf_fork);
+        if (sl.wf_join) cudaEventDestroy(sl.wf_join);
+        if (sl.side) cudaStreamDestroy(sl.side);
         if (sl.s) cudaStreamDestroy(sl.s);
     }
     cudaStreamDestroy(ctx->stream);

@@ -195,8 +195,11 @@ cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {
 }
 
 // One wavefront iteration (a.pool.q_in/q_out set by the caller; queue counters cleared first).
+// side != null (and no per-kernel timing): after the logic pass the iteration forks --
+// generation + trace on s, sphere steps + shadow rays on `side` (they touch disjoint
+// slots, records and counters; see wavefront.cuh) -- and joins before the next one.
 cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s,
-                                cudaEvent_t* ev) {
+                                cudaEvent_t* ev, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
     static unsigned g_logic[2][2] = {}, g_gen[2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
     static uint32_t cap_seen = 0, depth_seen = 0;
     const size_t trace_smem = wf_trace_smem<R>(a.sc.bvh_depth, kWfBlock);
@@ -230,11 +233,27 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
         else k_wf_logic<false, false><<<gl, kWfBlock, 0, s>>>(a);
     }
     mark(2);
+    const bool concurrent = side && !ev && (st || a.nee);
+    cudaStream_t s2 = s;
+    if (concurrent) {
+        cudaEventRecord(fork, s);
+        cudaStreamWaitEvent(side, fork, 0);
+        s2 = side;
+    }
+    if (concurrent) {  // sphere + shadow first on the side stream
+        if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s2>>>(a);
+        if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s2>>>(a);
+    }
     if (explicit_keys) k_wf_gen<true><<<g_gen[1], kWfBlock, 0, s>>>(a);
     else k_wf_gen<false><<<g_gen[0], kWfBlock, 0, s>>>(a);
     mark(3);
     k_wf_trace<<<g_trace, kWfBlock, trace_smem, s>>>(a);
     mark(4);
+    if (concurrent) {
+        cudaEventRecord(join, side);
+        cudaStreamWaitEvent(s, join, 0);
+        return cudaGetLastError();
+    }
     if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s>>>(a);
     mark(5);
     if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s>>>(a);

@@ -145,6 +145,13 @@ struct WfPool {
     Q4<R>* tr_o;      // origin, t_max
     Q4<R>* tr_d;      // direction, skip triangle (int bits)
     uint32_t* tr_f;   // (cull + 1) | inside << 8
+    // The previous iteration's trace records (the record buffers alternate between
+    // iterations): a fresh path's camera ray is read from there by the next logic pass
+    // while that pass writes this iteration's records.
+    const Q4<R>* tr_po;
+    const Q4<R>* tr_pd;
+    Q4<R>* tr_buf[2][2];   // [parity][origin, direction]
+    uint32_t* tr_fbuf[2];  // [parity]
     R* thit;          // traversal result: distance
     uint2* hinfo;     // traversal result: triangle, object | found << 31
     // Shadow queue records (indexed by queue position): slot in q_shadow.

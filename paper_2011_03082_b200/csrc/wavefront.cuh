@@ -68,7 +68,7 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
     p.t_pend = q.tpend[s];
     if (m.w & kMetaFresh) {  // camera ray: the state is in the trace record
         const uint32_t j = q.tq[s];
-        const Q4<R> o = q.tr_o[j], d = q.tr_d[j];
+        const Q4<R> o = q.tr_po[j], d = q.tr_pd[j];
         p.x = mk<R>(o.x, o.y, o.z);
         p.w = mk<R>(d.x, d.y, d.z);
         p.L = R(0);
@@ -306,7 +306,9 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
     *live = false;
     ++st.wf_slots;
     m = __ballot_sync(m, phase != kPhEmpty);
-    if (phase == kPhEmpty) return kEmitNone;  // ended in k_wf_sphere (already on the free queue)
+    // ended in k_wf_sphere (which runs concurrently with the generation kernel and so
+    // does not touch the free queue): free it now if new paths remain
+    if (phase == kPhEmpty) return *a.work < a.n_paths ? kEmitFree : kEmitNone;
     // the traversal result (and a fresh path's camera record) at the slot's trace-queue
     // position, issued with the slot loads
     uint2 hi = make_uint2(0u, 0u);
@@ -571,14 +573,12 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     }
 }
 
-// Pool start: every slot empty and on the free queue.
+// Pool start: every slot empty (the first logic pass puts them on the free queue).
 template <class R>
 SST_D void wf_init(const WfPool<R>& q) {
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < q.cap; s += gridDim.x * blockDim.x) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < q.cap; s += gridDim.x * blockDim.x)
         q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
-        q.q_free[s] = s;
-    }
-    if (blockIdx.x == 0 && threadIdx.x < kQCount) q.counts[threadIdx.x] = threadIdx.x == kQFree ? q.cap : 0u;
+    if (blockIdx.x == 0 && threadIdx.x < kQCount) q.counts[threadIdx.x] = 0u;
 }
 
 // Iteration start: queue lengths and the output live count to zero.
@@ -709,10 +709,9 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
             p.w = o.exit_dir;
             p.r_valid = false;
         }
-        if (end >= 0) {
+        if (end >= 0) {  // the slot goes back to the free queue in the next logic pass
             finish_path(a, p, end, st);
             q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
-            warp_push(s, q.counts + kQFree, q.q_free);
         } else {
             store_slot(q, s, p, kPhFlight);
         }
