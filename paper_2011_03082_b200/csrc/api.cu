@@ -718,17 +718,6 @@ void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
 
 bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
 
-// Iteration `it` writes the record buffer it & 1 and reads fresh camera rays from the other.
-template <class R>
-void set_record_parity(WfPool<R>& q, uint64_t it) {
-    const int c = static_cast<int>(it & 1), p = c ^ 1;
-    q.tr_o = q.tr_buf[c][0];
-    q.tr_d = q.tr_buf[c][1];
-    q.tr_f = q.tr_fbuf[c];
-    q.tr_po = q.tr_buf[p][0];
-    q.tr_pd = q.tr_buf[p][1];
-}
-
 // Carves the wavefront pool of `cap` slots out of the slot's device buffer.
 template <class R>
 WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
@@ -736,9 +725,8 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
                             n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
                             kQCount * 4, 8, n * 4, n * 4, n * 4,
-                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4,
-                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4};
-    size_t off[24], total = 0;
+                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>)};
+    size_t off[22], total = 0;
     int k = 0;
     for (size_t b : sizes) {
         off[k++] = total;
@@ -766,12 +754,10 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.q_la = reinterpret_cast<uint32_t*>(base + off[15]);
     q.q_lb = reinterpret_cast<uint32_t*>(base + off[16]);
     q.q_free = reinterpret_cast<uint32_t*>(base + off[17]);
-    for (int k = 0; k < 2; ++k) {
-        q.tr_buf[k][0] = reinterpret_cast<Q4<R>*>(base + off[18 + 3 * k]);
-        q.tr_buf[k][1] = reinterpret_cast<Q4<R>*>(base + off[19 + 3 * k]);
-        q.tr_fbuf[k] = reinterpret_cast<uint32_t*>(base + off[20 + 3 * k]);
-    }
-    set_record_parity(q, 0);
+    q.tr_o = reinterpret_cast<Q4<R>*>(base + off[18]);
+    q.tr_d = reinterpret_cast<Q4<R>*>(base + off[19]);
+    q.tr_f = reinterpret_cast<uint32_t*>(base + off[20]);
+    q.tr_cam = reinterpret_cast<Q4<R>*>(base + off[21]);
     return q;
 }
 
@@ -806,7 +792,6 @@ struct WfJob final : WfJobBase {
             a.pool.q_out = even ? a.pool.q_lb : a.pool.q_la;
             a.pool.cnt_in = even ? kQLiveA : kQLiveB;
             a.pool.cnt_out = even ? kQLiveB : kQLiveA;
-            set_record_parity(a.pool, it);
             cudaEvent_t* ev = nullptr;
             if (ctx->ktime) {
                 if (!ctx->kt_ev[0])
@@ -862,7 +847,6 @@ struct WfJob final : WfJobBase {
         }
         if (done) {
             if (!may_finish) return progressed ? 1 : 0;
-            set_record_parity(a.pool, it);  // fresh slots read the last iteration's records
             kt_begin(ctx, stream);
             if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, ex, stream));
             else CK(f64::launch_wf_finish(a, st, ex, stream));

@@ -379,7 +379,7 @@ SST_D T warp_sum(T v) {
 
 // Wavefront slot -> path state (wavefront.cuh).
 template <class R>
-SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase);
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam);
 
 template <class R, bool ST, bool EXPLICIT>
 SST_D void trace_persistent(const TraceArgs<R>& a) {
@@ -399,7 +399,7 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
                 if (a.resume) {  // hand-off of the wavefront pool's live slots
                     if (my < a.pool.counts[kQResume]) {
                         uint32_t phase;
-                        load_slot(a.pool, a.pool.q_live[my], p, &phase);
+                        load_slot(a.pool, a.pool.q_live[my], p, &phase, a.sc.cam_pos);
                         alive = true;
                     } else {
                         exhausted = true;

@@ -144,14 +144,10 @@ struct WfPool {
     // traversal results at the same positions (read by the next logic pass).
     Q4<R>* tr_o;      // origin, t_max
     Q4<R>* tr_d;      // direction, skip triangle (int bits)
-    uint32_t* tr_f;   // (cull + 1) | inside << 8
-    // The previous iteration's trace records (the record buffers alternate between
-    // iterations): a fresh path's camera ray is read from there by the next logic pass
-    // while that pass writes this iteration's records.
-    const Q4<R>* tr_po;
-    const Q4<R>* tr_pd;
-    Q4<R>* tr_buf[2][2];   // [parity][origin, direction]
-    uint32_t* tr_fbuf[2];  // [parity]
+    uint32_t* tr_f;   // (cull + 1) | inside << 8 | camera ray << 9
+    // Direction of a camera ray, copied by the trace kernel next to its result (a fresh
+    // path reads it there in the next logic pass, which overwrites the records).
+    Q4<R>* tr_cam;
     R* thit;          // traversal result: distance
     uint2* hinfo;     // traversal result: triangle, object | found << 31
     // Shadow queue records (indexed by queue position): slot in q_shadow.

@@ -59,7 +59,8 @@ SST_D int meta_obj(uint32_t m) { return static_cast<int>(m & 0xffu) - 1; }
 SST_D int meta_c(uint32_t m) { return static_cast<int>((m >> 8) & 3u); }
 
 template <class R>
-SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLocal<R>& p, uint32_t* phase) {
+SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLocal<R>& p, uint32_t* phase,
+                          const V3<R>& sc_cam_pos) {
     const Q4<R> xl = q.xl[s], wr = q.wr[s];
     p.x = mk<R>(xl.x, xl.y, xl.z);
     p.L = xl.w;
@@ -68,8 +69,8 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
     p.t_pend = q.tpend[s];
     if (m.w & kMetaFresh) {  // camera ray: the state is in the trace record
         const uint32_t j = q.tq[s];
-        const Q4<R> o = q.tr_po[j], d = q.tr_pd[j];
-        p.x = mk<R>(o.x, o.y, o.z);
+        const Q4<R> d = q.tr_cam[j];
+        p.x = sc_cam_pos;
         p.w = mk<R>(d.x, d.y, d.z);
         p.L = R(0);
         p.r_here = R(0);
@@ -92,8 +93,8 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
 }
 
 template <class R>
-SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase) {
-    load_slot_from(q, s, q.meta[s], p, phase);
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam) {
+    load_slot_from(q, s, q.meta[s], p, phase, cam);
 }
 
 template <class R>
@@ -318,7 +319,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
         hi = q.hinfo[j];
         t_hit = q.thit[j];
     }
-    load_slot_from(q, s, mt, p, &phase);
+    load_slot_from(q, s, mt, p, &phase, sc.cam_pos);
     ++st.lane_iters;
     int emit = kEmitNone;
     int end = -1;
@@ -551,7 +552,7 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
             rec.b = p.w;
             rec.t = Real<R>::kInf;
             rec.u = -1;
-            rec.v = 0u;  // no cull, outside
+            rec.v = 1u << 9;  // no cull, outside, camera ray
             put_trace(q, j, rec);
         }
         q.tq[s] = j;
@@ -619,6 +620,7 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
     bool have = false, exhausted = false;
     uint32_t s = 0;
     int skip = -1, cull = -1, want = 0;
+    bool cam = false;  // camera ray: its direction is copied next to the result
     R t_min = R(0);
     RayK<R> ray;
     Trav<R> tr;
@@ -646,6 +648,7 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
                     skip = bits_int<R>(d.w);
                     cull = static_cast<int>(f & 0xffu) - 1;
                     const bool inside = (f >> 8) & 1u;
+                    cam = (f >> 9) & 1u;
                     ray = make_ray(mk<R>(o.x, o.y, o.z), mk<R>(d.x, d.y, d.z));
                     want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
                     t_min = skip >= 0 ? sc.surf_eps : sc.t_min;
@@ -661,6 +664,7 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
         if (have) {
             tr.round(sc, ray, t_min, skip, cull, want, nodes, tris, stk);
             if (tr.done()) {
+                if (cam) q.tr_cam[s] = Q4<R>{ray.d.x, ray.d.y, ray.d.z, R(0)};
                 q.thit[s] = tr.t_best;
                 q.hinfo[s] = make_uint2(tr.found ? tr.hit.tri : 0u,
                                         (tr.found ? tr.hit.obj : 0u) | (tr.found ? 0x80000000u : 0u));
@@ -689,7 +693,7 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
         const uint32_t s = q.q_sphere[i];
         PathLocal<R> p;
         uint32_t phase;
-        load_slot(q, s, p, &phase);
+        load_slot(q, s, p, &phase, sc.cam_pos);
         ++st.sphere;
         StepOut<R> o;
         const MediumK<R>& m = sc.objs[p.obj].med[p.c];
