@@ -777,6 +777,7 @@ struct WfJob final : WfJobBase {
     int batch = 1;
     uint64_t it = 0, k = 0, nread = 0;  // iterations and batches launched, batches read
     bool full = true;                   // pool full (path supply left): logic walks all slots in order
+    uint32_t live_hint = 0;             // last live count read while draining (upper bound)
     bool supply = false, done = false;
     int out_last[2] = {kQLiveA, kQLiveA};
     std::function<void()> on_finish;
@@ -799,9 +800,10 @@ struct WfJob final : WfJobBase {
                 ev = ctx->kt_ev;
             }
             cudaStream_t side = ctx->wf_concurrent ? sl->side : nullptr;
+            const uint32_t hint = full ? cap : live_hint;
             if constexpr (std::is_same<R, float>::value)
-                CK(f32::launch_wf_iteration(a, st, ex, stream, ev, side, sl->wf_fork, sl->wf_join));
-            else CK(f64::launch_wf_iteration(a, st, ex, stream, ev, side, sl->wf_fork, sl->wf_join));
+                CK(f32::launch_wf_iteration(a, st, ex, stream, ev, side, sl->wf_fork, sl->wf_join, hint));
+            else CK(f64::launch_wf_iteration(a, st, ex, stream, ev, side, sl->wf_fork, sl->wf_join, hint));
             if (ev) {  // reset | logic | gen | trace | sphere | shadow
                 CK(cudaEventSynchronize(ev[6]));
                 static const int kinds[6] = {SST_KT_WF_RESET, SST_KT_WF_LOGIC, SST_KT_WF_GEN, SST_KT_WF_TRACE,
@@ -843,6 +845,7 @@ struct WfJob final : WfJobBase {
             // generation refills every free slot while ids remain: live < cap means the
             // supply is exhausted (the pool drains from here)
             if (live < cap) full = false, supply = true;
+            live_hint = live;
             if (live <= thresh) done = true;
         }
         if (done) {

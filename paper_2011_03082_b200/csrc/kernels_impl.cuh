@@ -198,8 +198,12 @@ cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {
 // side != null (and no per-kernel timing): after the logic pass the iteration forks --
 // generation + trace on s, sphere steps + shadow rays on `side` (they touch disjoint
 // slots, records and counters; see wavefront.cuh) -- and joins before the next one.
+// live_hint: an upper bound on the live slots (the pool size while it is full; during
+// the drain the last live count the host read): grids shrink with the drain, so the
+// late iterations do not pay for scheduling thousands of idle blocks.
 cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_keys, cudaStream_t s,
-                                cudaEvent_t* ev, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+                                cudaEvent_t* ev, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join,
+                                uint32_t live_hint) {
     static unsigned g_logic[2][2] = {}, g_gen[2] = {}, g_trace = 0, g_sphere = 0, g_shadow = 0;
     static uint32_t cap_seen = 0, depth_seen = 0;
     const size_t trace_smem = wf_trace_smem<R>(a.sc.bvh_depth, kWfBlock);
@@ -224,7 +228,12 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
     mark(0);
     k_wf_reset<<<1, 32, 0, s>>>(a);
     mark(1);
-    const unsigned gl = g_logic[st][explicit_keys];
+    const unsigned need = static_cast<unsigned>((static_cast<uint64_t>(live_hint) + kWfBlock - 1) / kWfBlock);
+    auto fit = [need](unsigned g) { return need < g ? (need > 0 ? need : 1u) : g; };
+    const bool draining = live_hint < a.pool.cap;  // supply exhausted: nothing to generate
+    const unsigned gl = fit(g_logic[st][explicit_keys]);
+    const unsigned gs = fit(g_sphere), gh = fit(g_shadow), gt = fit(g_trace);
+    const unsigned gg0 = draining ? 1u : g_gen[0], gg1 = draining ? 1u : g_gen[1];
     if (st) {
         if (explicit_keys) k_wf_logic<true, true><<<gl, kWfBlock, 0, s>>>(a);
         else k_wf_logic<true, false><<<gl, kWfBlock, 0, s>>>(a);
@@ -241,22 +250,22 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
         s2 = side;
     }
     if (concurrent) {  // sphere + shadow first on the side stream
-        if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s2>>>(a);
-        if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s2>>>(a);
+        if (st) k_wf_sphere<<<gs, kWfBlock, 0, s2>>>(a);
+        if (a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s2>>>(a);
     }
-    if (explicit_keys) k_wf_gen<true><<<g_gen[1], kWfBlock, 0, s>>>(a);
-    else k_wf_gen<false><<<g_gen[0], kWfBlock, 0, s>>>(a);
+    if (explicit_keys) k_wf_gen<true><<<gg1, kWfBlock, 0, s>>>(a);
+    else k_wf_gen<false><<<gg0, kWfBlock, 0, s>>>(a);
     mark(3);
-    k_wf_trace<<<g_trace, kWfBlock, trace_smem, s>>>(a);
+    k_wf_trace<<<gt, kWfBlock, trace_smem, s>>>(a);
     mark(4);
     if (concurrent) {
         cudaEventRecord(join, side);
         cudaStreamWaitEvent(s, join, 0);
         return cudaGetLastError();
     }
-    if (st) k_wf_sphere<<<g_sphere, kWfBlock, 0, s>>>(a);
+    if (st) k_wf_sphere<<<gs, kWfBlock, 0, s>>>(a);
     mark(5);
-    if (a.nee) k_wf_shadow<<<g_shadow, kWfBlock, 0, s>>>(a);
+    if (a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s>>>(a);
     mark(6);
     return cudaGetLastError();
 }

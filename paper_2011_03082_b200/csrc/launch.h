@@ -18,7 +18,7 @@ constexpr int kTraceBlock = 32;  // one warp per block: a long-path tail strands
     cudaError_t launch_wf_init(const TraceArgs<REAL>& a, cudaStream_t s);                       \
     cudaError_t launch_wf_iteration(const TraceArgs<REAL>& a, bool st, bool explicit_keys,      \
                                     cudaStream_t s, cudaEvent_t* ev, cudaStream_t side,         \
-                                    cudaEvent_t fork, cudaEvent_t join);                        \
+                                    cudaEvent_t fork, cudaEvent_t join, uint32_t live_hint);    \
     cudaError_t launch_wf_finish(const TraceArgs<REAL>& a, bool st, bool explicit_keys,         \
                                  cudaStream_t s);                                               \
     cudaError_t launch_film(const REAL* radiance, uint64_t stride, uint32_t n_samples,          \
