@@ -188,11 +188,12 @@ struct sst_gpu_ctx {
         cudaStream_t side = nullptr;
         cudaEvent_t wf_fork = nullptr, wf_join = nullptr;
     } slots[kSlots];
-    // Wavefront integrator: SST_WAVEFRONT=0 megakernel only, 1 (default) wavefront for
-    // the sphere tracer, 2 also for the delta-tracking path tracer (whose events are
-    // cheap and whose long paths favour the register-resident megakernel). Pool slots per launch,
-    // hand-off when live slots <= min(pool / 8, wf_tail), iterations per host check.
-    int wavefront = 1;
+    // Wavefront integrator: SST_WAVEFRONT=0 megakernel only, 1 wavefront for the sphere
+    // tracer only, 2 (default) also for the delta-tracking path tracer (C5 PT+NEE 1.42x,
+    // C3 sigma_t=160 1.44x the megakernel since the session-3 wavefront work; the long-path
+    // tail still goes to the megakernel). Pool slots per launch, hand-off when live slots
+    // <= min(pool / 8, wf_tail), iterations per host check.
+    int wavefront = 2;
     uint32_t wf_pool = 1u << 23;
     uint32_t wf_tail = 1u << 20;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
