@@ -48,14 +48,27 @@ def mlp_flops(dl, dp, de):
 # Algorithmic per-unit work of each wavefront kernel (counted from the
 # device counters of the measured slab):
 #   wf_logic  HBM: per slot visit the path state it must read (x,L 16 + w,r 16 + rng 8 +
-#             meta 16 + flight 4 + hit 12 = 72 B) and write back (60 B) + 2 queue
-#             entries (8 B); per delta-tracking event a 32 B NEE record.
+#             meta 16 + flight 4 + trace position 4 = 64 B), write back (60 B) and its
+#             live-list entry (4 B); per flight it sends to the trace kernel the 36 B ray
+#             record + trace position (4 B) + the 12 B result it reads back next pass
+#             (traversals minus the one shared camera ray per pixel-sample); per fresh path
+#             the camera-ray result and direction (28 B); per delta-tracking event its NEE
+#             record + queue entry (36 B); per sphere request a queue entry (4 B).
 #   wf_trace  FP32: per interior node 2 slab tests = 12 FFMA + 12 min/max = 36 FLOP;
 #             per Moller-Trumbore test 51 FLOP (2 cross, 4 dot, rcp, 3 mul, 3 sub).
 #   wf_shadow FP32: 51 FLOP per light-grid triangle test.
 #   wf_sphere FP32: decoder MLP FLOPs 2*(112 nL + 480 nP + 640 nE).
 NODE_FLOP, TRI_FLOP = 36.0, 51.0
-LOGIC_BYTES_PER_SLOT, NEE_RECORD_BYTES = 140.0, 32.0
+LOGIC_BYTES_PER_SLOT, LOGIC_BYTES_PER_FLIGHT, LOGIC_BYTES_PER_FRESH = 128.0, 52.0, 28.0
+NEE_RECORD_BYTES, SPHERE_QUEUE_BYTES = 36.0, 4.0
+
+
+def logic_bytes(k):
+    """Algorithmic HBM bytes of the logic kernel over a measured slab (device counters)."""
+    flights = max(0.0, float(k.traversals) - float(k.paths) / 3.0)
+    return (LOGIC_BYTES_PER_SLOT * k.wavefront_slot_visits + LOGIC_BYTES_PER_FLIGHT * flights
+            + LOGIC_BYTES_PER_FRESH * k.paths + NEE_RECORD_BYTES * k.pt_events
+            + SPHERE_QUEUE_BYTES * k.sphere_steps)
 
 
 class ClockSampler:
@@ -306,7 +319,7 @@ def bench_ours(args, world, rank, local):
     kt = r.kernel_timing(False)
     tri_trace = kst.triangle_tests - kst.shadow_triangle_tests
     kdef = {
-        "wf_logic": ("hbm", (LOGIC_BYTES_PER_SLOT * kst.wavefront_slot_visits + NEE_RECORD_BYTES * kst.pt_events) / 1e9,
+        "wf_logic": ("hbm", logic_bytes(kst) / 1e9,
                      hbm_peak, "GB/s"),
         "wf_trace": ("fp32", (NODE_FLOP * kst.node_visits + TRI_FLOP * tri_trace) / 1e12, fp32_peak, "TFLOP/s"),
         "wf_shadow": ("fp32", TRI_FLOP * kst.shadow_triangle_tests / 1e12, fp32_peak, "TFLOP/s"),
