@@ -392,6 +392,12 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
         ok[o].skip_unit = static_cast<R>(oh.skip_unit);
         for (int a = 0; a < 3; ++a) ok[o].skip_dims[a] = oh.skip_dims[a];
         ok[o].convex = oh.convex ? 1u : 0u;
+        {
+            const auto& roots = ctx->scene_cache.bvh.obj_root;
+            const char* e = std::getenv("SST_OBJ_ROOT");
+            const bool use = std::is_same<R, float>::value && !(e && e[0] == '0');
+            ok[o].bvh_root = use && o < roots.size() && roots[o] >= 0 ? roots[o] : 0;
+        }
     }
     objs.reserve(ok.size() * sizeof(ObjK<R>));
     CK(cudaMemcpyAsync(objs.p, ok.data(), ok.size() * sizeof(ObjK<R>), cudaMemcpyHostToDevice, ctx->stream));

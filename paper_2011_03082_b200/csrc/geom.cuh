@@ -321,9 +321,9 @@ struct Trav {
 template <class R, class Stack>
 SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
                                int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
-                               uint64_t& n_tris, Stack& stk) {
+                               uint64_t& n_tris, Stack& stk, int root = 0) {
     Trav<R> tr;
-    tr.init(t_max);
+    tr.init(t_max, root);
     while (!tr.done()) tr.round(sc, ray, t_min, skip, cull_obj, want_sign, n_nodes, n_tris, stk);
     *t_hit = tr.t_best;
     if (tr.found) *hit = tr.hit;
@@ -333,9 +333,10 @@ SST_D bool intersect_nearest_s(const DevScene<R>& sc, const RayK<R>& ray, R t_mi
 template <class R>
 SST_D bool intersect_nearest(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int skip,
                              int cull_obj, int want_sign, R* t_hit, Hit* hit, uint64_t& n_nodes,
-                             uint64_t& n_tris) {
+                             uint64_t& n_tris, int root = 0) {
     LocalStack<R, kStack> stk;
-    return intersect_nearest_s(sc, ray, t_min, t_max, skip, cull_obj, want_sign, t_hit, hit, n_nodes, n_tris, stk);
+    return intersect_nearest_s(sc, ray, t_min, t_max, skip, cull_obj, want_sign, t_hit, hit, n_nodes, n_tris, stk,
+                               root);
 }
 
 // Optical depth along [0, t_max] from a point inside a medium (order-free signed sum;

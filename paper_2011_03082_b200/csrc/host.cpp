@@ -454,6 +454,37 @@ FlatBvh build_bvh(const std::vector<std::array<std::array<double, 3>, 3>>& tv,
         const int32_t a = code_obj(bld.nodes[i].c0, node_obj), b = code_obj(bld.nodes[i].c1, node_obj);
         node_obj[i] = (a == b) ? a : -1;
     }
+    {  // per-object traversal roots (see host.h FlatBvh::obj_root)
+        uint32_t n_obj = 0;
+        for (uint32_t t : tri_obj) n_obj = std::max(n_obj, t + 1);
+        std::vector<Box> ob(n_obj);
+        for (size_t i = 0; i < tv.size(); ++i)
+            for (int k = 0; k < 3; ++k) ob[tri_obj[i]].grow(tv[i][k].data());
+        bool disjoint = true;
+        for (uint32_t a = 0; a < n_obj && disjoint; ++a)
+            for (uint32_t b = a + 1; b < n_obj && disjoint; ++b) {
+                bool overlap = true;
+                for (int k = 0; k < 3; ++k)
+                    overlap &= ob[a].lo[k] <= ob[b].hi[k] && ob[b].lo[k] <= ob[a].hi[k];
+                disjoint = !overlap;
+            }
+        out.obj_root.assign(n_obj, -1);
+        if (disjoint && n_obj > 1) {
+            std::vector<int32_t> parent(out.n_nodes, -1), count(n_obj, 0), cand(n_obj, -1);
+            for (uint32_t i = 0; i < out.n_nodes; ++i)
+                for (int32_t c : {bld.nodes[i].c0, bld.nodes[i].c1})
+                    if (c >= 0) parent[c] = static_cast<int32_t>(i);
+            for (uint32_t i = 0; i < out.n_nodes; ++i) {
+                const int32_t o = node_obj[i];
+                if (o >= 0 && (parent[i] < 0 || node_obj[parent[i]] < 0)) {
+                    ++count[o];
+                    cand[o] = static_cast<int32_t>(i);
+                }
+            }
+            for (uint32_t o = 0; o < n_obj; ++o)
+                if (count[o] == 1) out.obj_root[o] = cand[o];
+        }
+    }
     std::vector<NodeF> nf(out.n_nodes);
     std::vector<NodeD> nd(out.n_nodes);
     for (uint32_t i = 0; i < out.n_nodes; ++i) {

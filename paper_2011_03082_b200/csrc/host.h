@@ -60,6 +60,10 @@ struct FlatBvh {
     std::vector<uint8_t> nodes_f64, tris_f64;  // NodeD[], TriD[]
     uint32_t n_nodes = 0, n_tris = 0;
     uint32_t max_depth = 0;       // interior levels on the deepest root-leaf path (stack bound)
+    // Per object: the interior node whose subtree holds exactly that object's triangles,
+    // when the objects' bounding boxes are pairwise disjoint (a ray inside object o then
+    // meets o's surface before any other triangle); -1 = start at the root.
+    std::vector<int32_t> obj_root;
     std::vector<uint32_t> order;  // leaf position -> input triangle index
 };
 // tri_vertices: [n][3] corners; tri_obj: object id per triangle.

@@ -247,8 +247,9 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     if (trace && proceed) {
         const RayK<R> ray = make_ray(p.x, p.w);
         const int want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
+        // an in-medium flight starts at its object's subtree (disjoint objects, FP32)
         hit = intersect_nearest(sc, ray, p.skip >= 0 ? sc.surf_eps : sc.t_min, t_max, p.skip, p.cull, want,
-                                &t_hit, &h, st.nodes, st.tris);
+                                &t_hit, &h, st.nodes, st.tris, inside ? ob->bvh_root : 0);
         ++st.traversals;
     }
 #ifdef SST_TRACE_DEBUG

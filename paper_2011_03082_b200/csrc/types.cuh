@@ -65,6 +65,7 @@ struct ObjK {
     R skip_inv_voxel, skip_unit;
     uint32_t skip_dims[3];
     uint32_t convex;  // closed convex mesh: a ray leaving it cannot hit it again
+    int32_t bvh_root;  // FP32 in-medium traversals start here (host.h FlatBvh::obj_root); 0 = root
 };
 
 template <class R>

@@ -391,7 +391,8 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
                 rec.b = p.w;
                 rec.t = t_free;
                 rec.u = p.skip;
-                rec.v = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8);
+                rec.v = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8) |
+                        (inside ? static_cast<uint32_t>(p.obj + 1) << 16 : 0u);
                 run = false;
             } else {
                 collide = true;  // the flight stays inside: collision without traversal
@@ -652,7 +653,8 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
                     ray = make_ray(mk<R>(o.x, o.y, o.z), mk<R>(d.x, d.y, d.z));
                     want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
                     t_min = skip >= 0 ? sc.surf_eps : sc.t_min;
-                    tr.init(o.w);
+                    // an in-medium flight starts at its object's subtree (disjoint objects, FP32)
+                    tr.init(o.w, inside ? sc.objs[static_cast<int>(f >> 16) - 1].bvh_root : 0);
                     have = true;
                 }
             }
