@@ -107,6 +107,18 @@ struct SharedStack {
     SST_D R& dist(int i) { return t[i * stride]; }
 };
 
+// Three-input FP32 min / max (sm_100: one FMNMX3 instead of two FMNMX).
+SST_D float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+SST_D float min3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 // slab_hit (bvh.cpp:88-101) returning the entry distance.
 template <class R>
 SST_D bool slab(const RayK<R>& r, R lox, R hix, R loy, R hiy, R loz, R hiz, R t_min, R t_max,
@@ -118,8 +130,8 @@ SST_D bool slab(const RayK<R>& r, R lox, R hix, R loy, R hiy, R loz, R hiz, R t_
         const R nx = fmaf(lox, r.inv.x, -r.oi.x), fx = fmaf(hix, r.inv.x, -r.oi.x);
         const R ny = fmaf(loy, r.inv.y, -r.oi.y), fy = fmaf(hiy, r.inv.y, -r.oi.y);
         const R nz = fmaf(loz, r.inv.z, -r.oi.z), fz = fmaf(hiz, r.inv.z, -r.oi.z);
-        t0 = fmaxf(fmaxf(t0, fminf(nx, fx)), fmaxf(fminf(ny, fy), fminf(nz, fz)));
-        t1 = fminf(fminf(t1, fmaxf(nx, fx)), fminf(fmaxf(ny, fy), fmaxf(nz, fz)));
+        t0 = max3f(fmaxf(t0, fminf(nx, fx)), fminf(ny, fy), fminf(nz, fz));
+        t1 = min3f(fminf(t1, fmaxf(nx, fx)), fmaxf(ny, fy), fmaxf(nz, fz));
         *t_enter = t0;
         return t0 <= t1;
     }
