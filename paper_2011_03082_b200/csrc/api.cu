@@ -199,6 +199,7 @@ struct sst_gpu_ctx {
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
     bool wf_concurrent = true;  // SST_WF_CONCURRENT=0: one stream per iteration
+    int convex_end = 1;         // SST_CONVEX_END=0: trace every flight the SDF/skip bounds do not cull
     std::deque<std::unique_ptr<WfJobBase>> jobs;  // FIFO: finishes (and films) in launch order
     // per-kernel device timing (sst_gpu_kernel_timing)
     bool ktime = false;
@@ -965,6 +966,7 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.stats = ctx->stats.as<unsigned long long>();
     a.sphere_batch = ctx->sphere_batch;
     a.trace_batch = ctx->trace_batch;
+    a.convex_end = ctx->convex_end;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
     if (wf && use_wavefront(ctx, st) && n_paths < (1ull << 32) && ctx->desc.n_objects < 250) {
         run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream, std::move(on_finish), sync);
@@ -1250,6 +1252,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         if (const char* e = std::getenv("SST_WF_TAIL")) ctx->wf_tail = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("SST_WF_BATCH")) ctx->wf_batch = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SST_WF_CONCURRENT")) ctx->wf_concurrent = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SST_CONVEX_END")) ctx->convex_end = std::atoi(e) != 0;
         if (const char* e = std::getenv("SST_WF_CHUNK")) ctx->wf_chunk = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
         *out = ctx.release();
     });

@@ -141,6 +141,19 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
     p.t_pend = R(0);
 }
 
+// A flight inside a CONVEX object whose end point is conservatively inside (stored SDF
+// value < 0: the whole safe ball around it is in the medium) stays inside: the segment
+// between two points of a convex set lies in it, so the traversal cannot find a leaving
+// crossing (the start point is excluded by the skip triangle / t_min and the FP32
+// orientation filter). FP32 only (FP64 keeps the reference's traversal of every flight).
+template <class R>
+SST_D bool convex_flight_inside(const ObjK<R>& ob, V3<R> x, V3<R> w, R t) {
+    if (Real<R>::kIsDouble || !ob.convex) return false;
+    bool in_grid;
+    const R v = sdf_raw(ob, x + w * t, &in_grid);
+    return in_grid && v < R(0);
+}
+
 // FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)
 // only if x is OUTSIDE the object -- a path that believes it is inside missed its
 // exit crossing (non-watertight FP32 Moller-Trumbore at an edge). FP64 keeps the
@@ -209,6 +222,7 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             // radius and, when that is too coarse, the finer skip grid.
             trace = !(t_free < p.r_here);
             if (trace) trace = !(t_free < skip_radius(*ob, p.x));
+            if (trace && a.convex_end) trace = !convex_flight_inside(*ob, p.x, p.w, t_free);
         } else {
             trace = true;
         }

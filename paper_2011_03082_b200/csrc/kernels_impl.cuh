@@ -104,7 +104,9 @@ __global__ void __launch_bounds__(kWfBlock, SST_WF_SPHERE_BLOCKS) k_wf_sphere(Tr
 #ifndef SST_WF_SHADOW_BLOCKS
 #define SST_WF_SHADOW_BLOCKS 10
 #endif
-__global__ void __launch_bounds__(kWfBlock, SST_WF_SHADOW_BLOCKS) k_wf_shadow(TraceArgs<R> a) { wf_shadow<R>(a, a.pool); }
+__global__ void __launch_bounds__(kWfBlock, SST_WF_SHADOW_BLOCKS) k_wf_shadow(TraceArgs<R> a, int with_sphere) {
+    wf_shadow<R>(a, a.pool, with_sphere != 0);
+}
 __global__ void __launch_bounds__(kWfBlock) k_wf_compact(TraceArgs<R> a) { wf_compact<R>(a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_init(TraceArgs<R> a) { wf_init<R>(a.pool); }
 __global__ void k_wf_reset(TraceArgs<R> a) { wf_reset<R>(a.pool); }
@@ -251,13 +253,14 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
     }
     if (concurrent) {  // sphere + shadow first on the side stream
         if (st) k_wf_sphere<<<gs, kWfBlock, 0, s2>>>(a);
-        if (a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s2>>>(a);
+        if (a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s2>>>(a, 1);
     }
     if (explicit_keys) k_wf_gen<true><<<gg1, kWfBlock, 0, s>>>(a);
     else k_wf_gen<false><<<gg0, kWfBlock, 0, s>>>(a);
     mark(3);
     k_wf_trace<<<gt, kWfBlock, trace_smem, s>>>(a);
     mark(4);
+    if (concurrent && a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s>>>(a, 0);  // shares the logic records
     if (concurrent) {
         cudaEventRecord(join, side);
         cudaStreamWaitEvent(s, join, 0);
@@ -265,7 +268,7 @@ cudaError_t launch_wf_iteration(const TraceArgs<R>& a, bool st, bool explicit_ke
     }
     if (st) k_wf_sphere<<<gs, kWfBlock, 0, s>>>(a);
     mark(5);
-    if (a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s>>>(a);
+    if (a.nee) k_wf_shadow<<<gh, kWfBlock, 0, s>>>(a, 1);
     mark(6);
     return cudaGetLastError();
 }

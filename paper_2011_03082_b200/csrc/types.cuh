@@ -129,7 +129,9 @@ enum : int {
     kQFetchTrace = 6, kQFetchSphere = 7, kQFetchShadow = 8,
     kQFree = 9,     // slots whose path ended (generation input)
     kQTicket = 10,  // last-block detection of the generation kernel
-    kQCount = 12
+    kQShadowS = 11,       // sphere-step NEE records (stored from the back of the shadow arrays)
+    kQFetchShadowS = 12,  // their work-stealing cursor
+    kQCount = 14
 };
 template <class R>
 struct WfPool {
@@ -183,6 +185,7 @@ struct TraceArgs {
     int trace_batch;            // warp regrouping threshold for BVH traversals (0 = off)
     WfPool<R> pool;             // wavefront pool (wavefront.cuh)
     int resume;                 // megakernel resumes the pool's live slots (q_live) instead of new ids
+    int convex_end;             // FP32: skip traversals of flights that end inside a convex object
 };
 
 // TrainingSample (dataset.hpp:17-27): the SSWK record, 52 bytes, no padding.

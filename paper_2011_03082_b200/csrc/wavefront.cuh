@@ -381,6 +381,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
                     }
                     trace = !(t_free < p.r_here);
                     if (trace) trace = !(t_free < skip_radius(ob, p.x));
+                    if (trace && a.convex_end) trace = !convex_flight_inside(ob, p.x, p.w, t_free);
                 }
             }
             if (trace) {
@@ -586,7 +587,9 @@ SST_D void wf_init(const WfPool<R>& q) {
 // Iteration start: queue lengths and the output live count to zero.
 template <class R>
 SST_D void wf_reset(const WfPool<R>& q) {
-    if (threadIdx.x < 3 || (threadIdx.x >= kQFetchTrace && threadIdx.x <= kQFetchShadow)) q.counts[threadIdx.x] = 0u;
+    if (threadIdx.x < 3 || (threadIdx.x >= kQFetchTrace && threadIdx.x <= kQFetchShadow) || threadIdx.x == kQShadowS ||
+        threadIdx.x == kQFetchShadowS)
+        q.counts[threadIdx.x] = 0u;
     if (threadIdx.x == 3) q.counts[q.cnt_out] = 0u;
 }
 
@@ -707,7 +710,13 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
             end = kEndAbsorbed;
         } else {
             if (a.nee) {
-                const uint32_t j = warp_push(s, q.counts + kQShadow, q.q_shadow);
+                // sphere-step NEE records fill the shadow arrays from the back (their own
+                // counter): the logic pass's records can be consumed concurrently
+                cg::coalesced_group g = cg::coalesced_threads();
+                uint32_t base = 0;
+                if (g.thread_rank() == 0) base = atomicAdd(q.counts + kQShadowS, g.size());
+                const uint32_t j = q.cap - 1u - (g.shfl(base, 0) + g.thread_rank());
+                q.q_shadow[j] = s;
                 q.nee_p[j] = Q4<R>{o.rep_pos.x, o.rep_pos.y, o.rep_pos.z, o.lambda};
                 q.nee_w[j] = Q4<R>{o.rep_dir.x, o.rep_dir.y, o.rep_dir.z, int_bits<R>(p.obj | (static_cast<int>(p.c) << 8))};
             }
@@ -726,9 +735,26 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
 }
 
 // ------------------------------------------------------------------ k_wf_shadow
+// One NEE record at array position i: shadow ray through the light grid, radiance update.
 template <class R>
-SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
+SST_D void shadow_one(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t i, uint64_t& tris) {
     const DevScene<R>& sc = a.sc;
+    const uint32_t s = q.q_shadow[i];
+    const Q4<R> np = q.nee_p[i], nw = q.nee_w[i];
+    const R L0 = q.xl[s].w;  // issued early: the radiance update is the last use
+    const int oc = bits_int<R>(nw.w);
+    const int obj = oc & 0xff, c = oc >> 8;
+    const R add = nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w, tris);
+    q.xl[s].w = L0 + add;
+}
+
+// The logic pass's NEE records (front of the arrays, counts[kQShadow]) are consumed by
+// work stealing; with_sphere: then the sphere steps' records (back of the arrays,
+// counts[kQShadowS]). In a concurrent iteration a logic-only launch follows the trace
+// kernel on the job stream and a full one follows the sphere kernel on the side stream,
+// so whichever stream runs out of work first takes more of the shared queue.
+template <class R>
+SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q, bool with_sphere) {
     uint64_t tris = 0, shadow = 0;
     const uint32_t n = q.counts[kQShadow];
     for (;;) {
@@ -738,15 +764,18 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q) {
 #endif
         if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
         if (i >= n) continue;
-        const uint32_t s = q.q_shadow[i];
-        const Q4<R> np = q.nee_p[i], nw = q.nee_w[i];
-        const R L0 = q.xl[s].w;  // issued early: the radiance update is the last use
-        const int oc = bits_int<R>(nw.w);
-        const int obj = oc & 0xff, c = oc >> 8;
-        const R add = nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w,
-                               tris);
-        q.xl[s].w = L0 + add;
+        shadow_one(a, q, i, tris);
         ++shadow;
+    }
+    if (with_sphere) {
+        const uint32_t ns = q.counts[kQShadowS];
+        for (;;) {
+            const uint32_t i = warp_fetch(q.counts + kQFetchShadowS);
+            if (i - (threadIdx.x & 31u) >= ns) break;  // warp-uniform
+            if (i >= ns) continue;
+            shadow_one(a, q, q.cap - 1u - i, tris);
+            ++shadow;
+        }
     }
     unsigned long long v[kStCount] = {};
     v[kStShadow] = shadow;
