@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kTraceBlock, ST ? SST_ST_MIN_BLOCKS : SST_PT_M
 constexpr int kWfBlock = SST_WF_BLOCK;
 // Minimum resident blocks per SM (register caps) of the wavefront kernels; tuning knobs.
 #ifndef SST_WF_LOGIC_BLOCKS
-#define SST_WF_LOGIC_BLOCKS 8
+#define SST_WF_LOGIC_BLOCKS 7
 #endif
 #ifndef SST_WF_TRACE_BLOCKS
 #define SST_WF_TRACE_BLOCKS 1
