@@ -394,7 +394,8 @@ SST_D T warp_sum(T v) {
 
 // Wavefront slot -> path state (wavefront.cuh).
 template <class R>
-SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam);
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam,
+                     bool need_tpend);
 
 template <class R, bool ST, bool EXPLICIT>
 SST_D void trace_persistent(const TraceArgs<R>& a) {
@@ -414,7 +415,7 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
                 if (a.resume) {  // hand-off of the wavefront pool's live slots
                     if (my < a.pool.counts[kQResume]) {
                         uint32_t phase;
-                        load_slot(a.pool, a.pool.q_live[my], p, &phase, a.sc.cam_pos);
+                        load_slot(a.pool, a.pool.q_live[my], p, &phase, a.sc.cam_pos, true);
                         alive = true;
                     } else {
                         exhausted = true;

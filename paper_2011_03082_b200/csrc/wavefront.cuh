@@ -59,14 +59,17 @@ SST_D int meta_obj(uint32_t m) { return static_cast<int>(m & 0xffu) - 1; }
 SST_D int meta_c(uint32_t m) { return static_cast<int>((m >> 8) & 3u); }
 
 template <class R>
+// need_tpend: the queued flight length is only stored while a traversal is queued and
+// only the megakernel hand-off reads it from the slot (the logic pass takes it from the
+// traversal result: a miss leaves t_hit = t_max = the flight length).
 SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLocal<R>& p, uint32_t* phase,
-                          const V3<R>& sc_cam_pos) {
+                          const V3<R>& sc_cam_pos, bool need_tpend) {
     const Q4<R> xl = q.xl[s], wr = q.wr[s];
     p.x = mk<R>(xl.x, xl.y, xl.z);
     p.L = xl.w;
     p.w = mk<R>(wr.x, wr.y, wr.z);
     p.r_here = wr.w;
-    p.t_pend = q.tpend[s];
+    p.t_pend = need_tpend && meta_phase(m.w) == kPhTrace ? q.tpend[s] : Real<R>::kInf;
     if (m.w & kMetaFresh) {  // camera ray: the state is in the trace record
         const uint32_t j = q.tq[s];
         const Q4<R> d = q.tr_cam[j];
@@ -93,8 +96,9 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
 }
 
 template <class R>
-SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam) {
-    load_slot_from(q, s, q.meta[s], p, phase, cam);
+SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam,
+                     bool need_tpend) {
+    load_slot_from(q, s, q.meta[s], p, phase, cam, need_tpend);
 }
 
 template <class R>
@@ -104,7 +108,7 @@ SST_D void store_slot(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p, uin
     q.rng[s] = p.rng.s;
     q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), p.seg, static_cast<uint32_t>(p.skip),
                            pack_meta(p.obj, p.c, p.r_valid, phase, p.cull));
-    q.tpend[s] = p.t_pend;
+    if (phase == kPhTrace) q.tpend[s] = p.t_pend;
 }
 
 SST_D void set_phase(uint4* meta, uint32_t s, uint32_t phase) {
@@ -319,7 +323,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
         hi = q.hinfo[j];
         t_hit = q.thit[j];
     }
-    load_slot_from(q, s, mt, p, &phase, sc.cam_pos);
+    load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false);
     ++st.lane_iters;
     int emit = kEmitNone;
     int end = -1;
@@ -351,7 +355,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
                 p.skip = Real<R>::kIsDouble ? -1 : static_cast<int>(hi.x);
                 phase = kPhFlight;
             } else {
-                t_free = p.t_pend;
+                t_free = t_hit;  // a miss leaves t_best = t_max = the queued flight length
                 collide = true;
             }
         }
@@ -698,7 +702,7 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
         const uint32_t s = q.q_sphere[i];
         PathLocal<R> p;
         uint32_t phase;
-        load_slot(q, s, p, &phase, sc.cam_pos);
+        load_slot(q, s, p, &phase, sc.cam_pos, false);
         ++st.sphere;
         StepOut<R> o;
         const MediumK<R>& m = sc.objs[p.obj].med[p.c];
