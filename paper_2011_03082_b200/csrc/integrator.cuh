@@ -146,12 +146,16 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
 // between two points of a convex set lies in it, so the traversal cannot find a leaving
 // crossing (the start point is excluded by the skip triangle / t_min and the FP32
 // orientation filter). FP32 only (FP64 keeps the reference's traversal of every flight).
+// Any object: the safe balls at the two end points (radius r_x at the start -- the
+// larger of the SDF and skip-grid bounds -- and the SDF safe radius at the end) cover the
+// segment when r_x + r_y > t, so it cannot cross the surface either.
 template <class R>
-SST_D bool convex_flight_inside(const ObjK<R>& ob, V3<R> x, V3<R> w, R t) {
-    if (Real<R>::kIsDouble || !ob.convex) return false;
+SST_D bool flight_contained(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
+    if (Real<R>::kIsDouble) return false;
     bool in_grid;
     const R v = sdf_raw(ob, x + w * t, &in_grid);
-    return in_grid && v < R(0);
+    if (!in_grid || !(v < R(0))) return false;
+    return ob.convex || t < r_x - v;
 }
 
 // FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)
@@ -221,8 +225,12 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
             // reach the boundary: skip the traversal (exact). Bounds: the scene SDF
             // radius and, when that is too coarse, the finer skip grid.
             trace = !(t_free < p.r_here);
-            if (trace) trace = !(t_free < skip_radius(*ob, p.x));
-            if (trace && a.convex_end) trace = !convex_flight_inside(*ob, p.x, p.w, t_free);
+            if (trace) {
+                const R rs = skip_radius(*ob, p.x);
+                trace = !(t_free < rs);
+                if (trace && a.convex_end)
+                    trace = !flight_contained(*ob, p.x, p.w, t_free, Real<R>::fmax_(p.r_here, rs));
+            }
         } else {
             trace = true;
         }

@@ -384,8 +384,12 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
                         else t_free = -Real<R>::div_(Real<R>::log_(R(1) - u), m.sigma_t);
                     }
                     trace = !(t_free < p.r_here);
-                    if (trace) trace = !(t_free < skip_radius(ob, p.x));
-                    if (trace && a.convex_end) trace = !convex_flight_inside(ob, p.x, p.w, t_free);
+                    if (trace) {
+                        const R rs = skip_radius(ob, p.x);
+                        trace = !(t_free < rs);
+                        if (trace && a.convex_end)
+                            trace = !flight_contained(ob, p.x, p.w, t_free, Real<R>::fmax_(p.r_here, rs));
+                    }
                 }
             }
             if (trace) {
