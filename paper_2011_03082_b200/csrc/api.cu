@@ -195,7 +195,7 @@ struct sst_gpu_ctx {
     // <= min(pool / 8, wf_tail), iterations per host check.
     int wavefront = 2;
     uint32_t wf_pool = 1u << 23;
-    uint32_t wf_tail = 1u << 20;
+    uint32_t wf_tail = 1u << 19;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
     bool wf_concurrent = true;  // SST_WF_CONCURRENT=0: one stream per iteration
