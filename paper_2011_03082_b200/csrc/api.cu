@@ -726,21 +726,28 @@ void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
 
 bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
 
-// Carves the wavefront pool of `cap` slots out of the slot's device buffer.
+// Sizes of the wavefront pool's arrays for `cap` slots (carve_pool order).
 template <class R>
-WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
+size_t pool_layout(uint32_t cap, size_t (&off)[22]) {
     const size_t n = cap;
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
                             n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
                             kQCount * 4, 8, n * 4, n * 4, n * 4,
                             n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>)};
-    size_t off[22], total = 0;
+    size_t total = 0;
     int k = 0;
     for (size_t b : sizes) {
         off[k++] = total;
         total += (b + 255) & ~size_t(255);
     }
-    sl.wf.reserve(total);
+    return total;
+}
+
+// Carves the wavefront pool of `cap` slots out of the slot's device buffer.
+template <class R>
+WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
+    size_t off[22];
+    sl.wf.reserve(pool_layout<R>(cap, off));
     char* base = sl.wf.as<char>();
     WfPool<R> q{};
     q.cap = cap;
@@ -1098,6 +1105,23 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
     if (!ctx->timing_open) {
         CK(cudaEventRecord(ctx->ev0, ctx->stream));
         ctx->timing_open = true;
+    }
+    if (use_wavefront(ctx, integrator == SST_INTEGRATOR_ST)) {
+        // Every pipeline slot gets its radiance scratch and wavefront pool now (grow-only):
+        // a slot first used later -- e.g. inside a timed or latency-sensitive stretch of
+        // calls -- would otherwise cudaFree/cudaMalloc (device-synchronising) mid-pipeline.
+        size_t off[22];
+        const uint64_t cap = std::max<uint64_t>(32, std::min<uint64_t>(per_sample * chunk, ctx->wf_pool));
+        const size_t pool = pool_layout<R>(static_cast<uint32_t>(cap), off);
+        bool grow = false;
+        for (auto& s2 : ctx->slots) grow |= s2.rad.bytes < per_sample * chunk * sizeof(R) || s2.wf.bytes < pool;
+        if (grow) {
+            drain_jobs(ctx);
+            for (auto& s2 : ctx->slots) {
+                s2.rad.reserve(per_sample * chunk * sizeof(R));
+                s2.wf.reserve(pool);
+            }
+        }
     }
     CK(cudaEventRecord(ctx->ev_start, ctx->stream));
     for (uint32_t s = s0; s < s1; s += chunk) {
