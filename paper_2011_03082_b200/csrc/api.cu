@@ -541,6 +541,8 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
     ctx->grid_list_n = total;
 }
 
+void ensure_film_staging(sst_gpu_ctx* ctx, uint64_t n);
+
 void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     const bool tdbg = std::getenv("SST_DEBUG_TIMING") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
@@ -696,6 +698,11 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     CK(cudaStreamSynchronize(ctx->stream));
     lap("done");
     ctx->scene = true;
+    // host-film renders of this frame read back through pinned staging: allocate it (and
+    // the device film sums) now rather than inside the first render call
+    ensure_film_staging(ctx, 3ull * d->width * d->height);
+    ctx->film_sum.reserve(3ull * d->width * d->height * sizeof(double));
+    ctx->film_sq.reserve(3ull * d->width * d->height * sizeof(double));
 }
 
 template <class R>
@@ -1155,8 +1162,8 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
 // Host films accumulate the call's device sums: the D2H copies go through a pinned
 // staging buffer in pieces, and each piece is added (by a few host threads) while the
 // next one is in flight.
-void readback_films(sst_gpu_ctx* ctx, const double* dsum, const double* dsq, uint64_t n, double* film_sum,
-                    double* film_sq) {
+// Pinned staging for n film entries (sum + sum of squares); grow-only.
+void ensure_film_staging(sst_gpu_ctx* ctx, uint64_t n) {
     if (ctx->film_pin_n < 2 * n) {
         if (ctx->film_pin) CK(cudaFreeHost(ctx->film_pin));
         ctx->film_pin = nullptr;
@@ -1164,6 +1171,11 @@ void readback_films(sst_gpu_ctx* ctx, const double* dsum, const double* dsq, uin
         CK(cudaMallocHost(&ctx->film_pin, 2 * n * sizeof(double)));
         ctx->film_pin_n = 2 * n;
     }
+}
+
+void readback_films(sst_gpu_ctx* ctx, const double* dsum, const double* dsq, uint64_t n, double* film_sum,
+                    double* film_sq) {
+    ensure_film_staging(ctx, n);
     if (!ctx->film_pin_ev[0])
         for (auto& e : ctx->film_pin_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     constexpr int kPieces = 8;
