@@ -144,6 +144,7 @@ struct sst_gpu_ctx {
     uint64_t grid_list_n = 0;  // light-grid list entries
     uint32_t n_nodes = 0, n_tris = 0;
     std::vector<ObjectHost> objects;
+    std::vector<uint64_t> object_fp;  // fingerprint of objects[o] (re-upload of the same object: no copy)
     sst_scene_desc desc{};
     DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri;
     DevBuf grid_tris32;  // FP32 triangle records in light-grid list order (grid_tri gathered)
@@ -556,6 +557,9 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     if (d->width == 0 || d->height == 0) throw InvalidArgument("camera resolution must be >= 1x1");
     if (!(d->cam_vfov_deg > 0.0 && d->cam_vfov_deg < 180.0)) throw InvalidArgument("camera fov out of range");
     std::vector<ObjectHost> objs(d->n_objects);
+    std::vector<uint64_t> objs_fp(d->n_objects, 0);
+    std::vector<uint64_t> prev_fp;
+    prev_fp.swap(ctx->object_fp);  // a failed upload leaves no reusable objects behind
     std::vector<std::array<std::array<double, 3>, 3>> tv;
     std::vector<uint32_t> tobj;
     for (uint32_t o = 0; o < d->n_objects; ++o) {
@@ -599,6 +603,14 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
             ofp = fnv(&od.sdf_voxel, sizeof od.sdf_voxel, ofp);
             ofp = fnv(od.sdf_dims, sizeof od.sdf_dims, ofp);
             ofp = fnv(od.sdf_values, static_cast<size_t>(od.sdf_dims[0]) * od.sdf_dims[1] * od.sdf_dims[2] * sizeof(float), ofp);
+        }
+        objs_fp[o] = ofp;
+        if (o < ctx->objects.size() && o < prev_fp.size() && prev_fp[o] == ofp) {
+            // the same object as the previous upload: take its host copy over (no 3 MB copy)
+            const sst_medium media[3] = {objs[o].media[0], objs[o].media[1], objs[o].media[2]};
+            objs[o] = std::move(ctx->objects[o]);
+            for (int c = 0; c < 3; ++c) objs[o].media[c] = media[c];
+            continue;
         }
         if (auto it = ctx->obj_cache.find(ofp); it != ctx->obj_cache.end()) {
             const sst_medium media[3] = {objs[o].media[0], objs[o].media[1], objs[o].media[2]};
@@ -653,6 +665,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     lap(cached ? "bvh+grid(hit)" : "bvh+grid(build)");
     // upload
     ctx->objects = std::move(objs);
+    ctx->object_fp = std::move(objs_fp);
     ctx->desc = *d;
     ctx->desc.objects = nullptr;
     auto up = [&](DevBuf& b, const std::vector<uint8_t>& src) {
