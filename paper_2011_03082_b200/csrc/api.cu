@@ -201,6 +201,9 @@ struct sst_gpu_ctx {
     int wf_batch = 4;
     bool wf_concurrent = true;  // SST_WF_CONCURRENT=0: one stream per iteration
     int convex_end = 1;         // SST_CONVEX_END=0: trace every flight the SDF/skip bounds do not cull
+    // launches with fewer paths use the megakernel (the wavefront's per-iteration costs
+    // dominate below ~3e5 paths: tools/small_render_crossover.py); SST_WF_MIN_PATHS
+    uint64_t wf_min_paths = 327680;
     std::deque<std::unique_ptr<WfJobBase>> jobs;  // FIFO: finishes (and films) in launch order
     // per-kernel device timing (sst_gpu_kernel_timing)
     bool ktime = false;
@@ -995,7 +998,8 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
     a.trace_batch = ctx->trace_batch;
     a.convex_end = ctx->convex_end;
     CK(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), stream));
-    if (wf && use_wavefront(ctx, st) && n_paths < (1ull << 32) && ctx->desc.n_objects < 250) {
+    if (wf && use_wavefront(ctx, st) && n_paths >= ctx->wf_min_paths && n_paths < (1ull << 32) &&
+        ctx->desc.n_objects < 250) {
         run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream, std::move(on_finish), sync);
         return;
     }
@@ -1302,6 +1306,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         if (const char* e = std::getenv("SST_WF_BATCH")) ctx->wf_batch = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SST_WF_CONCURRENT")) ctx->wf_concurrent = std::atoi(e) != 0;
         if (const char* e = std::getenv("SST_CONVEX_END")) ctx->convex_end = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SST_WF_MIN_PATHS")) ctx->wf_min_paths = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("SST_WF_CHUNK")) ctx->wf_chunk = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
         *out = ctx.release();
     });

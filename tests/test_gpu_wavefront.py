@@ -18,7 +18,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-ENV_KEYS = ("SST_WAVEFRONT", "SST_WF_POOL", "SST_WF_TAIL", "SST_WF_BATCH")
+ENV_KEYS = ("SST_WAVEFRONT", "SST_WF_POOL", "SST_WF_TAIL", "SST_WF_BATCH", "SST_WF_MIN_PATHS")
 
 
 def _renderer(models_dir, precision, **env):
@@ -67,8 +67,9 @@ def test_wavefront_paths_identical_to_megakernel(models_dir, scenes, precision, 
     n = 40000 if precision == "f64" else 200000
     pix, smp, ch = _keys(scene.n_pixels, n)
     mk = _renderer(models_dir, precision, SST_WAVEFRONT=0)
-    configs = [dict(SST_WAVEFRONT=2),  # default pool: drain + hand-off
-               dict(SST_WAVEFRONT=2, SST_WF_POOL=2048, SST_WF_TAIL=64, SST_WF_BATCH=1)]  # many recycles
+    configs = [dict(SST_WAVEFRONT=2, SST_WF_MIN_PATHS=0),  # default pool: drain + hand-off
+               dict(SST_WAVEFRONT=2, SST_WF_MIN_PATHS=0, SST_WF_POOL=2048, SST_WF_TAIL=64,
+                    SST_WF_BATCH=1)]  # many recycles
     wfs = [_renderer(models_dir, precision, **c) for c in configs]
     try:
         for r in [mk] + wfs:
@@ -102,7 +103,7 @@ def test_wavefront_film_identical_to_megakernel(models_dir, scenes):
     from paper_2011_03082_b200 import PT, ST, abi
     scene = scenes["c5"]
     mk = _renderer(models_dir, "f64", SST_WAVEFRONT=0)
-    wf = _renderer(models_dir, "f64", SST_WAVEFRONT=2, SST_WF_POOL=8192, SST_WF_TAIL=256)
+    wf = _renderer(models_dir, "f64", SST_WAVEFRONT=2, SST_WF_MIN_PATHS=0, SST_WF_POOL=8192, SST_WF_TAIL=256)
     try:
         for r in (mk, wf):
             r.upload_scene(scene)
@@ -124,7 +125,7 @@ def test_wavefront_async_slabs_match_one_call(models_dir, scenes):
     import torch
     from paper_2011_03082_b200 import ST
     scene = scenes["c1"]
-    r = _renderer(models_dir, "f32", SST_WAVEFRONT=1, SST_WF_POOL=65536, SST_WF_TAIL=1024)
+    r = _renderer(models_dir, "f32", SST_WAVEFRONT=1, SST_WF_MIN_PATHS=0, SST_WF_POOL=65536, SST_WF_TAIL=1024)
     try:
         r.upload_scene(scene)
         n = 3 * scene.n_pixels
