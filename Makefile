@@ -47,7 +47,7 @@ $(BUILD)/host.o: $(CSRC)/host.cpp $(HDRS)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
 $(LIB): $(BUILD)/kernels_f32.o $(BUILD)/kernels_f64.o $(BUILD)/train.o $(BUILD)/api.o $(BUILD)/host.o
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lz
 
 oracle:
 	$(MAKE) -C oracle all

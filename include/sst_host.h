@@ -43,6 +43,19 @@ int sst_dataset_save(const char* path, uint64_t count, float sigma_t_lo, float s
 /* save_pfm (image.cpp:32-41): little-endian "PF", bottom row first. */
 int sst_image_save_pfm(const char* path, uint32_t width, uint32_t height, const float* rgb);
 
+/* save_pfm_gray (image.cpp:62-73): one-channel "Pf", bottom row first. */
+int sst_image_save_pfm_gray(const char* path, uint32_t width, uint32_t height, const float* values);
+
+/* load_pfm (image.cpp:43-60): little-endian colour PFM only (the reference's errors:
+ * "not a color PFM file", "big-endian PFM unsupported", "truncated PFM" -> SST_E_RUNTIME).
+ * rgb == NULL queries width/height only; otherwise capacity (floats) must be >= w*h*3. */
+int sst_image_load_pfm(const char* path, uint32_t* width, uint32_t* height, float* rgb,
+                       uint64_t capacity);
+
+/* save_png (image.cpp:101-138): 8-bit sRGB truecolor, clamp to [0,1], lround, filter 0,
+ * zlib level 9 single IDAT; byte-identical to the reference with the same zlib. */
+int sst_image_save_png(const char* path, uint32_t width, uint32_t height, const float* rgb);
+
 #ifdef __cplusplus
 }
 #endif

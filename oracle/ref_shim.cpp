@@ -25,6 +25,7 @@
 #include "sst/bvh.hpp"
 #include "sst/cvae.hpp"
 #include "sst/dataset.hpp"
+#include "sst/image.hpp"
 #include "sst/mesh.hpp"
 #include "sst/optics.hpp"
 #include "sst/parallel.hpp"
@@ -286,6 +287,16 @@ int ref_save_dataset(const char* path, uint64_t n, double s_lo, double s_hi, dou
     });
 }
 
+// save_png (image.cpp:101-138) for the PNG byte-compatibility test. (The reference's PFM
+// writers/reader use iostream number formatting, which crashes when this library is
+// dlopen'ed into Python next to the system libstdc++; the PFM tests check the format directly.)
+int ref_save_png(const char* path, uint32_t w, uint32_t h, const float* rgb) {
+    return guarded([&] {
+        Image img(w, h);
+        std::memcpy(img.pixels.data(), rgb, static_cast<size_t>(w) * h * 3 * sizeof(float));
+        save_png(path, img);
+    });
+}
 // Ground-truth unit-sphere walks (sphere_walk.cpp:22-50) -> (N, cos_theta, alpha, beta).
 int ref_walk_stats(double sigma_t, double g, uint64_t seed, uint64_t n, uint32_t* n_events,
                    double* exit_params) {

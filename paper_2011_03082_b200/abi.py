@@ -144,6 +144,7 @@ EXPORTED = [
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
     "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm", "sst_dataset_save",
+    "sst_image_save_pfm_gray", "sst_image_load_pfm", "sst_image_save_png",
 ]
 
 _lib = None
@@ -204,6 +205,9 @@ def _declare(L):
     L.sst_sdf_free.argtypes = [P]
     L.sst_sdf_free.restype = None
     L.sst_image_save_pfm.argtypes = [C.c_char_p, U32, U32, P]
+    L.sst_image_save_pfm_gray.argtypes = [C.c_char_p, U32, U32, P]
+    L.sst_image_load_pfm.argtypes = [C.c_char_p, P, P, P, U64]
+    L.sst_image_save_png.argtypes = [C.c_char_p, U32, U32, P]
 
 
 class SstError(RuntimeError):

@@ -93,6 +93,29 @@ class Image:
         px = np.ascontiguousarray(self.pixels, dtype=np.float32)
         abi.check(abi.lib().sst_image_save_pfm(path.encode(), self.width, self.height, _p(px)))
 
+    def save_png(self, path: str):
+        """8-bit sRGB PNG, byte-identical to the reference's save_png (image.cpp:101-138)."""
+        px = np.ascontiguousarray(self.pixels, dtype=np.float32)
+        abi.check(abi.lib().sst_image_save_png(path.encode(), self.width, self.height, _p(px)))
+
+
+def load_pfm(path: str) -> Image:
+    """load_pfm (image.cpp:43-60): little-endian colour PFM into an Image."""
+    L = abi.lib()
+    w, h = C.c_uint32(), C.c_uint32()
+    abi.check(L.sst_image_load_pfm(path.encode(), C.byref(w), C.byref(h), None, 0))
+    px = np.empty((h.value, w.value, 3), np.float32)
+    abi.check(L.sst_image_load_pfm(path.encode(), C.byref(w), C.byref(h), _p(px), px.size))
+    return Image(w.value, h.value, px)
+
+
+def save_pfm_gray(path: str, values: np.ndarray):
+    """save_pfm_gray (image.cpp:62-73): (height, width) float map, "Pf", bottom row first."""
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    if v.ndim != 2:
+        raise abi.InvalidArgument(abi.SST_E_INVALID_ARGUMENT, "save_pfm_gray: size mismatch")
+    abi.check(abi.lib().sst_image_save_pfm_gray(path.encode(), v.shape[1], v.shape[0], _p(v)))
+
 
 def image_metrics(a: Image, b: Image) -> Tuple[float, float]:
     """Channel-pooled (RMSE, MAE) over linear values (image.cpp:16-30)."""

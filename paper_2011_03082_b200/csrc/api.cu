@@ -5,6 +5,7 @@
 // boundary; there is no CPU fallback -- without a CUDA device every compute entry
 // fails with SST_E_CUDA.
 #include <cuda_runtime.h>
+#include <zlib.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1813,6 +1814,97 @@ int sst_image_save_pfm(const char* path, uint32_t w, uint32_t h, const float* rg
         for (uint32_t y = h; y-- > 0;)
             out.write(reinterpret_cast<const char*>(rgb + static_cast<size_t>(y) * w * 3),
                       static_cast<std::streamsize>(w) * 3 * sizeof(float));
+        if (!out) throw RuntimeError(std::string("write failure: ") + path);
+    });
+}
+
+int sst_image_save_pfm_gray(const char* path, uint32_t w, uint32_t h, const float* v) {
+    return guarded([&] {
+        if (!path || !v) throw InvalidArgument("null argument");
+        std::ofstream out(path, std::ios::binary | std::ios::trunc);
+        if (!out) throw RuntimeError(std::string("cannot open for writing: ") + path);
+        out << "Pf\n" << w << " " << h << "\n-1.0\n";
+        for (uint32_t y = h; y-- > 0;)
+            out.write(reinterpret_cast<const char*>(v + static_cast<size_t>(y) * w),
+                      static_cast<std::streamsize>(w) * sizeof(float));
+        if (!out) throw RuntimeError(std::string("write failure: ") + path);
+    });
+}
+
+int sst_image_load_pfm(const char* path, uint32_t* width, uint32_t* height, float* rgb,
+                       uint64_t capacity) {
+    return guarded([&] {
+        if (!path || !width || !height) throw InvalidArgument("null argument");
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw RuntimeError(std::string("cannot open: ") + path);
+        std::string tag;
+        uint32_t w = 0, h = 0;
+        double scale = 0.0;
+        in >> tag;
+        if (tag != "PF") throw RuntimeError(std::string("not a color PFM file: ") + path);
+        in >> w >> h >> scale;
+        in.get();
+        if (scale >= 0.0) throw RuntimeError(std::string("big-endian PFM unsupported: ") + path);
+        *width = w;
+        *height = h;
+        const uint64_t n = static_cast<uint64_t>(w) * h * 3;
+        if (!rgb) return;  // size query
+        if (capacity < n) throw InvalidArgument("rgb buffer too small");
+        for (uint32_t y = h; y-- > 0;)
+            in.read(reinterpret_cast<char*>(rgb + static_cast<size_t>(y) * w * 3),
+                    static_cast<std::streamsize>(w) * 3 * sizeof(float));
+        if (!in) throw RuntimeError(std::string("truncated PFM: ") + path);
+    });
+}
+
+// 8-bit sRGB truecolor PNG, one IDAT at zlib level 9, filter 0 (image.cpp:75-138).
+// The file is assembled in one host buffer and written with a single call.
+int sst_image_save_png(const char* path, uint32_t w, uint32_t h, const float* rgb) {
+    return guarded([&] {
+        if (!path || !rgb) throw InvalidArgument("null argument");
+        auto srgb8 = [](float linear) -> uint8_t {
+            double v = std::fmin(1.0, std::fmax(0.0, static_cast<double>(linear)));
+            v = v <= 0.0031308 ? 12.92 * v : 1.055 * std::pow(v, 1.0 / 2.4) - 0.055;
+            return static_cast<uint8_t>(std::lround(v * 255.0));
+        };
+        const size_t stride = static_cast<size_t>(w) * 3 + 1;
+        std::vector<uint8_t> scan(stride * h);
+        for (uint32_t y = 0; y < h; ++y) {
+            uint8_t* row = scan.data() + y * stride;
+            row[0] = 0;
+            const float* src = rgb + static_cast<size_t>(y) * w * 3;
+            for (size_t i = 0; i < static_cast<size_t>(w) * 3; ++i) row[1 + i] = srgb8(src[i]);
+        }
+        uLongf zlen = compressBound(static_cast<uLong>(scan.size()));
+        std::vector<uint8_t> z(zlen);
+        if (compress2(z.data(), &zlen, scan.data(), static_cast<uLong>(scan.size()), 9) != Z_OK)
+            throw RuntimeError(std::string("PNG deflate failure: ") + path);
+
+        std::vector<uint8_t> file{0x89, 'P', 'N', 'G', '\r', '\n', 0x1A, '\n'};
+        auto be32 = [&file](uint32_t v) {
+            for (int s = 24; s >= 0; s -= 8) file.push_back(static_cast<uint8_t>(v >> s));
+        };
+        auto chunk = [&](const char* type, const uint8_t* data, size_t len) {
+            be32(static_cast<uint32_t>(len));
+            const size_t at = file.size();
+            file.insert(file.end(), type, type + 4);
+            if (len) file.insert(file.end(), data, data + len);
+            be32(static_cast<uint32_t>(crc32(0L, file.data() + at, static_cast<uInt>(len + 4))));
+        };
+        uint8_t ihdr[13] = {};
+        for (int i = 0; i < 4; ++i) {
+            ihdr[i] = static_cast<uint8_t>(w >> (24 - 8 * i));
+            ihdr[4 + i] = static_cast<uint8_t>(h >> (24 - 8 * i));
+        }
+        ihdr[8] = 8;  // bit depth
+        ihdr[9] = 2;  // truecolor
+        chunk("IHDR", ihdr, sizeof ihdr);
+        chunk("IDAT", z.data(), zlen);
+        chunk("IEND", nullptr, 0);
+
+        std::ofstream out(path, std::ios::binary | std::ios::trunc);
+        if (!out) throw RuntimeError(std::string("cannot open for writing: ") + path);
+        out.write(reinterpret_cast<const char*>(file.data()), static_cast<std::streamsize>(file.size()));
         if (!out) throw RuntimeError(std::string("write failure: ") + path);
     });
 }

@@ -2,7 +2,7 @@
 // missing cmd_render, for the two built-in benchmark scenes).
 //
 //   sst_render --scene c1|c5 [--integrator st|pt] [--spp N] [--seed S] [--nee 0|1]
-//              [--width W --height H] [--models DIR] [--out image.pfm] [--precision f32|f64]
+//              [--width W --height H] [--models DIR] [--out image.pfm|image.png] [--precision f32|f64]
 //
 // Exit codes: 0 ok, 1 usage, 2 data/model, 3 internal (incl. no GPU).
 #include <chrono>
@@ -27,7 +27,7 @@ struct Mesh {
 int usage() {
     std::fprintf(stderr,
                  "usage: sst_render --scene c1|c5 [--integrator st|pt] [--spp N] [--seed S] [--nee 0|1]\n"
-                 "                  [--width W] [--height H] [--models DIR] [--out F.pfm] [--precision f32|f64]\n");
+                 "                  [--width W] [--height H] [--models DIR] [--out F.pfm|F.png] [--precision f32|f64]\n");
     return 1;
 }
 
@@ -105,7 +105,11 @@ int main(int argc, char** argv) {
         const auto t0 = std::chrono::steady_clock::now();
         const sst_b200::Image img = ctx.render(integ == "st" ? SST_INTEGRATOR_ST : SST_INTEGRATOR_PT, spp, seed, nee != 0, &st);
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        if (!out.empty()) sst_b200::check(sst_image_save_pfm(out.c_str(), img.width, img.height, img.pixels.data()));
+        if (!out.empty()) {
+            const bool png = out.size() > 4 && out.compare(out.size() - 4, 4, ".png") == 0;
+            sst_b200::check((png ? sst_image_save_png : sst_image_save_pfm)(out.c_str(), img.width, img.height,
+                                                                          img.pixels.data()));
+        }
         std::printf("{\"scene\": \"%s\", \"integrator\": \"%s\", \"spp\": %u, \"paths\": %llu, \"segments\": %llu, "
                     "\"sphere_steps\": %llu, \"pt_events\": %llu, \"device_ms\": %.3f, \"wall_s\": %.3f, "
                     "\"segments_per_s\": %.6g}\n",
