@@ -203,6 +203,12 @@ typedef struct {
     double r_min;             /* <= 0: max(2/sigma_t, 1.5 voxel) */
     uint32_t max_pt_events;   /* 0: 1e6 */
     uint32_t max_st_steps;    /* 0: 1e5 */
+    /* Light model: 0 = point light at light_position, light_power =
+     * Phi, inverse-square falloff; 1 = directional light: light_direction points TOWARD
+     * the light (normalised here), light_power = irradiance E, no falloff, and the shadow
+     * ray's optical depth is measured out to the last boundary exit. */
+    uint32_t light_kind;
+    double light_direction[3];
 } sst_scene_desc;
 
 /* Uploads the scene: builds the BVH on the host, builds missing SDFs on the

@@ -399,6 +399,8 @@ struct RefScene {
     std::vector<SdfGrid> sdf;
     std::vector<MediumParams> media;  // [obj*3 + channel]
     Vec3 light_pos;
+    bool directional;
+    Vec3 light_dir;
     double light_power[3];
     double background[3];
     Vec3 cam_pos, cam_fwd, cam_right, cam_up;
@@ -446,6 +448,11 @@ void* ref_scene_create(const sst_scene_desc* d) {
         sc->mesh.compute_face_normals();
         sc->bvh = std::make_unique<Bvh>(sc->mesh);
         sc->light_pos = Vec3(d->light_position[0], d->light_position[1], d->light_position[2]);
+        sc->directional = d->light_kind == 1;
+        if (sc->directional) {
+            const Vec3 ld(d->light_direction[0], d->light_direction[1], d->light_direction[2]);
+            sc->light_dir = ld / std::sqrt(dot(ld, ld));
+        }
         for (int c = 0; c < 3; ++c) {
             sc->light_power[c] = d->light_power[c];
             sc->background[c] = d->background[c];
@@ -487,10 +494,11 @@ static double r_min_for(const RefScene& s, int obj, int c) {
 // hits of intersect_all on [p, x_L].
 static double nee_term(const RefScene& s, int obj, int c, const Vec3& p, const Vec3& w,
                        double weight, std::vector<Hit>& hits) {
-    const Vec3 to_l = s.light_pos - p;
-    const double d2 = dot(to_l, to_l);
-    const double d = std::sqrt(d2);
-    const Vec3 wl = to_l / d;
+    // directional light: to the last boundary exit, irradiance, no 1/d^2
+    const Vec3 to_l = s.directional ? s.light_dir : s.light_pos - p;
+    const double d2 = s.directional ? 1.0 : dot(to_l, to_l);
+    const double d = s.directional ? 1e30 : std::sqrt(d2);
+    const Vec3 wl = s.directional ? s.light_dir : to_l / d;
     Ray ray{p, wl, d};
     s.bvh->intersect_all(ray, hits);
     double tau = 0.0, t_prev = 0.0;

@@ -541,6 +541,7 @@ struct so_scene {
     uint32_t (*sdf_d)[3];
     float** sdf_vals;
     v3 light; double power[3], bg[3];
+    int directional; v3 ldir;
     v3 cam, fwd, right, up;
     double tan_half, aspect;
     uint32_t w, h;
@@ -742,6 +743,8 @@ int so_scene_create(const sst_scene_desc* d, so_scene** out) {
     }
     build(s, 0, nt);
     s->light = ld3(d->light_position);
+    s->directional = d->light_kind == 1;
+    s->ldir = s->directional ? normalize(ld3(d->light_direction)) : ld3(d->light_position);
     for (int c = 0; c < 3; ++c) { s->power[c] = d->light_power[c]; s->bg[c] = d->background[c]; }
     s->cam = ld3(d->cam_position);
     const v3 look = ld3(d->cam_look_at), up = ld3(d->cam_up);
@@ -769,10 +772,11 @@ static double r_min_for(const so_scene* s, uint32_t obj, int c) {     /* SPEC.md
 
 /* NEE toward the point light */
 static double nee_term(const so_scene* s, uint32_t obj, int c, v3 p, v3 w, double weight) {
-    const v3 to_l = sub(s->light, p);
-    const double d2 = dot(to_l, to_l);
-    const double d = sqrt(d2);
-    const v3 wl = dvs(to_l, d);
+    /* directional: d_t out to the last boundary exit, irradiance, no falloff */
+    const v3 to_l = s->directional ? s->ldir : sub(s->light, p);
+    const double d2 = s->directional ? 1.0 : dot(to_l, to_l);
+    const double d = s->directional ? 1e30 : sqrt(d2);
+    const v3 wl = s->directional ? s->ldir : dvs(to_l, d);
     hit_t hits[256];
     const uint32_t nh = intersect_all(s, p, wl, 1e-9, d, hits, 256);
     double tau = 0.0, t_prev = 0.0;

@@ -80,7 +80,8 @@ class SceneDesc(C.Structure):
                 ("light_position", D * 3), ("light_power", D * 3), ("background", D * 3),
                 ("cam_position", D * 3), ("cam_look_at", D * 3), ("cam_up", D * 3),
                 ("cam_vfov_deg", D), ("width", U32), ("height", U32), ("r_min", D),
-                ("max_pt_events", U32), ("max_st_steps", U32)]
+                ("max_pt_events", U32), ("max_st_steps", U32),
+                ("light_kind", U32), ("light_direction", D * 3)]
 
 
 class PathStats(C.Structure):

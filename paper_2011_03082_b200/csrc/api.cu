@@ -437,6 +437,12 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     sc.width = d.width;
     sc.height = d.height;
     sc.light = tor(v(d.light_position));
+    sc.directional = d.light_kind == 1;
+    {
+        const double* ld = d.light_direction;
+        const double n = std::sqrt(ld[0] * ld[0] + ld[1] * ld[1] + ld[2] * ld[2]);
+        sc.light_dir = sc.directional ? mk<R>(R(ld[0] / n), R(ld[1] / n), R(ld[2] / n)) : mk<R>(R(0), R(0), R(1));
+    }
     for (int c = 0; c < 3; ++c) {
         sc.power[c] = static_cast<R>(d.light_power[c]);
         sc.bg[c] = static_cast<R>(d.background[c]);
@@ -450,7 +456,7 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     sc.cap_pt = d.max_pt_events ? d.max_pt_events : 1000000u;
     sc.cap_st = d.max_st_steps ? d.max_st_steps : 100000u;
     const char* no_grid = std::getenv("SST_NO_LIGHT_GRID");
-    const bool use_grid = ctx->grid_res && !(no_grid && no_grid[0] == '1');
+    const bool use_grid = ctx->grid_res && !sc.directional && !(no_grid && no_grid[0] == '1');
     sc.grid_off = use_grid ? ctx->grid_off.as<uint32_t>() : nullptr;
     sc.grid_tri = use_grid ? ctx->grid_tri.as<uint32_t>() : nullptr;
     sc.grid_tris = use_grid && std::is_same<R, float>::value ? ctx->grid_tris32.p : nullptr;
@@ -644,8 +650,21 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     uint64_t sfp = fnv(tv.data(), tv.size() * sizeof(tv[0]));
     sfp = fnv(tobj.data(), tobj.size() * sizeof(uint32_t), sfp);
     sfp = fnv(d->light_position, sizeof d->light_position, sfp);
-    const bool cached = ctx->scene_cache.fp == sfp && ctx->scene_cache.grid_res;
-    if (!cached) {
+    if (d->light_kind > 1) throw InvalidArgument("light_kind must be 0 (point) or 1 (directional)");
+    const bool directional = d->light_kind == 1;
+    if (directional && !(d->light_direction[0] * d->light_direction[0] + d->light_direction[1] * d->light_direction[1] +
+                             d->light_direction[2] * d->light_direction[2] > 0.0))
+        throw InvalidArgument("directional light needs a non-zero light_direction");
+    const bool cached = !directional && ctx->scene_cache.fp == sfp && ctx->scene_cache.grid_res;
+    if (directional) {  // no light-space grid (it is a cube map around a point light)
+        ctx->scene_cache = sst_gpu_ctx::SceneCache{};
+        ctx->scene_cache.bvh = build_bvh(tv, tobj);
+        if (ctx->scene_cache.bvh.max_depth + 1 > static_cast<uint32_t>(kStack))
+            throw InvalidArgument("BVH deeper than the traversal stack (" + std::to_string(kStack) + ")");
+        ctx->grid_res = 0;
+        ctx->scene_bytes_grid = 0;
+        ctx->grid_list_n = 0;
+    } else if (!cached) {
         ctx->scene_cache = sst_gpu_ctx::SceneCache{};
         ctx->scene_cache.bvh = build_bvh(tv, tobj);
         if (ctx->scene_cache.bvh.max_depth + 1 > static_cast<uint32_t>(kStack))

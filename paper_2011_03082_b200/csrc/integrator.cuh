@@ -47,11 +47,21 @@ SST_D R hg_eval(R g, R c) {
     return Real<R>::div_(R(kInv4PiD) * (R(1) - g * g), denom * Real<R>::sqrt_(denom));
 }
 
+// Shadow-ray length of a directional light (beyond every scene; FP32-representable).
+constexpr double kFarLight = 1e30;
+
 // NEE toward the point light from p (in object obj, channel c) with incoming w:
 // weight * Phi * hg(g, w.wl) * exp(-tau) / d^2.
 template <class R>
 SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<R> w, R weight,
                  uint64_t& tri_tests) {
+    if (sc.directional) {
+        // E * hg(g, w.wl) * exp(-tau), tau over the in-medium part of the ray out to the
+        // last boundary exit (closed meshes: every hit beyond it is an entry/exit pair).
+        const RayK<R> ray = make_ray(p, sc.light_dir);
+        const R tau = optical_depth(sc, ray, sc.t_min, R(kFarLight), c);
+        return weight * sc.power[c] * hg_eval(m.g, dot(w, sc.light_dir)) * Real<R>::exp_(R(-1) * tau);
+    }
     const V3<R> to_l = sc.light - p;
     const R d2 = dot(to_l, to_l);
     const R d = Real<R>::sqrt_(d2);

@@ -75,6 +75,8 @@ struct DevScene {
     const ObjK<R>* objs;
     uint32_t n_objects;
     V3<R> light;
+    V3<R> light_dir;  // directional light (unit, toward the light); used iff directional
+    int directional;
     R power[3], bg[3];
     V3<R> cam_pos, cam_fwd, cam_right, cam_up;
     R tan_half, aspect;

@@ -66,6 +66,8 @@ class Scene:
     r_min: float = 0.0
     max_pt_events: int = 0
     max_st_steps: int = 0
+    light_kind: int = 0  # 0 point (light_position, Phi), 1 directional (light_direction, E)
+    light_direction: Sequence[float] = (0.0, 1.0, 0.0)  # toward the light
     _keep: list = field(default_factory=list, repr=False)
 
     @property
@@ -103,7 +105,7 @@ class Scene:
         d.n_objects = len(self.objects)
         d.objects = C.cast(objs, C.POINTER(abi.ObjectDesc))
         for name in ("light_position", "light_power", "background", "cam_position", "cam_look_at",
-                     "cam_up"):
+                     "cam_up", "light_direction"):
             arr = getattr(d, name)
             for a, v in enumerate(getattr(self, name)):
                 arr[a] = float(v)
@@ -112,6 +114,7 @@ class Scene:
         d.r_min = self.r_min
         d.max_pt_events = self.max_pt_events
         d.max_st_steps = self.max_st_steps
+        d.light_kind = self.light_kind
         # the descriptor owns the buffers it points to (temporaries like
         # `Scene(...).to_desc()` must not leave dangling pointers)
         d._keep = keep

@@ -316,3 +316,35 @@ def test_density_doubling_st_sublinear(renderer, ico3):
             seg[(integ, sigma)] = s.segments
     assert seg[(PT, 160.0)] / seg[(PT, 80.0)] > 1.6
     assert seg[(ST, 160.0)] / seg[(ST, 80.0)] < 1.6
+
+
+@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
+def test_directional_light_paths_match_oracle(renderer, oracle, models_dir, ico3, precision, rtol, frac):
+    """Directional light (SPEC.md:598): no light grid, shadow rays to the last exit."""
+    from paper_2011_03082_b200.scene import SdfGrid, c5_scene
+    sc = c5_scene(ico3, 64, 36, sdf_resolution=24)
+    sc.light_kind, sc.light_direction, sc.light_power = 1, (-1.0, 0.4, 0.3), (3.0, 3.0, 3.0)
+    renderer.upload_scene(sc)
+    sdfs = [SdfGrid(*renderer.get_sdf(o)) for o in range(4)]
+    osc_scene = c5_scene(ico3, 64, 36)
+    osc_scene.light_kind, osc_scene.light_direction = sc.light_kind, sc.light_direction
+    osc_scene.light_power = sc.light_power
+    for o, g in zip(osc_scene.objects, sdfs):
+        o.sdf = g
+    osc = oracle.Scene(osc_scene.to_desc())
+    om = oracle.Models(models_dir)
+    rng = np.random.default_rng(23)
+    n = 3000
+    pix = rng.integers(0, 64 * 36, n)
+    smp = rng.integers(0, 1000, n)
+    ch = rng.integers(0, 3, n)
+    renderer.set_precision(precision)
+    try:
+        for integ in (0, 1):
+            g_rad, g_seg = renderer.trace_paths(integ, 1, 5, pix, smp, ch)
+            o_rad, o_seg = osc.trace_paths(om, integ, 1, 5, pix, smp, ch)
+            ok = (g_seg == o_seg) & (np.abs(g_rad - o_rad) <= 1e-12 + rtol * np.abs(o_rad))
+            assert ok.mean() >= frac, (precision, integ, ok.mean())
+            assert (o_rad > 0).mean() > 0.05
+    finally:
+        renderer.set_precision("f32")

@@ -56,11 +56,13 @@ def scenes():
     from paper_2011_03082_b200 import make_icosphere
     from paper_2011_03082_b200.scene import c1_scene, c5_scene
     mesh = make_icosphere(3, 1.0)
-    return {"c1": c1_scene(mesh, 64, 64), "c5": c5_scene(mesh, 192, 108)}
+    c5dir = c5_scene(mesh, 192, 108)  # directional light: BVH shadow rays, no light grid
+    c5dir.light_kind, c5dir.light_direction, c5dir.light_power = 1, (-1.0, 0.4, 0.3), (3.0, 3.0, 3.0)
+    return {"c1": c1_scene(mesh, 64, 64), "c5": c5_scene(mesh, 192, 108), "c5dir": c5dir}
 
 
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-@pytest.mark.parametrize("scene_name", ["c1", "c5"])
+@pytest.mark.parametrize("scene_name", ["c1", "c5", "c5dir"])
 def test_wavefront_paths_identical_to_megakernel(models_dir, scenes, precision, scene_name):
     from paper_2011_03082_b200 import abi
     scene = scenes[scene_name]

@@ -60,3 +60,27 @@ def test_integrator_live_res64(ref, oracle, models_dir):
         r1, s1 = rs.trace_paths(rm, integ, 1, 7, pix, smp, ch, abi.PathStats())
         r2, s2 = os_.trace_paths(om, integ, 1, 7, pix, smp, ch, abi.PathStats())
         assert (r1 == r2).all() and (s1 == s2).all()
+
+
+def test_integrator_live_directional_light(ref, oracle, models_dir):
+    """Directional light: reference-composed vs C-restated, bit-exact."""
+    from paper_2011_03082_b200 import abi, make_icosphere
+    from paper_2011_03082_b200.scene import SdfGrid, c1_scene
+    P, T = make_icosphere(3, 1.0)
+    sdf = SdfGrid(*ref.build_sdf(P, T, 32))
+    sc = c1_scene((P, T), 64, 64, sdf=sdf)
+    sc.light_kind, sc.light_direction, sc.light_power = 1, (0.3, 2.0, 1.0), (2.0, 2.0, 2.0)
+    desc = sc.to_desc()
+    rs = ref.Scene(C.byref(desc))
+    os_ = oracle.Scene(desc)
+    rng = np.random.default_rng(5)
+    n = 800
+    pix = rng.integers(0, 64 * 64, n)
+    smp = rng.integers(0, 64, n)
+    ch = rng.integers(0, 3, n)
+    rm, om = ref.Models(models_dir), oracle.Models(models_dir)
+    for integ in (0, 1):
+        r1, s1 = rs.trace_paths(rm, integ, 1, 7, pix, smp, ch, abi.PathStats())
+        r2, s2 = os_.trace_paths(om, integ, 1, 7, pix, smp, ch, abi.PathStats())
+        assert (r1 == r2).all() and (s1 == s2).all()
+        assert (r1 > 0).mean() > 0.05
