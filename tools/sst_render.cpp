@@ -27,7 +27,8 @@ struct Mesh {
 int usage() {
     std::fprintf(stderr,
                  "usage: sst_render --scene c1|c5 [--integrator st|pt] [--spp N] [--seed S] [--nee 0|1]\n"
-                 "                  [--width W] [--height H] [--models DIR] [--out F.pfm|F.png] [--precision f32|f64]\n");
+                 "                  [--width W] [--height H] [--models DIR] [--out F.pfm|F.png] [--precision f32|f64]\n"
+                 "                  [--dir-light X,Y,Z E]  (directional light toward X,Y,Z, irradiance E)\n");
     return 1;
 }
 
@@ -38,6 +39,8 @@ int main(int argc, char** argv) {
     uint32_t spp = 16, width = 0, height = 0;
     uint64_t seed = 1;
     int nee = 1;
+    double dir_light[3] = {0.0, 0.0, 0.0}, dir_e = 0.0;
+    bool directional = false;
     for (int i = 1; i < argc; ++i) {
         const std::string a = argv[i];
         auto next = [&]() -> const char* { return i + 1 < argc ? argv[++i] : nullptr; };
@@ -52,6 +55,12 @@ int main(int argc, char** argv) {
         else if (a == "--models" && (v = next())) models = v;
         else if (a == "--out" && (v = next())) out = v;
         else if (a == "--precision" && (v = next())) prec = v;
+        else if (a == "--dir-light" && (v = next())) {
+            const char* e = next();
+            if (!e || std::sscanf(v, "%lf,%lf,%lf", &dir_light[0], &dir_light[1], &dir_light[2]) != 3) return usage();
+            dir_e = std::atof(e);
+            directional = true;
+        }
         else return usage();
     }
     if ((scene != "c1" && scene != "c5") || (integ != "st" && integ != "pt") || spp == 0) return usage();
@@ -86,6 +95,13 @@ int main(int argc, char** argv) {
             d.light_position[a] = lp[a];
             d.light_power[a] = pw;
             d.cam_look_at[a] = 0.0;
+        }
+        if (directional) {
+            d.light_kind = 1;
+            for (int a = 0; a < 3; ++a) {
+                d.light_direction[a] = dir_light[a];
+                d.light_power[a] = dir_e;
+            }
         }
         d.cam_position[2] = scene == "c1" ? 3.0 : 7.5;
         d.cam_up[1] = 1.0;
