@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SST_GPU_ABI_VERSION 2
+#define SST_GPU_ABI_VERSION 3  /* 3: sst_scene_desc light_kind / light_direction */
 
 enum {
     SST_OK = 0,

@@ -149,6 +149,7 @@ EXPORTED = [
 ]
 
 _lib = None
+ABI_VERSION = 3  # include/sst_gpu.h SST_GPU_ABI_VERSION
 
 
 def lib():
@@ -159,8 +160,12 @@ def lib():
             raise RuntimeError(
                 f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
                 "there is no CPU fallback")
-        _lib = C.CDLL(LIB_PATH)
-        _declare(_lib)
+        L = C.CDLL(LIB_PATH)
+        _declare(L)
+        v = L.sst_gpu_abi_version()
+        if v != ABI_VERSION:
+            raise RuntimeError(f"{LIB_PATH} has ABI version {v}, these bindings expect {ABI_VERSION}: rebuild it")
+        _lib = L
     return _lib
 
 

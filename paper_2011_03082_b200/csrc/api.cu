@@ -139,6 +139,7 @@ struct sst_gpu_ctx {
     std::vector<double> weights;
     double norms[6] = {};
     uint64_t model_gen = 0;
+    uint64_t weights_fp = 0;  // fingerprint of (weights, norms): equal weights share the constant bank
 
     bool scene = false;
     uint64_t scene_bytes = 0, scene_bytes_grid = 0;
@@ -167,8 +168,12 @@ struct sst_gpu_ctx {
     // skip grid / convexity, and the scene BVH + light grid. Re-uploading an
     // unchanged scene recomputes nothing but still copies everything to the device.
     std::map<uint64_t, ObjectHost> obj_cache;
+    // The BVH is keyed by the geometry alone; the light grid by (geometry, light
+    // position), so a re-upload that moves only the light -- or any directional-light
+    // upload -- keeps the BVH.
     struct SceneCache {
-        uint64_t fp = 0;
+        uint64_t geo_fp = 0, grid_fp = 0;
+        bool have_bvh = false;
         FlatBvh bvh;
         std::vector<uint32_t> grid_off, grid_tri;
         uint32_t grid_res = 0;
@@ -220,8 +225,22 @@ struct sst_gpu_ctx {
 
 namespace {
 
-std::mutex g_const_mu;
-std::map<int, std::pair<const sst_gpu_ctx*, uint64_t>> g_const_owner;  // device -> (ctx, gen)
+// Decoder weights live in per-device __constant__ memory (FFMA operands, decoder.cuh).
+// Contexts on one device share it: the owner record says whose weights are resident.
+// Every launch that reads the weights first calls ensure_constants() and keeps the
+// returned lock until the launch is enqueued, so no other thread can swap the bank
+// in between. A swap to DIFFERENT weights first waits for every launch already
+// enqueued on the device (cudaDeviceSynchronize) -- some may belong to another
+// context's asynchronous renders -- and a context that lost the bank re-takes it
+// (same protocol) before its next launch, including the later iterations of its
+// draining wavefront jobs.
+std::recursive_mutex g_const_mu;
+struct ConstOwner {
+    const sst_gpu_ctx* ctx;
+    uint64_t gen;
+    uint64_t weights_fp;
+};
+std::map<int, ConstOwner> g_const_owner;  // device -> resident weights
 uint64_t g_serial = 0;
 
 uint64_t fnv(const void* data, size_t n, uint64_t h = 0xCBF29CE484222325ULL) {
@@ -238,15 +257,25 @@ void require_device(sst_gpu_ctx* ctx) {
     CK(cudaSetDevice(ctx->device));
 }
 
-// __constant__ memory is per device: re-upload when another context owns it.
-void ensure_constants(sst_gpu_ctx* ctx) {
+using ConstLock = std::unique_lock<std::recursive_mutex>;
+
+ConstLock ensure_constants(sst_gpu_ctx* ctx) {
     if (!ctx->models) throw InvalidArgument("no models uploaded (sst_gpu_upload_models / sst_gpu_load_models_dir)");
-    std::lock_guard<std::mutex> lk(g_const_mu);
+    ConstLock lk(g_const_mu);
     auto it = g_const_owner.find(ctx->device);
-    if (it != g_const_owner.end() && it->second.first == ctx && it->second.second == ctx->model_gen) return;
+    if (it != g_const_owner.end()) {
+        ConstOwner& o = it->second;
+        if (o.ctx == ctx && o.gen == ctx->model_gen) return lk;
+        if (o.weights_fp == ctx->weights_fp) {  // the same weights are resident: nothing to copy
+            o = {ctx, ctx->model_gen, ctx->weights_fp};
+            return lk;
+        }
+        CK(cudaDeviceSynchronize());  // launches that read the resident weights have finished
+    }
     CK(f32::upload_constants(ctx->weights.data(), ctx->norms, ctx->stream));
     CK(f64::upload_constants(ctx->weights.data(), ctx->norms, ctx->stream));
-    g_const_owner[ctx->device] = {ctx, ctx->model_gen};
+    g_const_owner[ctx->device] = {ctx, ctx->model_gen, ctx->weights_fp};
+    return lk;
 }
 
 void join_slots(sst_gpu_ctx* ctx);
@@ -262,6 +291,7 @@ void set_models(sst_gpu_ctx* ctx, const HostModel (&m)[3]) {
     }
     ctx->weights = std::move(w);
     std::memcpy(ctx->norms, norms, sizeof norms);
+    ctx->weights_fp = fnv(ctx->norms, sizeof ctx->norms, fnv(ctx->weights.data(), ctx->weights.size() * sizeof(double)));
     ctx->models = true;
     ctx->model_gen = ++g_serial;
 }
@@ -554,6 +584,9 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
 
 void ensure_film_staging(sst_gpu_ctx* ctx, uint64_t n);
 
+template <class Lap>
+void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool directional, Lap& lap);
+
 void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     const bool tdbg = std::getenv("SST_DEBUG_TIMING") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
@@ -566,6 +599,25 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
     if (!d || d->n_objects == 0 || !d->objects) throw InvalidArgument("scene has no objects");
     if (d->width == 0 || d->height == 0) throw InvalidArgument("camera resolution must be >= 1x1");
     if (!(d->cam_vfov_deg > 0.0 && d->cam_vfov_deg < 180.0)) throw InvalidArgument("camera fov out of range");
+    if (d->light_kind > 1) throw InvalidArgument("light_kind must be 0 (point) or 1 (directional)");
+    const bool directional = d->light_kind == 1;
+    if (directional && !(d->light_direction[0] * d->light_direction[0] + d->light_direction[1] * d->light_direction[1] +
+                             d->light_direction[2] * d->light_direction[2] > 0.0))
+        throw InvalidArgument("directional light needs a non-zero light_direction");
+    // From here on the previous scene's host objects may be moved into this upload;
+    // a failure past this point leaves NO scene (never a half-moved one).
+    try {
+        upload_scene_body(ctx, d, directional, lap);
+    } catch (...) {
+        ctx->scene = false;
+        ctx->objects.clear();
+        ctx->object_fp.clear();
+        throw;
+    }
+}
+
+template <class Lap>
+void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool directional, Lap& lap) {
     std::vector<ObjectHost> objs(d->n_objects);
     std::vector<uint64_t> objs_fp(d->n_objects, 0);
     std::vector<uint64_t> prev_fp;
@@ -647,30 +699,29 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         ctx->obj_cache[ofp] = objs[o];
     }
     lap("objects");
-    uint64_t sfp = fnv(tv.data(), tv.size() * sizeof(tv[0]));
-    sfp = fnv(tobj.data(), tobj.size() * sizeof(uint32_t), sfp);
-    sfp = fnv(d->light_position, sizeof d->light_position, sfp);
-    if (d->light_kind > 1) throw InvalidArgument("light_kind must be 0 (point) or 1 (directional)");
-    const bool directional = d->light_kind == 1;
-    if (directional && !(d->light_direction[0] * d->light_direction[0] + d->light_direction[1] * d->light_direction[1] +
-                             d->light_direction[2] * d->light_direction[2] > 0.0))
-        throw InvalidArgument("directional light needs a non-zero light_direction");
-    const bool cached = !directional && ctx->scene_cache.fp == sfp && ctx->scene_cache.grid_res;
-    if (directional) {  // no light-space grid (it is a cube map around a point light)
-        ctx->scene_cache = sst_gpu_ctx::SceneCache{};
-        ctx->scene_cache.bvh = build_bvh(tv, tobj);
-        if (ctx->scene_cache.bvh.max_depth + 1 > static_cast<uint32_t>(kStack))
+    uint64_t gfp = fnv(tv.data(), tv.size() * sizeof(tv[0]));
+    gfp = fnv(tobj.data(), tobj.size() * sizeof(uint32_t), gfp);
+    const uint64_t lfp = fnv(d->light_position, sizeof d->light_position, gfp);
+    auto& cache = ctx->scene_cache;
+    const bool bvh_cached = cache.have_bvh && cache.geo_fp == gfp;
+    if (!bvh_cached) {
+        cache = sst_gpu_ctx::SceneCache{};
+        FlatBvh b = build_bvh(tv, tobj);
+        if (b.max_depth + 1 > static_cast<uint32_t>(kStack))
             throw InvalidArgument("BVH deeper than the traversal stack (" + std::to_string(kStack) + ")");
+        cache.bvh = std::move(b);
+        cache.geo_fp = gfp;
+        cache.have_bvh = true;
+    }
+    const bool cached = !directional && cache.grid_fp == lfp && cache.grid_res;
+    if (directional) {  // no light-space grid (it is a cube map around a point light)
         ctx->grid_res = 0;
         ctx->scene_bytes_grid = 0;
         ctx->grid_list_n = 0;
     } else if (!cached) {
-        ctx->scene_cache = sst_gpu_ctx::SceneCache{};
-        ctx->scene_cache.bvh = build_bvh(tv, tobj);
-        if (ctx->scene_cache.bvh.max_depth + 1 > static_cast<uint32_t>(kStack))
-            throw InvalidArgument("BVH deeper than the traversal stack (" + std::to_string(kStack) + ")");
-        build_light_grid(ctx, d, tv, ctx->scene_cache.bvh);
-        ctx->scene_cache.fp = sfp;
+        cache.grid_fp = 0;
+        build_light_grid(ctx, d, tv, cache.bvh);
+        cache.grid_fp = lfp;
     } else {  // copy the cached light grid to the device (inputs travel every upload)
         const auto& sc = ctx->scene_cache;
         ctx->grid_off.reserve(sc.grid_off.size() * sizeof(uint32_t));
@@ -685,7 +736,7 @@ void upload_scene(sst_gpu_ctx* ctx, const sst_scene_desc* d) {
         ctx->grid_list_n = sc.grid_tri.size();
     }
     const FlatBvh& bvh = ctx->scene_cache.bvh;
-    lap(cached ? "bvh+grid(hit)" : "bvh+grid(build)");
+    lap(bvh_cached ? (cached ? "bvh+grid(hit)" : "bvh(hit)") : "bvh+grid(build)");
     // upload
     ctx->objects = std::move(objs);
     ctx->object_fp = std::move(objs_fp);
@@ -845,6 +896,8 @@ struct WfJob final : WfJobBase {
     bool supply_done() const override { return supply; }
 
     void launch_batch() {
+        ConstLock lk;  // sphere steps read the decoder constants (ensure_constants)
+        if (st) lk = ensure_constants(ctx);
         for (int b = 0; b < batch; ++b, ++it) {
             const bool even = (it & 1) == 0;  // live lists ping-pong: A -> B -> A ...
             a.pool.q_in = full ? nullptr : (even ? a.pool.q_la : a.pool.q_lb);
@@ -908,6 +961,8 @@ struct WfJob final : WfJobBase {
         }
         if (done) {
             if (!may_finish) return progressed ? 1 : 0;
+            ConstLock lk;
+            if (st) lk = ensure_constants(ctx);
             kt_begin(ctx, stream);
             if constexpr (std::is_same<R, float>::value) CK(f32::launch_wf_finish(a, st, ex, stream));
             else CK(f64::launch_wf_finish(a, st, ex, stream));
@@ -1023,6 +1078,8 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
         run_wavefront<R>(ctx, a, st, explicit_keys, *wf, stream, std::move(on_finish), sync);
         return;
     }
+    ConstLock lk;
+    if (st) lk = ensure_constants(ctx);
     kt_begin(ctx, stream);
     if constexpr (std::is_same<R, float>::value) CK(f32::launch_trace(a, st, explicit_keys, stream));
     else CK(f64::launch_trace(a, st, explicit_keys, stream));
@@ -1150,28 +1207,46 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         CK(cudaEventRecord(ctx->ev0, ctx->stream));
         ctx->timing_open = true;
     }
+    // Pipeline slots of this call: asynchronous calls rotate over all kSlots (their
+    // drains overlap later calls); a synchronous call uses slots 0 .. (its chunk count
+    // - 1) only, so a one-chunk host-film render keeps ONE slot's buffers resident.
+    const uint32_t n_chunks = (n_samples + chunk - 1) / chunk;
+    const int n_slots = sync ? static_cast<int>(std::min<uint32_t>(sst_gpu_ctx::kSlots, n_chunks))
+                             : sst_gpu_ctx::kSlots;
     if (use_wavefront(ctx, integrator == SST_INTEGRATOR_ST)) {
-        // Every pipeline slot gets its radiance scratch and wavefront pool now (grow-only):
-        // a slot first used later -- e.g. inside a timed or latency-sensitive stretch of
-        // calls -- would otherwise cudaFree/cudaMalloc (device-synchronising) mid-pipeline.
+        // The slots this call may use get their radiance scratch and wavefront pool now
+        // (grow-only): a slot first used later -- e.g. inside a timed or
+        // latency-sensitive stretch of calls -- would otherwise cudaFree/cudaMalloc
+        // (device-synchronising) mid-pipeline.
         size_t off[22];
         const uint64_t cap = std::max<uint64_t>(32, std::min<uint64_t>(per_sample * chunk, ctx->wf_pool));
         const size_t pool = pool_layout<R>(static_cast<uint32_t>(cap), off);
         bool grow = false;
-        for (auto& s2 : ctx->slots) grow |= s2.rad.bytes < per_sample * chunk * sizeof(R) || s2.wf.bytes < pool;
+        for (int k = 0; k < n_slots; ++k) {
+            const auto& s2 = ctx->slots[k];
+            grow |= s2.rad.bytes < per_sample * chunk * sizeof(R) || s2.wf.bytes < pool;
+        }
         if (grow) {
             drain_jobs(ctx);
-            for (auto& s2 : ctx->slots) {
-                s2.rad.reserve(per_sample * chunk * sizeof(R));
-                s2.wf.reserve(pool);
+            for (int k = 0; k < n_slots; ++k) {
+                ctx->slots[k].rad.reserve(per_sample * chunk * sizeof(R));
+                ctx->slots[k].wf.reserve(pool);
             }
         }
     }
     CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+    int sync_slot = 0;
     for (uint32_t s = s0; s < s1; s += chunk) {
         const uint32_t ns = std::min(chunk, s1 - s);
-        auto& sl = ctx->slots[ctx->next_slot];
-        ctx->next_slot = (ctx->next_slot + 1) % sst_gpu_ctx::kSlots;
+        int slot_index;
+        if (sync) {
+            slot_index = sync_slot;
+            sync_slot = (sync_slot + 1) % n_slots;
+        } else {
+            slot_index = ctx->next_slot;
+            ctx->next_slot = (ctx->next_slot + 1) % sst_gpu_ctx::kSlots;
+        }
+        auto& sl = ctx->slots[slot_index];
         wait_slot(ctx, &sl);  // a job still draining on this slot owns its buffers
         sl.rad.reserve(per_sample * chunk * sizeof(R));
         CK(cudaStreamWaitEvent(sl.s, ctx->ev_start, 0));
@@ -1342,9 +1417,11 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
     }
     cudaStreamSynchronize(ctx->stream);
     {
-        std::lock_guard<std::mutex> lk(g_const_mu);
+        // the weights stay resident (other contexts with equal weights may be reading
+        // them): forget only the owner, so a later swap still waits for the device
+        const ConstLock lk(g_const_mu);
         auto it = g_const_owner.find(ctx->device);
-        if (it != g_const_owner.end() && it->second.first == ctx) g_const_owner.erase(it);
+        if (it != g_const_owner.end() && it->second.ctx == ctx) it->second.ctx = nullptr;
     }
     for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri, &ctx->grid_tris32,
                       &ctx->radiance, &ctx->segments, &ctx->work, &ctx->stats, &ctx->error, &ctx->film_sum,
@@ -1474,7 +1551,7 @@ int sst_gpu_sphere_step_batch(sst_gpu_ctx* ctx, uint64_t n, const sst_step_in* i
         require_device(ctx);
         if (!in || !out) throw InvalidArgument("null batch descriptors");
         if (ptr_kind != SST_PTR_HOST && ptr_kind != SST_PTR_DEVICE) throw InvalidArgument("bad ptr_kind");
-        ensure_constants(ctx);
+        const ConstLock lk = ensure_constants(ctx);
         if (n == 0) return;
         if (ptr_kind == SST_PTR_HOST) {
             for (uint64_t i = 0; i < n; ++i) {

@@ -1,7 +1,10 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the sample-slab sharding and the
-film reduce (paper_2011_03082_b200/dist.py). The per-rank slab renderer is the C
-oracle on a tiny scene, so the test exercises the real partition and exchange
-logic without a GPU; on B200 the same code path runs with NCCL (bench.py)."""
+"""Multi-process (world_size 2 and 4, gloo, CPU) tests of the sample-slab sharding and
+the fixed-order film reduce (paper_2011_03082_b200/dist.py). The per-rank slab renderer
+is the C oracle on a tiny scene, so the test exercises the real partition and exchange
+logic without a GPU; on B200 the same code path runs with NCCL (bench.py).
+
+The films of 1, 2 and 4 ranks must be BIT-identical (canonical sample groups added in
+group order), not merely close."""
 import os
 import socket
 import sys
@@ -11,7 +14,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 W = H = 6
-SPP = 7
+SPP = 11  # 8 canonical groups of 1-2 samples: uneven groups
 
 
 def test_sample_slabs_partition_the_frame():
@@ -62,6 +65,7 @@ def _worker(rank, world, port, out_dir):
         return st
 
     fsum, fsq, stats = render_frame(slab, W * H * 3, SPP)
+    assert (fsum is None) == (rank != 0)
     if rank == 0:
         np.savez(os.path.join(out_dir, "r0.npz"), sum=fsum.numpy(), sq=fsq.numpy(), st=stats.numpy())
     dist.barrier()
@@ -76,17 +80,47 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
-def test_two_rank_gloo_film_reduce_equals_single_process(tmp_path, world):
+def test_canonical_groups_cover_the_frame():
+    from paper_2011_03082_b200.dist import FRAME_GROUPS, group_owners, group_slab, groups_of_rank
+    for world in (1, 2, 3, 4, 8):
+        got = [g for r in range(world) for g in groups_of_rank(r, world)]
+        assert got == list(range(FRAME_GROUPS))
+        assert group_owners(world) == [r for r in range(world) for _ in groups_of_rank(r, world)]
+    for spp in (1, 11, 5000):
+        slabs = [group_slab(g, spp) for g in range(FRAME_GROUPS)]
+        assert slabs[0][0] == 0 and slabs[-1][1] == spp
+        assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+
+
+def _single_process_frame():
+    import torch
+
+    from paper_2011_03082_b200.dist import render_frame
+
+    def slab(s0, s1, fsum, fsq):
+        fs, fq, st = _oracle_slab(s0, s1)
+        fsum += torch.from_numpy(fs)
+        fsq += torch.from_numpy(fq)
+        return st
+
+    fsum, fsq, stats = render_frame(slab, W * H * 3, SPP)
+    return fsum.numpy(), fsq.numpy(), stats.numpy()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_film_reduce_bit_identical_to_single_process(tmp_path, world):
     pytest.importorskip("torch")
     import torch.multiprocessing as mp
     port = _free_port()
     mp.start_processes(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
     got = np.load(tmp_path / "r0.npz")
+    fs1, fq1, st1 = _single_process_frame()
+    # same paths (keyed RNG), same canonical groups, same addition order -> bit-identical
+    assert (got["sum"] == fs1).all() and (got["sq"] == fq1).all()
+    assert (got["st"] == st1).all()
+    assert st1[0] == W * H * 3 * SPP
+    # and equal (up to FP64 summation order) to one oracle render of the whole frame
     fs, fq, st = _oracle_slab(0, SPP)
-    # same paths (keyed RNG); only the FP64 summation order differs
-    assert np.allclose(got["sum"], fs, rtol=1e-12, atol=1e-300)
-    assert np.allclose(got["sq"], fq, rtol=1e-12, atol=1e-300)
-    assert (got["st"] == st).all()
-    assert st[0] == W * H * 3 * SPP
+    assert np.allclose(fs1, fs, rtol=1e-12, atol=1e-300)
+    assert (st == st1).all()

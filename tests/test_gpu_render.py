@@ -7,9 +7,14 @@ Tolerances:
       equality is not reachable: CUDA libm and glibc differ by ulps, and the
       reference's grazing-exit normal component sqrt(1 - a^2 - b^2) (scatter.cpp:124)
       turns a 1e-16 difference after the unit-disk projection into ~1e-8.
-  Per-path, FP32: segment counts identical and radiance within 1e-3 relative
-      (+1e-7 absolute) on >= 98% of paths; FP32 position rounding near a voxel or
-      boundary makes a path take a different (equally valid) branch.
+  Per-path, FP32: gates just below the rates measured on B200 (tools/parity_rates.py,
+      profiles/r02/parity_rates.json): sigma_t = 10 scenes >= 99.8% of paths within
+      1e-4 relative; the multi-medium scenes (sigma_t up to 160) >= 99.7% within 1e-3
+      and the bumpy sigma_t = 40 scene >= 99.8% within 1e-3 / 97% within 1e-4. FP32
+      state drift (~1 ulp per event) is multiplied by sigma_t through Beer-Lambert,
+      which is what bounds the 1e-4 rate of dense media.
+  Every per-path oracle test runs on both engines: the register-resident megakernel
+  (small launches) and the wavefront kernels the bench times (SST_WF_MIN_PATHS=0).
   Images: per-pixel 3-sigma test between independent GPU and oracle renders
       (<= 1.5% of pixel-channels outside, expected 0.27%), RMSE within 1.5x the
       combined Monte Carlo standard error.
@@ -24,6 +29,33 @@ pytestmark = pytest.mark.gpu
 def ico3():
     from paper_2011_03082_b200 import make_icosphere
     return make_icosphere(3, 1.0)
+
+
+@pytest.fixture(scope="module")
+def wf_renderer(models_dir):
+    """A context that runs every launch on the wavefront kernels (SST_WF_MIN_PATHS=0)."""
+    import os
+
+    from paper_2011_03082_b200 import Renderer
+    saved = {k: os.environ.get(k) for k in ("SST_WF_MIN_PATHS", "SST_WAVEFRONT")}
+    os.environ["SST_WF_MIN_PATHS"] = "0"
+    os.environ.pop("SST_WAVEFRONT", None)
+    try:
+        r = Renderer(0, "f32")
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    r.load_models_dir(models_dir)
+    yield r
+    r.close()
+
+
+@pytest.fixture(params=["megakernel", "wavefront"])
+def engine(request, renderer, wf_renderer):
+    return renderer if request.param == "megakernel" else wf_renderer
 
 
 def _golden_sdf(golden, name):
@@ -65,8 +97,8 @@ def _golden_paths(renderer, golden, ico3, precision):
     return res
 
 
-def test_f64_paths_match_reference_golden(renderer, golden, ico3):
-    res = _golden_paths(renderer, golden, ico3, "f64")
+def test_f64_paths_match_reference_golden(engine, golden, ico3):
+    res = _golden_paths(engine, golden, ico3, "f64")
     for (integ, nee), (rad, seg) in res.items():
         ref_r = golden[f"path_{integ}{nee}_radiance"]
         ref_s = golden[f"path_{integ}{nee}_segments"]
@@ -74,13 +106,14 @@ def test_f64_paths_match_reference_golden(renderer, golden, ico3):
         assert ok.mean() >= 0.999, ((integ, nee), ok.mean())
 
 
-def test_f32_paths_match_reference_golden(renderer, golden, ico3):
-    res = _golden_paths(renderer, golden, ico3, "f32")
+def test_f32_paths_match_reference_golden(engine, golden, ico3):
+    res = _golden_paths(engine, golden, ico3, "f32")
     for (integ, nee), (rad, seg) in res.items():
         ref_r = golden[f"path_{integ}{nee}_radiance"]
         ref_s = golden[f"path_{integ}{nee}_segments"]
-        ok = (seg == ref_s) & (np.abs(rad - ref_r) <= 1e-7 + 1e-3 * np.abs(ref_r))
-        assert ok.mean() >= 0.98, ((integ, nee), ok.mean())
+        ok4 = (seg == ref_s) & (np.abs(rad - ref_r) <= 1e-12 + 1e-4 * np.abs(ref_r))
+        ok3 = (seg == ref_s) & (np.abs(rad - ref_r) <= 1e-12 + 1e-3 * np.abs(ref_r))
+        assert ok4.mean() >= 0.998 and ok3.mean() >= 0.999, ((integ, nee), ok4.mean(), ok3.mean())
 
 
 def test_render_deterministic_and_slab_additive(renderer, ico3):
@@ -179,8 +212,9 @@ def test_async_pipelined_render_equals_sync(renderer, ico3):
     assert np.allclose(s.cpu().numpy(), ref.sum, rtol=1e-12, atol=1e-15)
 
 
-@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
-def test_multi_object_scene_paths_match_oracle(renderer, oracle, models_dir, ico3, precision, rtol, frac):
+@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.997)])
+def test_multi_object_scene_paths_match_oracle(engine, oracle, models_dir, ico3, precision, rtol, frac):
+    renderer = engine
     """C5-style scene (4 media; shadow rays crossing other objects, light grid culling)."""
     from paper_2011_03082_b200.scene import SdfGrid, c5_scene
     sc = c5_scene(ico3, 64, 36, sdf_resolution=24)
@@ -244,8 +278,10 @@ def test_fp32_leak_recovery_bounds_path_length():
         r.close()
 
 
-@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
-def test_nonconvex_bumpy_scene_paths_match_oracle(renderer, oracle, models_dir, precision, rtol, frac):
+@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.998),
+                                                  ("f32", 1e-4, 0.97)])
+def test_nonconvex_bumpy_scene_paths_match_oracle(engine, oracle, models_dir, precision, rtol, frac):
+    renderer = engine
     """Config-3 geometry (bumpy sphere, non-convex: no exit culling; FP32 relies on the
     orientation-aware hits), density 40, both integrators, NEE on."""
     from paper_2011_03082_b200 import make_bumpy_sphere
@@ -318,8 +354,9 @@ def test_density_doubling_st_sublinear(renderer, ico3):
     assert seg[(ST, 160.0)] / seg[(ST, 80.0)] < 1.6
 
 
-@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.98)])
-def test_directional_light_paths_match_oracle(renderer, oracle, models_dir, ico3, precision, rtol, frac):
+@pytest.mark.parametrize("precision,rtol,frac", [("f64", 1e-6, 0.999), ("f32", 1e-3, 0.997)])
+def test_directional_light_paths_match_oracle(engine, oracle, models_dir, ico3, precision, rtol, frac):
+    renderer = engine
     """Directional light (SPEC.md:598): no light grid, shadow rays to the last exit."""
     from paper_2011_03082_b200.scene import SdfGrid, c5_scene
     sc = c5_scene(ico3, 64, 36, sdf_resolution=24)
