@@ -40,6 +40,26 @@ int sst_dataset_save(const char* path, uint64_t count, float sigma_t_lo, float s
                      float g_hi, uint32_t phi_kind, float phi_a, float phi_b, uint64_t seed,
                      const void* samples);
 
+/* DatasetHeader (dataset.hpp:43-50) as stored in an SSWK file. */
+typedef struct sst_dataset_header {
+    uint32_t version;
+    uint64_t count;
+    float sigma_t_lo, sigma_t_hi, g_lo, g_hi;
+    uint32_t phi_kind; /* PhiSampler::Kind */
+    float phi_a, phi_b;
+    uint64_t seed;
+} sst_dataset_header;
+
+/* load_dataset (dataset.cpp:121-151): SSWK v1. Call with samples == NULL to read the
+ * header (count) only, then with a buffer of >= header->count 52-byte records
+ * (capacity = records it holds). Errors as the reference's (SST_E_RUNTIME): missing
+ * file, "dataset <path>: bad magic bytes", "...: unsupported version",
+ * "...: truncated or corrupt file"; capacity < count is SST_E_INVALID_ARGUMENT. */
+int sst_dataset_load(const char* path, sst_dataset_header* header, void* samples, uint64_t capacity);
+
+/* export_dataset_csv (dataset.cpp:153-164): header line + one "%.9g" row per record. */
+int sst_dataset_export_csv(const char* path, uint64_t count, const void* samples);
+
 /* save_pfm (image.cpp:32-41): little-endian "PF", bottom row first. */
 int sst_image_save_pfm(const char* path, uint32_t width, uint32_t height, const float* rgb);
 

@@ -287,6 +287,36 @@ int ref_save_dataset(const char* path, uint64_t n, double s_lo, double s_hi, dou
     });
 }
 
+// load_dataset (dataset.cpp:121-151): hdr = {version, sigma_t_lo, sigma_t_hi, g_lo, g_hi,
+// phi_kind, phi_a, phi_b}; the records are copied when samples != nullptr.
+int ref_load_dataset(const char* path, double hdr[8], uint64_t* count, uint64_t* seed, void* samples,
+                     uint64_t capacity) {
+    return guarded([&] {
+        const Dataset ds = load_dataset(path);
+        const DatasetHeader& h = ds.header;
+        const double v[8] = {double(h.version), h.sigma_t_lo, h.sigma_t_hi, h.g_lo, h.g_hi,
+                             double(static_cast<uint32_t>(h.phi.kind)), h.phi.a, h.phi.b};
+        std::memcpy(hdr, v, sizeof v);
+        *count = h.count;
+        *seed = h.seed;
+        if (samples) {
+            if (capacity < ds.samples.size()) throw std::invalid_argument("capacity");
+            std::memcpy(samples, ds.samples.data(), ds.samples.size() * sizeof(TrainingSample));
+        }
+    });
+}
+
+// export_dataset_csv (dataset.cpp:153-164) of n records.
+int ref_export_dataset_csv(const char* path, uint64_t n, const void* samples) {
+    return guarded([&] {
+        Dataset ds;
+        ds.header.count = n;
+        ds.samples.resize(n);
+        std::memcpy(ds.samples.data(), samples, n * sizeof(TrainingSample));
+        export_dataset_csv(path, ds);
+    });
+}
+
 // save_png (image.cpp:101-138) for the PNG byte-compatibility test. (The reference's PFM
 // writers/reader use iostream number formatting, which crashes when this library is
 // dlopen'ed into Python next to the system libstdc++; the PFM tests check the format directly.)

@@ -69,6 +69,8 @@ def _declare(L):
     L.ref_train_model.argtypes = [I, P, U64, U64, P, C.c_char_p, I, P, P, P]
     L.ref_save_dataset.argtypes = [C.c_char_p, U64, D, D, D, D, I, D, D, U64, P]
     L.ref_save_png.argtypes = [C.c_char_p, U32, U32, P]
+    L.ref_load_dataset.argtypes = [C.c_char_p, P, P, P, P, U64]
+    L.ref_export_dataset_csv.argtypes = [C.c_char_p, U64, P]
     L.ref_make_icosphere.argtypes = [I, D, P, P, P, P]
     L.ref_make_icosphere.restype = None
     L.ref_make_bumpy_sphere.argtypes = [I, D, D, D, P, P, P, P]

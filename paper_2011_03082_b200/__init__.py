@@ -7,10 +7,10 @@ in libsst_gpu.so (hand-written CUDA for sm_100a behind a C ABI, include/sst_gpu.
 this package is the Python host mirror. See DESIGN.md.
 """
 from . import abi  # noqa: F401
-from .api import (PT, ST, Film, Image, Renderer, image_metrics, load_obj,  # noqa: F401
-                  make_bumpy_sphere, make_icosphere, rng_init, save_dataset)
+from .api import (PT, ST, Film, Image, Renderer, export_dataset_csv, image_metrics, load_dataset,  # noqa: F401
+                  load_obj, make_bumpy_sphere, make_icosphere, rng_init, save_dataset)
 from .scene import Medium, Scene, SceneObject, SdfGrid, c1_scene, c3_scene, c5_scene, uniform_media  # noqa: F401
 
 __all__ = ["abi", "PT", "ST", "Film", "Image", "Renderer", "image_metrics", "load_obj",
-           "make_bumpy_sphere", "make_icosphere", "rng_init", "save_dataset", "Medium", "Scene", "SceneObject",
+           "make_bumpy_sphere", "make_icosphere", "rng_init", "save_dataset", "load_dataset", "export_dataset_csv", "Medium", "Scene", "SceneObject",
            "SdfGrid", "c1_scene", "c3_scene", "c5_scene", "uniform_media"]

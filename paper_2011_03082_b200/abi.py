@@ -101,6 +101,13 @@ class DatasetStats(C.Structure):
                 ("device_ms", D)]
 
 
+class DatasetHeader(C.Structure):
+    """sst_dataset_header (include/sst_host.h) = DatasetHeader (dataset.hpp:43-50)."""
+    _fields_ = [("version", U32), ("count", U64), ("sigma_t_lo", C.c_float), ("sigma_t_hi", C.c_float),
+                ("g_lo", C.c_float), ("g_hi", C.c_float), ("phi_kind", U32), ("phi_a", C.c_float),
+                ("phi_b", C.c_float), ("seed", U64)]
+
+
 class TrainConfig(C.Structure):
     """TrainConfig (cvae.hpp:101-114); defaults are the reference's."""
     _fields_ = [("lr", D), ("batch_size", U32), ("epochs", U32), ("weight_decay", D), ("seed", U64),
@@ -145,7 +152,8 @@ EXPORTED = [
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
     "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm", "sst_dataset_save",
-    "sst_image_save_pfm_gray", "sst_image_load_pfm", "sst_image_save_png",
+    "sst_image_save_pfm_gray", "sst_image_load_pfm", "sst_image_save_png", "sst_dataset_load",
+    "sst_dataset_export_csv",
 ]
 
 _lib = None
@@ -200,6 +208,8 @@ def _declare(L):
     L.sst_gpu_train_models.argtypes = [P, P, U64, I, U64, P, P, C.c_char_p, I, I, P]
     L.sst_dataset_save.argtypes = [C.c_char_p, U64, C.c_float, C.c_float, C.c_float, C.c_float, U32,
                                    C.c_float, C.c_float, U64, P]
+    L.sst_dataset_load.argtypes = [C.c_char_p, C.POINTER(DatasetHeader), P, U64]
+    L.sst_dataset_export_csv.argtypes = [C.c_char_p, U64, P]
     L.sst_gpu_trace_paths.argtypes = [P, I, I, U64, U64, P, P, P, P, P, C.POINTER(PathStats)]
     L.sst_mesh_icosphere.argtypes = [I, D, P, P, P, P]
     L.sst_mesh_bumpy_sphere.argtypes = [I, D, D, D, P, P, P, P]

@@ -57,6 +57,22 @@ def save_dataset(path, samples, sigma_t, g, phi, seed):
                                          int(phi[0]), phi[1], phi[2], seed, _p(samples)))
 
 
+def load_dataset(path):
+    """load_dataset (dataset.cpp:121-151): (abi.DatasetHeader, TrainingSample records)."""
+    L = abi.lib()
+    h = abi.DatasetHeader()
+    abi.check(L.sst_dataset_load(path.encode(), C.byref(h), None, 0))
+    out = np.zeros(h.count, dtype=abi.SAMPLE_DTYPE)
+    abi.check(L.sst_dataset_load(path.encode(), C.byref(h), _p(out), len(out)))
+    return h, out
+
+
+def export_dataset_csv(path, samples):
+    """export_dataset_csv (dataset.cpp:153-164)."""
+    samples = np.ascontiguousarray(samples, dtype=abi.SAMPLE_DTYPE)
+    abi.check(abi.lib().sst_dataset_export_csv(path.encode(), len(samples), _p(samples)))
+
+
 def make_icosphere(subdivisions: int = 3, radius: float = 1.0):
     return _mesh_out(abi.lib().sst_mesh_icosphere, subdivisions, radius)
 

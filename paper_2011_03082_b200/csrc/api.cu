@@ -1901,6 +1901,63 @@ int sst_dataset_save(const char* path, uint64_t count, float s_lo, float s_hi, f
     });
 }
 
+int sst_dataset_load(const char* path, sst_dataset_header* header, void* samples, uint64_t capacity) {
+    return guarded([&] {
+        if (!path || !header) throw InvalidArgument("null argument");
+        std::ifstream f(path, std::ios::binary);
+        if (!f) throw RuntimeError(std::string("cannot open for reading: ") + path);
+        const std::string what = std::string("dataset ") + path;
+        char magic[4];
+        f.read(magic, 4);
+        if (!f || std::memcmp(magic, "SSWK", 4) != 0) throw RuntimeError(what + ": bad magic bytes");
+        auto get = [&](void* p, size_t n) { f.read(static_cast<char*>(p), static_cast<std::streamsize>(n)); };
+        sst_dataset_header h{};
+        get(&h.version, 4);
+        if (!f) throw RuntimeError(what + ": truncated or corrupt file");
+        if (h.version != 1) throw RuntimeError(what + ": unsupported version");
+        get(&h.count, 8);
+        get(&h.sigma_t_lo, 4);
+        get(&h.sigma_t_hi, 4);
+        get(&h.g_lo, 4);
+        get(&h.g_hi, 4);
+        get(&h.phi_kind, 4);
+        get(&h.phi_a, 4);
+        get(&h.phi_b, 4);
+        get(&h.seed, 8);
+        if (!f) throw RuntimeError(what + ": truncated or corrupt file");
+        // the records must all be there (the reference reads them and checks the stream)
+        const std::streamoff here = f.tellg();
+        f.seekg(0, std::ios::end);
+        const std::streamoff end = f.tellg();
+        f.seekg(here);
+        const uint64_t rec = sizeof(TrainingSampleDev);
+        if (end < here || static_cast<uint64_t>(end - here) / rec < h.count)
+            throw RuntimeError(what + ": truncated or corrupt file");
+        *header = h;
+        if (!samples) return;
+        if (capacity < h.count) throw InvalidArgument("sample buffer smaller than the dataset");
+        get(samples, h.count * rec);  // records are the packed little-endian fields
+        if (!f) throw RuntimeError(what + ": truncated or corrupt file");
+    });
+}
+
+int sst_dataset_export_csv(const char* path, uint64_t count, const void* samples) {
+    return guarded([&] {
+        if (!path || (!samples && count)) throw InvalidArgument("null argument");
+        std::FILE* f = std::fopen(path, "w");
+        if (!f) throw RuntimeError(std::string("cannot open for writing: ") + path);
+        std::fputs("sigma_t,g,phi,n_events,cos_theta,alpha,beta,X0,X1,X2,W0,W1,W2\n", f);
+        const auto* s = static_cast<const TrainingSampleDev*>(samples);
+        for (uint64_t i = 0; i < count; ++i) {
+            const TrainingSampleDev& r = s[i];
+            std::fprintf(f, "%.9g,%.9g,%.9g,%u,%.9g,%.9g,%.9g,%.9g,%.9g,%.9g,%.9g,%.9g,%.9g\n", r.sigma_t, r.g,
+                         r.phi, r.n_events, r.cos_theta, r.alpha, r.beta, r.rep_position[0], r.rep_position[1],
+                         r.rep_position[2], r.rep_direction[0], r.rep_direction[1], r.rep_direction[2]);
+        }
+        if (std::fclose(f) != 0) throw RuntimeError(std::string("write failure: ") + path);
+    });
+}
+
 int sst_image_save_pfm(const char* path, uint32_t w, uint32_t h, const float* rgb) {
     return guarded([&] {
         if (!path || !rgb) throw InvalidArgument("null argument");

@@ -44,6 +44,63 @@ def test_sswk_writer_matches_reference(golden, tmp_path):
     assert open(p, "rb").read() == golden["ds_b_sswk"].tobytes()
 
 
+def test_sswk_reader_matches_reference(golden, tmp_path):
+    """load_dataset (dataset.cpp:121-151) of the reference's own SSWK bytes: same header
+    and records; the reference's loader reads our writer's file identically."""
+    import paper_2011_03082_b200 as sb
+    p = str(tmp_path / "ref.sswk")
+    open(p, "wb").write(golden["ds_b_sswk"].tobytes())
+    h, recs = sb.load_dataset(p)
+    ds = _golden(golden, "ds_b")
+    assert h.version == 1 and h.count == len(ds) and h.seed == 12
+    assert (h.sigma_t_lo, h.sigma_t_hi, h.g_lo, h.g_hi) == (0.0, 200.0, -1.0, 1.0)
+    assert (h.phi_kind, h.phi_a, h.phi_b) == (0, -5.0, -0.5)
+    assert recs.tobytes() == np.ascontiguousarray(ds).tobytes()
+    # round trip through our writer
+    q = str(tmp_path / "ours.sswk")
+    sb.save_dataset(q, recs, (h.sigma_t_lo, h.sigma_t_hi), (h.g_lo, h.g_hi), (h.phi_kind, h.phi_a, h.phi_b), h.seed)
+    assert open(q, "rb").read() == golden["ds_b_sswk"].tobytes()
+
+
+def test_sswk_reader_errors_mirror_reference(golden, tmp_path):
+    import paper_2011_03082_b200 as sb
+    from paper_2011_03082_b200 import abi
+    raw = golden["ds_b_sswk"].tobytes()
+    cases = {"magic": b"XXXX" + raw[4:], "version": raw[:4] + b"\x02\x00\x00\x00" + raw[8:],
+             "truncated": raw[:-7], "header": raw[:20]}
+    msgs = {"magic": "bad magic bytes", "version": "unsupported version", "truncated": "truncated or corrupt",
+            "header": "truncated or corrupt"}
+    for k, b in cases.items():
+        p = str(tmp_path / f"{k}.sswk")
+        open(p, "wb").write(b)
+        with pytest.raises(abi.SstError, match=msgs[k]):
+            sb.load_dataset(p)
+    with pytest.raises(abi.SstError, match="cannot open"):
+        sb.load_dataset(str(tmp_path / "missing.sswk"))
+
+
+def test_sswk_reader_and_csv_match_reference_library(ref, oracle, tmp_path):
+    """Live against the reference library: its load_dataset and export_dataset_csv."""
+    import ctypes as C
+
+    import paper_2011_03082_b200 as sb
+    ds = oracle.generate_dataset(257, sigma=(0.0, 60.0), g=(-0.5, 0.9), seed=31)
+    p = str(tmp_path / "d.sswk")
+    sb.save_dataset(p, ds, (0.0, 60.0), (-0.5, 0.9), (2, 0.9, 1.0), 31)
+    hdr = np.zeros(8)
+    cnt, seed = C.c_uint64(), C.c_uint64()
+    out = np.zeros(257, dtype=ds.dtype)
+    ref.check(ref.lib().ref_load_dataset(p.encode(), ref.ptr(hdr), C.byref(cnt), C.byref(seed), ref.ptr(out), 257))
+    h, recs = sb.load_dataset(p)
+    assert cnt.value == h.count == 257 and seed.value == h.seed == 31
+    assert list(hdr) == [h.version, h.sigma_t_lo, h.sigma_t_hi, h.g_lo, h.g_hi, h.phi_kind, h.phi_a, h.phi_b]
+    assert recs.tobytes() == out.tobytes()
+    a, b = str(tmp_path / "ours.csv"), str(tmp_path / "ref.csv")
+    sb.export_dataset_csv(a, recs)
+    ref.check(ref.lib().ref_export_dataset_csv(b.encode(), 257, ref.ptr(out)))
+    assert open(a, "rb").read() == open(b, "rb").read()
+
+
 def _ks(a, b):
     a, b = np.sort(a), np.sort(b)
     x = np.concatenate([a, b])
