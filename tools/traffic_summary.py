@@ -1,6 +1,10 @@
 """Per-kernel-kind average DRAM traffic per launch from an ncu CSV launch list
 (--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum):
-  python tools/traffic_summary.py launches.csv out.json [source-note]"""
+  python tools/traffic_summary.py launches.csv out.json [source-note] [src_hash]
+src_hash (bench.source_hash() of the sources the captured library was built from) is
+stamped into the output; bench.py reports `roofline.traffic` only from a file whose
+stamp matches the sources it runs.
+"""
 import collections
 import csv
 import json
@@ -26,6 +30,8 @@ for (i, name), m in per.items():
     a["bytes"] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
     a["ns"] += m.get("gpu__time_duration.sum", 0)
 out = {"source": sys.argv[3] if len(sys.argv) > 3 else sys.argv[1], "kernels": {}}
+if len(sys.argv) > 4:
+    out["src_hash"] = sys.argv[4]
 for k, a in agg.items():
     out["kernels"][k] = {"launches": a["launches"], "dram_bytes_per_launch": a["bytes"] / a["launches"],
                          "ncu_avg_us": a["ns"] / a["launches"] / 1e3}
