@@ -280,6 +280,42 @@ int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed
                         double* radiance, uint32_t* segments, sst_path_stats* stats);
 
 /* ------------------------------------------------------------------------ */
+/* Verification hooks (csrc/verify.cuh): properties the fast paths rely on,    */
+/* checked on the device against exact FP64 references.                       */
+/* ------------------------------------------------------------------------ */
+
+/* Conservativeness of the flight-culling rules (acceptance 8, extended
+ * to every rule): n random in-medium free flights of the uploaded scene (half uniform
+ * in an object's SDF box, half 1e-6..1e-1 below its surface; exponential lengths at
+ * the medium's density) through the context precision's production predicates -- SDF
+ * safe radius, skip-grid radius, convex / two-ball end-point containment -- and every
+ * culled flight checked against all triangles in exact FP64 (no epsilon); every
+ * queried radius against the exact point-mesh distance. Any violation is a bug. */
+typedef struct {
+    uint64_t flights;
+    uint64_t culled_sdf, culled_skip, culled_endpoint_convex, culled_endpoint_twoball;
+    uint64_t violations_sdf, violations_skip, violations_endpoint_convex, violations_endpoint_twoball;
+    uint64_t radius_violations;      /* SDF safe radius > exact distance to the surface */
+    uint64_t skip_radius_violations; /* skip-grid radius > exact distance */
+} sst_cull_report;
+int sst_gpu_verify_culling(sst_gpu_ctx* ctx, uint64_t n, uint64_t seed, sst_cull_report* out);
+
+/* NEE estimator identity (acceptance 7; single_sample_nee_weight,
+ * SPEC.md:567-575) on brute-force unit-sphere walks (walk_sphere, sphere_walk.cpp:22-50)
+ * at (sigma_t, g, phi): full per-event sum F = sum_k phi^k f(X_k) against the
+ * single-representative estimate Lambda f(X_k*), k* ~ phi^k drawn by the dataset
+ * generator's sample_representative (sphere_walk.cpp:75-102), averaged over `resamples`
+ * draws per walk; f = point-light NEE term (light at light_pos, outside the sphere). */
+typedef struct {
+    uint64_t walks, events, resamples;
+    double full_mean;      /* mean over walks of F */
+    double single_mean;    /* mean over walks of the resampled single-representative estimate */
+    double diff_stderr;    /* standard error of (single - full) per walk, over walks */
+} sst_nee_identity_report;
+int sst_gpu_nee_identity(sst_gpu_ctx* ctx, uint64_t walks, uint32_t resamples, double sigma_t, double g,
+                         double phi, const double light_pos[3], uint64_t seed, sst_nee_identity_report* out);
+
+/* ------------------------------------------------------------------------ */
 /* Config 4: CVAE training-data generation, the device form of  */
 /* generate_dataset (dataset.cpp:40-92) over walk_sphere / parameterize_exit /    */
 /* sample_representative (sphere_walk.cpp:22-102). Sample i uses                 */

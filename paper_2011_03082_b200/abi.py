@@ -101,6 +101,23 @@ class DatasetStats(C.Structure):
                 ("device_ms", D)]
 
 
+class CullReport(C.Structure):
+    """sst_cull_report (include/sst_gpu.h)."""
+    _fields_ = [(n, U64) for n in ("flights", "culled_sdf", "culled_skip", "culled_endpoint_convex",
+                                   "culled_endpoint_twoball", "violations_sdf", "violations_skip",
+                                   "violations_endpoint_convex", "violations_endpoint_twoball",
+                                   "radius_violations", "skip_radius_violations")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class NeeIdentityReport(C.Structure):
+    """sst_nee_identity_report (include/sst_gpu.h)."""
+    _fields_ = [("walks", U64), ("events", U64), ("resamples", U64), ("full_mean", D), ("single_mean", D),
+                ("diff_stderr", D)]
+
+
 class DatasetHeader(C.Structure):
     """sst_dataset_header (include/sst_host.h) = DatasetHeader (dataset.hpp:43-50)."""
     _fields_ = [("version", U32), ("count", U64), ("sigma_t_lo", C.c_float), ("sigma_t_hi", C.c_float),
@@ -149,6 +166,7 @@ EXPORTED = [
     "sst_gpu_sphere_step_batch", "sst_gpu_upload_scene", "sst_gpu_scene_info", "sst_gpu_get_sdf", "sst_gpu_render",
     "sst_gpu_trace_paths", "sst_gpu_read_stats", "sst_gpu_kernel_timing", "sst_gpu_generate_dataset",
     "sst_train_config_default", "sst_gpu_train_model", "sst_gpu_train_models",
+    "sst_gpu_verify_culling", "sst_gpu_nee_identity",
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
     "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm", "sst_dataset_save",
@@ -208,6 +226,8 @@ def _declare(L):
     L.sst_gpu_train_models.argtypes = [P, P, U64, I, U64, P, P, C.c_char_p, I, I, P]
     L.sst_dataset_save.argtypes = [C.c_char_p, U64, C.c_float, C.c_float, C.c_float, C.c_float, U32,
                                    C.c_float, C.c_float, U64, P]
+    L.sst_gpu_verify_culling.argtypes = [P, U64, U64, C.POINTER(CullReport)]
+    L.sst_gpu_nee_identity.argtypes = [P, U64, U32, D, D, D, P, U64, C.POINTER(NeeIdentityReport)]
     L.sst_dataset_load.argtypes = [C.c_char_p, C.POINTER(DatasetHeader), P, U64]
     L.sst_dataset_export_csv.argtypes = [C.c_char_p, U64, P]
     L.sst_gpu_trace_paths.argtypes = [P, I, I, U64, U64, P, P, P, P, P, C.POINTER(PathStats)]

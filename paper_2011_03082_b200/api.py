@@ -356,6 +356,22 @@ class Renderer:
                                                  int(install), stats))
         return ep, list(stats)
 
+    def verify_culling(self, n, seed=1) -> dict:
+        """sst_gpu_verify_culling: the flight-culling rules of the uploaded scene against
+        exact FP64 geometry (counts of culled flights and of violations)."""
+        rep = abi.CullReport()
+        abi.check(abi.lib().sst_gpu_verify_culling(self.h, int(n), int(seed), C.byref(rep)))
+        return rep.as_dict()
+
+    def nee_identity(self, walks, resamples, sigma_t, g, phi, light=(0.0, 0.0, 3.0), seed=1):
+        """sst_gpu_nee_identity: full per-event NEE sum vs the single-representative
+        estimate on unit-sphere walks."""
+        rep = abi.NeeIdentityReport()
+        lp = np.ascontiguousarray(light, dtype=np.float64)
+        abi.check(abi.lib().sst_gpu_nee_identity(self.h, int(walks), int(resamples), sigma_t, g, phi, _p(lp),
+                                                 int(seed), C.byref(rep)))
+        return rep
+
     def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None):
         pixel = np.ascontiguousarray(pixel, dtype=np.uint32)
         sample = np.ascontiguousarray(sample, dtype=np.uint32)

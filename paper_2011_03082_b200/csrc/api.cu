@@ -821,13 +821,14 @@ void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
 bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
 
 // Sizes of the wavefront pool's arrays for `cap` slots (carve_pool order).
+constexpr int kPoolArrays = 23;
 template <class R>
-size_t pool_layout(uint32_t cap, size_t (&off)[22]) {
-    const size_t n = cap;
+size_t pool_layout(uint32_t cap, size_t (&off)[kPoolArrays]) {
+    const size_t n = cap, nk = n * kNeeChain;
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
-                            n * 8, n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4, n * 4, n * 4,
+                            n * 8, nk * sizeof(Q4<R>), nk * sizeof(Q4<R>), n * 4, n * 4, (nk + n) * 4, n * 4,
                             kQCount * 4, 8, n * 4, n * 4, n * 4,
-                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>)};
+                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>), nk * sizeof(R)};
     size_t total = 0;
     int k = 0;
     for (size_t b : sizes) {
@@ -840,7 +841,7 @@ size_t pool_layout(uint32_t cap, size_t (&off)[22]) {
 // Carves the wavefront pool of `cap` slots out of the slot's device buffer.
 template <class R>
 WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
-    size_t off[22];
+    size_t off[kPoolArrays];
     sl.wf.reserve(pool_layout<R>(cap, off));
     char* base = sl.wf.as<char>();
     WfPool<R> q{};
@@ -867,6 +868,7 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.tr_d = reinterpret_cast<Q4<R>*>(base + off[19]);
     q.tr_f = reinterpret_cast<uint32_t*>(base + off[20]);
     q.tr_cam = reinterpret_cast<Q4<R>*>(base + off[21]);
+    q.nee_res = reinterpret_cast<R*>(base + off[22]);
     return q;
 }
 
@@ -1218,7 +1220,7 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         // (grow-only): a slot first used later -- e.g. inside a timed or
         // latency-sensitive stretch of calls -- would otherwise cudaFree/cudaMalloc
         // (device-synchronising) mid-pipeline.
-        size_t off[22];
+        size_t off[kPoolArrays];
         const uint64_t cap = std::max<uint64_t>(32, std::min<uint64_t>(per_sample * chunk, ctx->wf_pool));
         const size_t pool = pool_layout<R>(static_cast<uint32_t>(cap), off);
         bool grow = false;
@@ -1361,6 +1363,39 @@ void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, 
     collect_stats(ctx, stats);
 }
 
+}  // namespace
+
+namespace {
+template <class R>
+void verify_culling_impl(sst_gpu_ctx* ctx, uint64_t n, uint64_t seed, sst_cull_report* out) {
+    ScopedBuf cnt;
+    cnt.reserve(kCvCount * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(cnt.p, 0, kCvCount * sizeof(unsigned long long), ctx->stream));
+    CullCheckArgs<R> a{};
+    a.sc = scene_of<R>(ctx);
+    a.tris = ctx->tris64.as<TriD>();
+    a.n_tris = ctx->n_tris;
+    a.n = n;
+    a.seed = seed;
+    a.convex_end = ctx->convex_end;
+    a.counts = cnt.as<unsigned long long>();
+    if constexpr (std::is_same<R, float>::value) CK(f32::launch_verify_cull(a, ctx->stream));
+    else CK(f64::launch_verify_cull(a, ctx->stream));
+    unsigned long long h[kCvCount];
+    CK(cudaMemcpyAsync(h, cnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    out->flights = h[kCvFlights];
+    out->culled_sdf = h[kCvCullSdf];
+    out->culled_skip = h[kCvCullSkip];
+    out->culled_endpoint_convex = h[kCvCullConvex];
+    out->culled_endpoint_twoball = h[kCvCullTwoBall];
+    out->violations_sdf = h[kCvViolSdf];
+    out->violations_skip = h[kCvViolSkip];
+    out->violations_endpoint_convex = h[kCvViolConvex];
+    out->violations_endpoint_twoball = h[kCvViolTwoBall];
+    out->radius_violations = h[kCvRadiusViol];
+    out->skip_radius_violations = h[kCvSkipRadiusViol];
+}
 }  // namespace
 
 // =========================================================================== C ABI
@@ -1758,6 +1793,57 @@ int sst_gpu_generate_dataset(sst_gpu_ctx* ctx, uint64_t n, double s_lo, double s
             stats->max_events = std::max<uint64_t>(stats->max_events, hs[2]);
             stats->device_ms += ms;
         }
+    });
+}
+
+int sst_gpu_verify_culling(sst_gpu_ctx* ctx, uint64_t n, uint64_t seed, sst_cull_report* out) {
+    return guarded([&] {
+        require_device(ctx);
+        if (!ctx->scene) throw InvalidArgument("no scene uploaded (sst_gpu_upload_scene)");
+        if (!out) throw InvalidArgument("null output pointer");
+        *out = sst_cull_report{};
+        drain_jobs(ctx);
+        if (ctx->precision == SST_PREC_F64) verify_culling_impl<double>(ctx, n, seed, out);
+        else verify_culling_impl<float>(ctx, n, seed, out);
+    });
+}
+
+int sst_gpu_nee_identity(sst_gpu_ctx* ctx, uint64_t walks, uint32_t resamples, double sigma_t, double g,
+                         double phi, const double light_pos[3], uint64_t seed, sst_nee_identity_report* out) {
+    return guarded([&] {
+        require_device(ctx);
+        if (!out || !light_pos) throw InvalidArgument("null argument");
+        if (!(sigma_t > 0.0) || !(g > -1.0 && g < 1.0) || !(phi >= 0.0 && phi <= 1.0) || resamples == 0)
+            throw DomainError("nee_identity: sigma_t > 0, g in (-1, 1), phi in [0, 1], resamples >= 1");
+        if (light_pos[0] * light_pos[0] + light_pos[1] * light_pos[1] + light_pos[2] * light_pos[2] <= 1.0)
+            throw InvalidArgument("nee_identity: the light must lie outside the unit sphere");
+        ScopedBuf buf;
+        buf.reserve(3 * sizeof(double) + 3 * sizeof(unsigned long long));
+        CK(cudaMemsetAsync(buf.p, 0, 3 * sizeof(double) + 3 * sizeof(unsigned long long), ctx->stream));
+        NeeIdentityArgs a{};
+        a.walks = walks;
+        a.resamples = resamples;
+        a.sigma_t = sigma_t;
+        a.g = g;
+        a.phi = phi;
+        for (int k = 0; k < 3; ++k) a.light[k] = light_pos[k];
+        a.seed = seed;
+        a.sums = buf.as<double>();
+        a.counts = reinterpret_cast<unsigned long long*>(buf.as<char>() + 3 * sizeof(double));
+        CK(ctx->precision == SST_PREC_F64 ? f64::launch_nee_identity(a, ctx->stream)
+                                          : f32::launch_nee_identity(a, ctx->stream));
+        double h[3];
+        unsigned long long c[3];
+        CK(cudaMemcpyAsync(h, a.sums, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(c, a.counts, sizeof c, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        out->walks = c[0];
+        out->events = c[1];
+        out->resamples = c[2];
+        const double w = c[0] ? static_cast<double>(c[0]) : 1.0;
+        out->full_mean = h[0] / w;
+        out->single_mean = h[1] / w;
+        out->diff_stderr = std::sqrt(h[2] / w) / std::sqrt(w);
     });
 }
 

@@ -85,6 +85,25 @@ SST_D void write_sample(const DatasetArgs& a, const WalkLane<R>& w) {
     a.out[w.idx - a.first] = o;
 }
 
+// sample_representative (sphere_walk.cpp:75-102): event k in [1, n] with P(k) ~ phi^k
+// (uniform for phi = 1, k = 1 for phi = 0), one FP64 uniform draw.
+SST_D uint32_t representative_k(double phi, uint64_t n, Rng& rng) {
+    uint64_t k = 1;
+    if (phi <= 0.0) {
+        k = 1;
+    } else if (phi >= 1.0) {
+        const uint64_t t = static_cast<uint64_t>(rng.template uniform<double>() * static_cast<double>(n));
+        k = 1 + (n - 1 < t ? n - 1 : t);
+    } else {
+        const double u = rng.template uniform<double>();
+        const double phi_n = exp(static_cast<double>(n) * log(phi));
+        const double target = 1.0 - u * (1.0 - phi_n);
+        k = static_cast<uint64_t>(ceil(log(target) / log(phi)));
+        k = k < 1 ? 1 : (k > n ? n : k);
+    }
+    return static_cast<uint32_t>(k);
+}
+
 template <class R>
 SST_D void dataset_persistent(const DatasetArgs& a) {
     const unsigned lane = threadIdx.x & 31u;
@@ -145,23 +164,7 @@ SST_D void dataset_persistent(const DatasetArgs& a) {
             w.n = w.count;
             ev1 += w.count;
             nmax = nmax > w.count ? nmax : w.count;
-            // sample_representative (sphere_walk.cpp:75-102)
-            const double phi = w.phi_d;
-            const uint64_t n = w.count;
-            uint64_t k = 1;
-            if (phi <= 0.0) {
-                k = 1;
-            } else if (phi >= 1.0) {
-                const uint64_t t = static_cast<uint64_t>(w.rng.template uniform<double>() * static_cast<double>(n));
-                k = 1 + (n - 1 < t ? n - 1 : t);
-            } else {
-                const double u = w.rng.template uniform<double>();
-                const double phi_n = exp(static_cast<double>(n) * log(phi));
-                const double target = 1.0 - u * (1.0 - phi_n);
-                k = static_cast<uint64_t>(ceil(log(target) / log(phi)));
-                k = k < 1 ? 1 : (k > n ? n : k);
-            }
-            w.k = static_cast<uint32_t>(k);
+            w.k = representative_k(w.phi_d, w.count, w.rng);
             walk_begin(w);  // replay from the walk's first draw
             w.pass = 2;
             if (w.k == 1) {

@@ -413,7 +413,7 @@ SST_D T warp_sum(T v) {
 // Wavefront slot -> path state (wavefront.cuh).
 template <class R>
 SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam,
-                     bool need_tpend);
+                     bool need_tpend, bool fold);
 
 template <class R, bool ST, bool EXPLICIT>
 SST_D void trace_persistent(const TraceArgs<R>& a) {
@@ -432,9 +432,17 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
                 const uint64_t my = base + __popc(need & ((1u << lane) - 1u));
                 if (a.resume) {  // hand-off of the wavefront pool's live slots
                     if (my < a.pool.counts[kQResume]) {
-                        uint32_t phase;
-                        load_slot(a.pool, a.pool.q_live[my], p, &phase, a.sc.cam_pos, true);
-                        alive = true;
+                        uint32_t phase;  // the slot's staged NEE contributions are added here
+                        load_slot(a.pool, a.pool.q_live[my], p, &phase, a.sc.cam_pos, true, true);
+                        if (phase == 4u) {  // kPhEnded: absorbed once those were in
+                            a.radiance[p.id] = p.L;
+                            if (a.segments) a.segments[p.id] = p.seg;
+                            ++st.paths;
+                            st.seg += p.seg;
+                            ++st.absorbed;
+                        } else {
+                            alive = true;
+                        }
                     } else {
                         exhausted = true;
                     }
@@ -446,7 +454,10 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
                 }
             }
         }
-        if (!__any_sync(0xffffffffu, alive)) break;
+        if (!__any_sync(0xffffffffu, alive)) {
+            if (__all_sync(0xffffffffu, exhausted)) break;
+            continue;  // every fetched slot had already ended (hand-off): fetch again
+        }
         st.lane_iters += alive;
         st.warp_iters += lane == 0;
         const int end = path_advance<R, ST>(a, p, st, alive);

@@ -6,6 +6,7 @@
 #include "dataset.cuh"
 #include "integrator.cuh"
 #include "wavefront.cuh"
+#include "verify.cuh"
 #include "launch.h"
 
 namespace sstg {
@@ -313,6 +314,23 @@ cudaError_t launch_film(const R* radiance, uint64_t stride, uint32_t n_samples, 
     uint64_t grid = (stride + block - 1) / block;
     if (grid > 65535u * 16u) grid = 65535u * 16u;
     k_film<<<static_cast<unsigned>(grid), block, 0, s>>>(radiance, stride, n_samples, sum, sumsq);
+    return cudaGetLastError();
+}
+
+// Verification kernels (verify.cuh): the culling rules of this precision build against
+// exact FP64 geometry, and the NEE estimator identity.
+__global__ void __launch_bounds__(128) k_verify_cull(CullCheckArgs<R> a) { verify_cull<R>(a); }
+__global__ void __launch_bounds__(128) k_nee_identity(NeeIdentityArgs a) { nee_identity<R>(a); }
+
+cudaError_t launch_verify_cull(const CullCheckArgs<R>& a, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    k_verify_cull<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nee_identity(const NeeIdentityArgs& a, cudaStream_t s) {
+    if (a.walks == 0) return cudaSuccess;
+    k_nee_identity<<<static_cast<unsigned>((a.walks + 127) / 128), 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 

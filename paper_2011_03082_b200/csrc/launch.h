@@ -24,6 +24,8 @@ constexpr int kTraceBlock = 32;  // one warp per block: a long-path tail strands
     cudaError_t launch_film(const REAL* radiance, uint64_t stride, uint32_t n_samples,          \
                             double* sum, double* sumsq, cudaStream_t s);                        \
     cudaError_t launch_dataset(const DatasetArgs& a, cudaStream_t s);                           \
+    cudaError_t launch_verify_cull(const CullCheckArgs<REAL>& a, cudaStream_t s);               \
+    cudaError_t launch_nee_identity(const NeeIdentityArgs& a, cudaStream_t s);                  \
     }
 
 SST_DECLARE_LAUNCHERS(f32, float)

@@ -135,6 +135,17 @@ enum : int {
     kQFetchShadowS = 12,  // their work-stealing cursor
     kQCount = 14
 };
+// NEE mailbox (wavefront.cuh): a logic visit chains up to kNeeChain delta-tracking
+// events; their NEE records are staged per slot at s * kNeeChain + i, the shadow kernel
+// writes each contribution to nee_res at the same index, and the slot's next visit adds
+// them to its radiance in event order. 2 measured best on C5 (logic 93.7 -> 87 ms per
+// 32-spp slab; 3: 92, 4: 96, 8: 131 -- a warp runs as long as its longest chain).
+#ifndef SST_NEE_CHAIN
+#define SST_NEE_CHAIN 2
+#endif
+constexpr uint32_t kNeeChain = SST_NEE_CHAIN;
+static_assert(kNeeChain >= 1 && kNeeChain <= 15, "pending count lives in 4 meta bits");
+
 template <class R>
 struct WfPool {
     uint32_t cap;     // slots
@@ -155,9 +166,12 @@ struct WfPool {
     Q4<R>* tr_cam;
     R* thit;          // traversal result: distance
     uint2* hinfo;     // traversal result: triangle, object | found << 31
-    // Shadow queue records (indexed by queue position): slot in q_shadow.
+    // NEE records staged per slot ([cap * kNeeChain], index s * kNeeChain + i); the
+    // shadow queue q_shadow ([cap * (kNeeChain + 1)]) holds record indices: the logic
+    // records from the front, the sphere steps' records from the back.
     Q4<R>* nee_p;     // NEE record: point, weight
     Q4<R>* nee_w;     // NEE record: direction, obj | channel << 8 (int bits)
+    R* nee_res;       // contribution of each record (written by k_wf_shadow)
     uint32_t *q_sphere, *q_shadow, *q_live;
     uint32_t *q_la, *q_lb;  // ping-pong lists of live slots (logic input / output)
     uint32_t* q_free;       // free slots (path ended), refilled by the generation kernel
@@ -227,6 +241,33 @@ struct StepBatchArgs {
     double *rep_pos, *rep_dir, *lambda;
     unsigned long long* counters;  // [3] length, path, event
     int* error;
+};
+
+// Verification kernels (verify.cuh).
+// counters of k_verify_cull (sst_cull_report order)
+enum : int {
+    kCvFlights = 0, kCvCullSdf, kCvCullSkip, kCvCullConvex, kCvCullTwoBall, kCvViolSdf, kCvViolSkip,
+    kCvViolConvex, kCvViolTwoBall, kCvRadiusViol, kCvSkipRadiusViol, kCvCount
+};
+
+template <class R>
+struct CullCheckArgs {
+    DevScene<R> sc;
+    const TriD* tris;  // FP64 triangles (leaf order) of the uploaded scene
+    uint32_t n_tris;
+    uint64_t n, seed;
+    int convex_end;
+    unsigned long long* counts;  // [kCvCount]
+};
+
+struct NeeIdentityArgs {
+    uint64_t walks;
+    uint32_t resamples;
+    double sigma_t, g, phi;
+    double light[3];
+    uint64_t seed;
+    double* sums;                // [0] sum F, [1] sum S, [2] sum (S - F)^2
+    unsigned long long* counts;  // [0] walks, [1] events, [2] resamples
 };
 
 }  // namespace sstg

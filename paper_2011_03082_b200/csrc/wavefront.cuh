@@ -44,6 +44,14 @@ SST_D uint32_t meta_phase(uint32_t m) { return (m >> 11) & 3u; }
 // meta.w bit 13: a path fresh from the generation kernel whose position / direction
 // live only in its camera-ray trace record (xl / wr were not written; L = 0).
 constexpr uint32_t kMetaFresh = 1u << 13;
+// NEE mailbox (types.cuh kNeeChain): meta.w bits 24-27 = number of staged NEE records
+// whose contributions the slot's next logic visit adds to L (in event order); bit 14 =
+// the path was absorbed after staging some: the next visit adds them, then ends it.
+constexpr uint32_t kMetaEndAbsorbed = 1u << 14;
+constexpr int kMetaPendShift = 24;
+SST_D uint32_t meta_pending(uint32_t m) { return (m >> kMetaPendShift) & 0xfu; }
+// Transient phase returned by load_slot for a slot whose path already ended (absorbed).
+constexpr uint32_t kPhEnded = 4;
 // Integer payloads carried in the spare lane of a record vector.
 template <class R>
 SST_D R int_bits(int v) {
@@ -58,12 +66,41 @@ SST_D int bits_int(R v) {
 SST_D int meta_obj(uint32_t m) { return static_cast<int>(m & 0xffu) - 1; }
 SST_D int meta_c(uint32_t m) { return static_cast<int>((m >> 8) & 3u); }
 
+// The slot's mailbox entries, loaded as one vector (issued with the slot state, before
+// the pending count is known: most visits have some).
 template <class R>
+struct Mailbox {
+    R v[kNeeChain];
+};
+template <class R>
+SST_D Mailbox<R> load_mailbox(const WfPool<R>& q, uint32_t s) {
+    Mailbox<R> mb;
+    const R* src = q.nee_res + static_cast<size_t>(s) * kNeeChain;
+    if constexpr (sizeof(R) == 4 && kNeeChain == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(src);
+        mb.v[0] = t.x;
+        mb.v[1] = t.y;
+    } else if constexpr (sizeof(R) == 4 && kNeeChain == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(src);
+        mb.v[0] = t.x;
+        mb.v[1] = t.y;
+        mb.v[2] = t.z;
+        mb.v[3] = t.w;
+    } else {
+#pragma unroll
+        for (uint32_t i = 0; i < kNeeChain; ++i) mb.v[i] = src[i];
+    }
+    return mb;
+}
+
 // need_tpend: the queued flight length is only stored while a traversal is queued and
 // only the megakernel hand-off reads it from the slot (the logic pass takes it from the
 // traversal result: a miss leaves t_hit = t_max = the flight length).
+// fold: add the contributions of the slot's staged NEE records (the logic visit and the
+// megakernel hand-off; never the sphere kernel, which runs while they are computed).
+template <class R>
 SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLocal<R>& p, uint32_t* phase,
-                          const V3<R>& sc_cam_pos, bool need_tpend) {
+                          const V3<R>& sc_cam_pos, bool need_tpend, bool fold, const Mailbox<R>* mb = nullptr) {
     const Q4<R> xl = q.xl[s], wr = q.wr[s];
     p.x = mk<R>(xl.x, xl.y, xl.z);
     p.L = xl.w;
@@ -93,22 +130,43 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
     p.waited = 0;
     p.twaited = 0;
     p.pixel = 0;
+    if (fold) {
+        const uint32_t k = meta_pending(m.w);
+        if (mb) {
+#pragma unroll
+            for (uint32_t i = 0; i < kNeeChain; ++i)
+                if (i < k) p.L += mb->v[i];
+        } else {
+            for (uint32_t i = 0; i < k; ++i) p.L += q.nee_res[s * kNeeChain + i];
+        }
+        if (m.w & kMetaEndAbsorbed) *phase = kPhEnded;
+    }
 }
 
 template <class R>
 SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* phase, const V3<R>& cam,
-                     bool need_tpend) {
-    load_slot_from(q, s, q.meta[s], p, phase, cam, need_tpend);
+                     bool need_tpend, bool fold) {
+    load_slot_from(q, s, q.meta[s], p, phase, cam, need_tpend, fold);
 }
 
+// pending: staged NEE records not yet added to L; flags: kMetaEndAbsorbed.
 template <class R>
-SST_D void store_slot(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p, uint32_t phase) {
+SST_D void store_slot(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p, uint32_t phase, uint32_t pending = 0u,
+                      uint32_t flags = 0u) {
     q.xl[s] = Q4<R>{p.x.x, p.x.y, p.x.z, p.L};
     q.wr[s] = Q4<R>{p.w.x, p.w.y, p.w.z, p.r_here};
     q.rng[s] = p.rng.s;
     q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), p.seg, static_cast<uint32_t>(p.skip),
-                           pack_meta(p.obj, p.c, p.r_valid, phase, p.cull));
+                           pack_meta(p.obj, p.c, p.r_valid, phase, p.cull) | (pending << kMetaPendShift) | flags);
     if (phase == kPhTrace) q.tpend[s] = p.t_pend;
+}
+
+// Staged NEE record i of slot s.
+template <class R>
+SST_D void put_nee(const WfPool<R>& q, uint32_t s, uint32_t i, V3<R> x, V3<R> w, R weight, int obj, int c) {
+    const uint32_t idx = s * kNeeChain + i;
+    q.nee_p[idx] = Q4<R>{x.x, x.y, x.z, weight};
+    q.nee_w[idx] = Q4<R>{w.x, w.y, w.z, int_bits<R>(obj | (c << 8))};
 }
 
 SST_D void set_phase(uint4* meta, uint32_t s, uint32_t phase) {
@@ -145,8 +203,6 @@ SST_D void prefetch_shadow(const WfPool<R>& q, uint32_t j, uint32_t n, uint32_t 
     j += SST_WF_PREFETCH_AHEAD;
     if (j >= len) return;
     if (n > len - j) n = len - j;
-    l2_prefetch(q.nee_p + j, n * sizeof(Q4<R>));
-    l2_prefetch(q.nee_w + j, n * sizeof(Q4<R>));
     l2_prefetch(q.q_shadow + j, n * sizeof(uint32_t));
 }
 
@@ -249,6 +305,52 @@ SST_D void block_pushn(const bool (&want)[N], uint32_t value, uint32_t* const (&
     __syncthreads();
 }
 
+// block_pushn plus one COUNTED queue: the calling thread appends cnt consecutive
+// entries first, first + 1, ... (its chained NEE records) at consecutive positions.
+template <int N>
+SST_D void block_pushn_counted(const bool (&want)[N], uint32_t value, uint32_t* const (&counter)[N],
+                               uint32_t* const (&queue)[N], uint32_t (&pos)[N], uint32_t cnt, uint32_t first,
+                               uint32_t* ccounter, uint32_t* cqueue) {
+    __shared__ uint32_t wc[8][33];
+    __shared__ uint32_t qbase[8];
+    static_assert(N + 1 <= 8, "queues");
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned nw = (blockDim.x + 31u) >> 5;
+    unsigned b[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        b[j] = __ballot_sync(0xffffffffu, want[j]);
+        if (lane == 0) wc[j][warp] = __popc(b[j]);
+    }
+    uint32_t incl = cnt;  // warp inclusive scan of the counted queue
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<unsigned>(o)) incl += t;
+    }
+    if (lane == 31) wc[N][warp] = incl;
+    __syncthreads();
+    if (threadIdx.x <= N && (threadIdx.x == N ? ccounter != nullptr : counter[threadIdx.x] != nullptr)) {
+        const int j = threadIdx.x;
+        uint32_t tot = 0;
+        for (unsigned i = 0; i < nw; ++i) {
+            const uint32_t c = wc[j][i];
+            wc[j][i] = tot;
+            tot += c;
+        }
+        qbase[j] = tot ? atomicAdd(j == N ? ccounter : counter[j], tot) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        pos[j] = qbase[j] + wc[j][warp] + __popc(b[j] & ((1u << lane) - 1u));
+        if (want[j] && queue[j]) queue[j][pos[j]] = value;
+    }
+    const uint32_t at = qbase[N] + wc[N][warp] + incl - cnt;
+    for (uint32_t i = 0; i < cnt; ++i) cqueue[at + i] = first + i;
+    __syncthreads();
+}
+
 // Warp-granular work stealing over a queue of n items: returns the next item index
 // for this lane (>= n when the queue is exhausted for the whole warp).
 SST_D uint32_t warp_fetch(uint32_t* cursor) {
@@ -269,7 +371,6 @@ SST_D uint32_t warp_push(uint32_t value, uint32_t* counter, uint32_t* queue) {
 
 // Queue record written after the block push (the position is known only then):
 // trace -- a = origin, b = direction, t = t_max, u = skip, v = (cull + 1) | inside << 8;
-// shadow -- a = point, b = direction, t = weight, u = obj | channel << 8.
 template <class R>
 struct WfRec {
     V3<R> a, b;
@@ -285,13 +386,7 @@ SST_D void put_trace(const WfPool<R>& q, uint32_t j, const WfRec<R>& r) {
     q.tr_f[j] = r.v;
 }
 
-template <class R>
-SST_D void put_shadow(const WfPool<R>& q, uint32_t j, const WfRec<R>& r) {
-    q.nee_p[j] = Q4<R>{r.a.x, r.a.y, r.a.z, r.t};
-    q.nee_w[j] = Q4<R>{r.b.x, r.b.y, r.b.z, int_bits<R>(r.u)};
-}
-
-enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3, kEmitFree = 4 };
+enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitFree = 4 };
 
 // ------------------------------------------------------------------ k_wf_logic
 // The non-traversal part of path_advance for one slot, run until the slot needs a
@@ -299,7 +394,7 @@ enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitShadow = 3, kE
 // ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
 SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, unsigned m, LaneStats& st,
-                        bool* live, WfRec<R>& rec) {
+                        bool* live, WfRec<R>& rec, uint32_t* nrec_out) {
     // m: the lanes of this warp calling (converged). The loop below has no break /
     // continue / return inside: every stage is an if-block that all lanes of the warp
     // reach together, so lanes that got to a collision by different routes (after a
@@ -307,13 +402,22 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
     const DevScene<R>& sc = a.sc;
     PathLocal<R> p;
     const uint4 mt = q.meta[s];
+    const Mailbox<R> mb = load_mailbox(q, s);
     uint32_t phase = meta_phase(mt.w);
     *live = false;
+    *nrec_out = 0u;
     ++st.wf_slots;
-    m = __ballot_sync(m, phase != kPhEmpty);
+    const bool ended = (mt.w & kMetaEndAbsorbed) != 0u;
+    m = __ballot_sync(m, phase != kPhEmpty && !ended);
     // ended in k_wf_sphere (which runs concurrently with the generation kernel and so
     // does not touch the free queue): free it now if new paths remain
     if (phase == kPhEmpty) return *a.work < a.n_paths ? kEmitFree : kEmitNone;
+    if (ended) {  // absorbed after staging NEE records: add them, then the path ends
+        load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false, true, &mb);
+        finish_path(a, p, kEndAbsorbed, st);
+        q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
+        return kEmitFree;
+    }
     // the traversal result (and a fresh path's camera record) at the slot's trace-queue
     // position, issued with the slot loads
     uint2 hi = make_uint2(0u, 0u);
@@ -323,13 +427,14 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
         hi = q.hinfo[j];
         t_hit = q.thit[j];
     }
-    load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false);
+    load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false, true, &mb);
     ++st.lane_iters;
     int emit = kEmitNone;
     int end = -1;
     bool run = true;
+    uint32_t nrec = 0u;  // NEE records staged by this visit (the mailbox)
 #pragma unroll 1
-    for (int guard = 0; guard < 8; ++guard) {
+    for (int guard = 0; guard < 4 + 2 * static_cast<int>(kNeeChain); ++guard) {
         if (!__any_sync(m, run)) break;
         bool collide = false;
         R t_free = Real<R>::kInf;
@@ -443,17 +548,15 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
                     if (!((p.rng.next() >> 11) < m.survive_below)) {  // u < phi, bit-exact
                         end = kEndAbsorbed;
                     } else {
-                        if (a.nee) {  // NEE with the incoming direction (no draws)
-                            rec.a = p.x;
-                            rec.b = p.w;
-                            rec.t = R(1);
-                            rec.u = p.obj | (static_cast<int>(p.c) << 8);
-                            emit = kEmitShadow;
+                        if (a.nee) {  // NEE with the incoming direction (no draws), staged
+                            put_nee(q, s, nrec, p.x, p.w, R(1), p.obj, static_cast<int>(p.c));
+                            ++nrec;
                         }
                         const R u1 = p.rng.template uniform<R>();
                         const R u2 = p.rng.template uniform<R>();
                         p.w = hg_sample(m.g, p.w, u1, u2);
-                        run = false;  // one event per pass
+                        // the next event chains into this visit until the mailbox is full
+                        if (a.nee && nrec >= kNeeChain) run = false;
                     }
                 }
             }
@@ -461,12 +564,19 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
         if (end >= 0) run = false;
     }
     if (end >= 0) {
-        finish_path(a, p, end, st);
+        if (end == kEndAbsorbed && nrec > 0u) {  // its staged contributions arrive next pass
+            store_slot(q, s, p, kPhFlight, nrec, kMetaEndAbsorbed);
+            *live = true;
+            *nrec_out = nrec;
+            return kEmitNone;
+        }
+        finish_path(a, p, end, st);  // capped: L = 0, the staged records do not matter
         q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
         return kEmitFree;
     }
-    store_slot(q, s, p, phase);
+    store_slot(q, s, p, phase, nrec);
     *live = true;
+    *nrec_out = nrec;
     return emit;
 }
 
@@ -495,21 +605,21 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
 #endif
         int emit = kEmitNone;
         bool live = false;
+        uint32_t nrec = 0u;
         WfRec<R> rec;
         const uint32_t s = i < n_in ? (q.q_in ? q.q_in[i] : i) : 0u;
         const unsigned m = __ballot_sync(0xffffffffu, i < n_in);
-        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, m, st, &live, rec);
-        const bool want[5] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitShadow, emit == kEmitFree};
-        uint32_t* const ctr[5] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
-                                  q.counts + kQShadow, q.counts + kQFree};
-        uint32_t* const qs[5] = {q.q_out, nullptr, q.q_sphere, q.q_shadow, q.q_free};
-        uint32_t pos[5];
-        block_pushn<5>(want, s, ctr, qs, pos);
+        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, m, st, &live, rec, &nrec);
+        const bool want[4] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitFree};
+        uint32_t* const ctr[4] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
+                                  q.counts + kQFree};
+        uint32_t* const qs[4] = {q.q_out, nullptr, q.q_sphere, q.q_free};
+        uint32_t pos[4];
+        // the staged NEE records of the visit go onto the shadow queue as record indices
+        block_pushn_counted<4>(want, s, ctr, qs, pos, nrec, s * kNeeChain, q.counts + kQShadow, q.q_shadow);
         if (emit == kEmitTrace) {
             put_trace(q, pos[1], rec);
             q.tq[s] = pos[1];
-        } else if (emit == kEmitShadow) {
-            put_shadow(q, pos[3], rec);
         }
     }
     flush_lane_stats(a.stats, st);
@@ -706,7 +816,11 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
         const uint32_t s = q.q_sphere[i];
         PathLocal<R> p;
         uint32_t phase;
-        load_slot(q, s, p, &phase, sc.cam_pos, false);
+        const uint4 mt = q.meta[s];
+        // the records the logic visit staged before this step are computed meanwhile
+        // (their shadow launch runs concurrently): stay pending, this step's record follows
+        load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false, false);
+        uint32_t pend = meta_pending(mt.w);
         ++st.sphere;
         StepOut<R> o;
         const MediumK<R>& m = sc.objs[p.obj].med[p.c];
@@ -718,42 +832,43 @@ SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
             end = kEndAbsorbed;
         } else {
             if (a.nee) {
-                // sphere-step NEE records fill the shadow arrays from the back (their own
+                // sphere-step NEE records go onto the shadow queue from the back (their own
                 // counter): the logic pass's records can be consumed concurrently
+                put_nee(q, s, pend, o.rep_pos, o.rep_dir, o.lambda, p.obj, static_cast<int>(p.c));
                 cg::coalesced_group g = cg::coalesced_threads();
                 uint32_t base = 0;
                 if (g.thread_rank() == 0) base = atomicAdd(q.counts + kQShadowS, g.size());
-                const uint32_t j = q.cap - 1u - (g.shfl(base, 0) + g.thread_rank());
-                q.q_shadow[j] = s;
-                q.nee_p[j] = Q4<R>{o.rep_pos.x, o.rep_pos.y, o.rep_pos.z, o.lambda};
-                q.nee_w[j] = Q4<R>{o.rep_dir.x, o.rep_dir.y, o.rep_dir.z, int_bits<R>(p.obj | (static_cast<int>(p.c) << 8))};
+                const uint32_t j = q.cap * (kNeeChain + 1u) - 1u - (g.shfl(base, 0) + g.thread_rank());
+                q.q_shadow[j] = s * kNeeChain + pend;
+                ++pend;
             }
             p.x = o.exit_pos;
             p.w = o.exit_dir;
             p.r_valid = false;
         }
-        if (end >= 0) {  // the slot goes back to the free queue in the next logic pass
+        if (end == kEndAbsorbed && pend > 0u) {  // earlier staged contributions: next pass ends it
+            store_slot(q, s, p, kPhFlight, pend, kMetaEndAbsorbed);
+        } else if (end >= 0) {  // the slot goes back to the free queue in the next logic pass
             finish_path(a, p, end, st);
             q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
         } else {
-            store_slot(q, s, p, kPhFlight);
+            store_slot(q, s, p, kPhFlight, pend);
         }
     }
     flush_lane_stats(a.stats, st);
 }
 
 // ------------------------------------------------------------------ k_wf_shadow
-// One NEE record at array position i: shadow ray through the light grid, radiance update.
+// One staged NEE record (index idx = slot * kNeeChain + i): shadow ray through the light
+// grid; the contribution goes to the record's mailbox entry (the slot adds it next pass).
 template <class R>
-SST_D void shadow_one(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t i, uint64_t& tris) {
+SST_D void shadow_one(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t idx, uint64_t& tris) {
     const DevScene<R>& sc = a.sc;
-    const uint32_t s = q.q_shadow[i];
-    const Q4<R> np = q.nee_p[i], nw = q.nee_w[i];
-    const R L0 = q.xl[s].w;  // issued early: the radiance update is the last use
+    const Q4<R> np = q.nee_p[idx], nw = q.nee_w[idx];
     const int oc = bits_int<R>(nw.w);
     const int obj = oc & 0xff, c = oc >> 8;
-    const R add = nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w, tris);
-    q.xl[s].w = L0 + add;
+    q.nee_res[idx] =
+        nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w, tris);
 }
 
 // The logic pass's NEE records (front of the arrays, counts[kQShadow]) are consumed by
@@ -772,7 +887,7 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q, bool with_sphere
 #endif
         if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
         if (i >= n) continue;
-        shadow_one(a, q, i, tris);
+        shadow_one(a, q, q.q_shadow[i], tris);
         ++shadow;
     }
     if (with_sphere) {
@@ -781,7 +896,7 @@ SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q, bool with_sphere
             const uint32_t i = warp_fetch(q.counts + kQFetchShadowS);
             if (i - (threadIdx.x & 31u) >= ns) break;  // warp-uniform
             if (i >= ns) continue;
-            shadow_one(a, q, q.cap - 1u - i, tris);
+            shadow_one(a, q, q.q_shadow[q.cap * (kNeeChain + 1u) - 1u - i], tris);
             ++shadow;
         }
     }

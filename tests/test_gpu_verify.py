@@ -1,0 +1,54 @@
+"""On-device verification hooks (csrc/verify.cuh).
+
+Conservativeness (acceptance 8 -- "zero sphere-triangle intersections at
+queried radii", extended to every flight-culling rule the wavefront uses): >= 1e6
+random in-medium flights per scene through the production FP32 predicates, every
+culled flight and every queried radius checked against exact FP64 geometry. Zero
+violations allowed. Scenes: the bench's C5 (convex icospheres: SDF, skip grid and
+convex end-point culling) and the C3 bumpy sphere (non-convex: two-ball culling).
+
+NEE estimator identity (acceptance 7): the single-representative
+Lambda-weighted estimate (k ~ phi^k, the dataset generator's sample_representative)
+against the full per-event sum on brute-force unit-sphere walks, 1e6 resamplings:
+agreement within 0.5% (and within 5 standard errors of the resampling noise).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("scene_name", ["c5", "c3_bumpy"])
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_flight_culling_is_conservative(renderer, scene_name, precision):
+    import paper_2011_03082_b200 as sb
+    if scene_name == "c5":
+        sc = sb.c5_scene(sb.make_icosphere(3, 1.0), 64, 36)
+    else:
+        sc = sb.c3_scene(sb.make_bumpy_sphere(4, 1.0, 0.2, 3.0), 40.0, 64, 64)
+    renderer.upload_scene(sc)
+    renderer.set_precision(precision)
+    try:
+        rep = renderer.verify_culling(1_200_000, seed=5)
+    finally:
+        renderer.set_precision("f32")
+    assert rep["flights"] >= 1_000_000, rep
+    for k, v in rep.items():
+        if "violation" in k:
+            assert v == 0, (k, rep)
+    assert rep["culled_sdf"] > 0.2 * rep["flights"], rep  # the rules really cull
+    if precision == "f32":
+        if scene_name == "c5":
+            assert rep["culled_endpoint_convex"] > 0, rep
+        else:
+            assert rep["culled_endpoint_twoball"] > 0, rep
+
+
+@pytest.mark.parametrize("sigma_t,g,phi", [(10.0, 0.8, 0.9), (40.0, 0.3, 0.99), (5.0, -0.5, 1.0)])
+def test_nee_single_representative_is_unbiased(renderer, sigma_t, g, phi):
+    rep = renderer.nee_identity(100_000, 10, sigma_t, g, phi, light=(0.0, 2.0, 2.0), seed=3)
+    assert rep.walks == 100_000 and rep.resamples == 1_000_000
+    rel = abs(rep.single_mean - rep.full_mean) / rep.full_mean
+    assert rel <= 0.005, (rel, rep.full_mean, rep.single_mean)
+    assert abs(rep.single_mean - rep.full_mean) <= 5 * rep.diff_stderr + 1e-15, (rep.full_mean, rep.single_mean,
+                                                                               rep.diff_stderr)

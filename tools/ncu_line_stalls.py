@@ -9,7 +9,8 @@ from collections import defaultdict
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 filt = sys.argv[3] if len(sys.argv) > 3 else ""
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = sys.argv[4:] and ["-k", "regex:" + sys.argv[4]] or []
+txt = subprocess.run(["ncu", "-i", rep] + kf + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 tot = defaultdict(float)
 reasons = defaultdict(lambda: defaultdict(float))
