@@ -84,3 +84,33 @@ def test_integrator_live_directional_light(ref, oracle, models_dir):
         r2, s2 = os_.trace_paths(om, integ, 1, 7, pix, smp, ch, abi.PathStats())
         assert (r1 == r2).all() and (s1 == s2).all()
         assert (r1 > 0).mean() > 0.05
+
+
+def test_reference_integrator_step_reduction_ratio(ref, models_dir):
+    """SPEC.md:695 (acceptance 6) with the REFERENCE's own functions: the
+    reference-composed integrator (oracle/ref_shim.cpp over sample_sphere_step,
+    query_safe_radius, Bvh) gives the same ST/PT sequential-step ratio as the GPU --
+    ~0.2-0.26 at sigma_t * diameter = 100 with SPEC's own r_min = max(2/sigma_t, 1.5
+    voxel) and a res-64 SDF (the GPU render path is per-path identical to it, tests/
+    test_gpu_parity_production.py). The literal "<= 10%" is a property of SPEC's r_min
+    on a surface-lit object, not of the B200 port; the ratio falls with density."""
+    import ctypes as C
+
+    from paper_2011_03082_b200 import abi, make_icosphere
+    from paper_2011_03082_b200.scene import SdfGrid, c1_scene
+    P, T = make_icosphere(3, 1.0)
+    sdf = SdfGrid(*ref.build_sdf(P, T, 64))
+    models = ref.Models(models_dir)
+    ratios = []
+    for sigma in (50.0, 200.0):  # sigma * diameter = 100, 400
+        desc = c1_scene((P, T), 48, 48, sigma_t=sigma, sdf=sdf).to_desc()
+        sc = ref.Scene(C.byref(desc))
+        rng = np.random.default_rng(4)
+        n = 6000
+        pix, smp, ch = rng.integers(0, 48 * 48, n), rng.integers(0, 64, n), rng.integers(0, 3, n)
+        st_s, pt_s = abi.PathStats(), abi.PathStats()
+        sc.trace_paths(models, 1, 0, 1, pix, smp, ch, st_s)
+        sc.trace_paths(models, 0, 0, 1, pix, smp, ch, pt_s)
+        ratios.append(st_s.segments / pt_s.segments)
+    assert 0.1 < ratios[0] < 0.35, ratios   # the literal 10% is not met at sigma*d = 100 ...
+    assert ratios[1] < ratios[0], ratios    # ... and the ratio improves with density
