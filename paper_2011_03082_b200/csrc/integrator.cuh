@@ -168,6 +168,14 @@ SST_D bool flight_contained(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
     return ob.convex || t < r_x - v;
 }
 
+// flight_contained with the end point's SDF value already loaded (wavefront logic pass).
+template <class R>
+SST_D bool end_contained(const ObjK<R>& ob, R v_end, bool in_grid, R t, R r_x) {
+    if (Real<R>::kIsDouble) return false;
+    if (!in_grid || !(v_end < R(0))) return false;
+    return ob.convex || t < r_x - v_end;
+}
+
 // FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)
 // only if x is OUTSIDE the object -- a path that believes it is inside missed its
 // exit crossing (non-watertight FP32 Moller-Trumbore at an edge). FP64 keeps the

@@ -471,9 +471,25 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
             bool trace = true;
             if (inside) {
                 const ObjK<R>& ob = sc.objs[p.obj];
+                const MediumK<R>& m = ob.med[p.c];
+                // The free-path draw (on a copy of the stream, committed only if the path
+                // is still inside) and the three gathers of the culling tests -- SDF at x,
+                // skip grid at x, SDF at the flight's end -- are issued together: one
+                // L2 round trip instead of three dependent ones. Same draws, same tests.
+                Rng r2 = p.rng;
+                R t_c = Real<R>::kInf;
+                if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
+                    const R u = r2.template uniform<R>();
+                    if (Real<R>::kIsDouble) t_c = -Real<R>::log1p_(-u) / m.sigma_t;
+                    else t_c = -Real<R>::div_(Real<R>::log_(R(1) - u), m.sigma_t);
+                }
+                bool in_grid = true, in_end = false;
+                R v = R(0), v_end = R(1);
+                if (!p.r_valid) v = sdf_raw(ob, p.x, &in_grid);
+                const R rs = skip_radius(ob, p.x);
+                if (!Real<R>::kIsDouble && a.convex_end && m.sigma_t > R(0))
+                    v_end = sdf_raw(ob, p.x + p.w * t_c, &in_end);
                 if (!p.r_valid) {
-                    bool in_grid;
-                    const R v = sdf_raw(ob, p.x, &in_grid);
                     p.r_here = v < R(0) ? -v : R(0);
                     p.r_valid = true;
                     if (leaked(ob, v, in_grid)) {
@@ -482,18 +498,13 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
                     }
                 }
                 if (inside) {
-                    const MediumK<R>& m = ob.med[p.c];
-                    if (m.sigma_t > R(0)) {  // sample_free_path (optics.cpp:55-60)
-                        const R u = p.rng.template uniform<R>();
-                        if (Real<R>::kIsDouble) t_free = -Real<R>::log1p_(-u) / m.sigma_t;
-                        else t_free = -Real<R>::div_(Real<R>::log_(R(1) - u), m.sigma_t);
-                    }
+                    p.rng = r2;
+                    t_free = t_c;
                     trace = !(t_free < p.r_here);
                     if (trace) {
-                        const R rs = skip_radius(ob, p.x);
                         trace = !(t_free < rs);
                         if (trace && a.convex_end)
-                            trace = !flight_contained(ob, p.x, p.w, t_free, Real<R>::fmax_(p.r_here, rs));
+                            trace = !end_contained(ob, v_end, in_end, t_free, Real<R>::fmax_(p.r_here, rs));
                     }
                 }
             }
