@@ -278,6 +278,14 @@ int sst_gpu_kernel_timing(sst_gpu_ctx* ctx, int enable, double* ms, uint64_t* la
 int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
                         const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
                         double* radiance, uint32_t* segments, sst_path_stats* stats);
+/* ... plus each path's exit state (exit_state: host double [6 n], may be NULL): the
+ * position and direction when the path ended -- escape: the last boundary exit (or the
+ * camera) and the escape direction; absorption or step cap: the collision point (a
+ * sphere step's centre) and the incoming direction. The "per-path exit state" of the
+ * parity bar; oracle/ref_shim.cpp ref_trace_paths_ex defines the same for the reference. */
+int sst_gpu_trace_paths_ex(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
+                           const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                           double* radiance, uint32_t* segments, double* exit_state, sst_path_stats* stats);
 
 /* ------------------------------------------------------------------------ */
 /* Verification hooks (csrc/verify.cuh): properties the fast paths rely on,    */

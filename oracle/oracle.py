@@ -61,6 +61,7 @@ def lib():
         L.so_dataset_fingerprint.argtypes = [P, U64, U64]
         L.so_dataset_fingerprint.restype = U64
         L.so_trace_paths.argtypes = [P, P, I, I, U64, U64, P, P, P, P, P, C.POINTER(abi.PathStats)]
+        L.so_trace_paths_ex.argtypes = [P, P, I, I, U64, U64, P, P, P, P, P, P, C.POINTER(abi.PathStats)]
     return _lib
 
 
@@ -185,17 +186,20 @@ class Scene:
         lib().so_bvh_intersect(self.h, ptr(o), ptr(d), t_min, t_max, C.byref(t), C.byref(tri))
         return t.value, tri.value
 
-    def trace_paths(self, models, integrator, nee, seed, pixel, sample, channel, stats=None):
+    def trace_paths(self, models, integrator, nee, seed, pixel, sample, channel, stats=None, exit_state=False):
+        """(radiance, segments) per path; with exit_state=True also (n, 6) final
+        position and direction."""
         pixel = np.ascontiguousarray(pixel, dtype=np.uint32)
         sample = np.ascontiguousarray(sample, dtype=np.uint32)
         channel = np.ascontiguousarray(channel, dtype=np.uint8)
         n = len(pixel)
         rad = np.empty(n)
         seg = np.empty(n, np.uint32)
-        check(lib().so_trace_paths(self.h, models.h if models is not None else None, integrator,
-                                   int(nee), seed, n, ptr(pixel), ptr(sample), ptr(channel), ptr(rad),
-                                   ptr(seg), C.byref(stats) if stats is not None else None))
-        return rad, seg
+        ex = np.empty((n, 6)) if exit_state else None
+        check(lib().so_trace_paths_ex(self.h, models.h if models is not None else None, integrator,
+                                      int(nee), seed, n, ptr(pixel), ptr(sample), ptr(channel), ptr(rad),
+                                      ptr(seg), ptr(ex), C.byref(stats) if stats is not None else None))
+        return (rad, seg, ex) if exit_state else (rad, seg)
 
 
 SAMPLE_DTYPE = np.dtype([("sigma_t", "<f4"), ("g", "<f4"), ("phi", "<f4"), ("n_events", "<u4"),

@@ -510,6 +510,10 @@ struct PathResult {
     double radiance = 0.0;
     uint32_t segments = 0, sphere_steps = 0, pt_events = 0, shadow = 0;
     int end = 0;  // 0 escaped, 1 absorbed, 2 capped
+    // exit state: position and direction when the path ends (escape: the last boundary
+    // exit / camera and the escape direction; absorption or cap: the collision point and
+    // the incoming direction)
+    Vec3 x, w;
 };
 
 static double r_min_for(const RefScene& s, int obj, int c) {
@@ -566,6 +570,8 @@ static PathResult trace_one(const RefScene& s, const ScatterModels* models, int 
         if (!entry) {
             res.radiance += s.background[c];
             res.end = 0;
+            res.x = x;
+            res.w = w;
             return res;
         }
         const int obj = static_cast<int>(s.tri_obj[entry->triangle]);
@@ -583,6 +589,8 @@ static PathResult trace_one(const RefScene& s, const ScatterModels* models, int 
             if (res.segments >= cap) {
                 res.radiance = 0.0;  // dropped
                 res.end = 2;
+                res.x = x;
+                res.w = w;
                 return res;
             }
             ++res.segments;
@@ -594,6 +602,8 @@ static PathResult trace_one(const RefScene& s, const ScatterModels* models, int 
                     sample_sphere_step(*models, m.sigma_t, m.g, m.phi, w, x, r, nee, rng);
                 if (o.absorbed) {
                     res.end = 1;
+                    res.x = x;
+                    res.w = w;
                     return res;
                 }
                 if (nee) {
@@ -607,6 +617,8 @@ static PathResult trace_one(const RefScene& s, const ScatterModels* models, int 
                 ++res.pt_events;
                 if (!(rng.uniform() < m.phi)) {  // Russian roulette by albedo
                     res.end = 1;
+                    res.x = x;
+                    res.w = w;
                     return res;
                 }
                 if (nee) {
@@ -622,9 +634,21 @@ static PathResult trace_one(const RefScene& s, const ScatterModels* models, int 
 }
 
 // Traces n explicit paths (parallel_for over paths; SST_THREADS threads).
+int ref_trace_paths_ex(void* scene, void* models, int integrator, int nee, uint64_t seed, uint64_t n,
+                       const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                       double* radiance, uint32_t* segments, double* exit_state, sst_path_stats* stats);
+
 int ref_trace_paths(void* scene, void* models, int integrator, int nee, uint64_t seed, uint64_t n,
                     const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
                     double* radiance, uint32_t* segments, sst_path_stats* stats) {
+    return ref_trace_paths_ex(scene, models, integrator, nee, seed, n, pixel, sample, channel, radiance, segments,
+                              nullptr, stats);
+}
+
+// ... and each path's exit state (exit_state: double [6 n], position then direction).
+int ref_trace_paths_ex(void* scene, void* models, int integrator, int nee, uint64_t seed, uint64_t n,
+                       const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                       double* radiance, uint32_t* segments, double* exit_state, sst_path_stats* stats) {
     auto* s = static_cast<RefScene*>(scene);
     auto* m = static_cast<ScatterModels*>(models);
     if (integrator == SST_INTEGRATOR_ST && !m) {
@@ -639,6 +663,15 @@ int ref_trace_paths(void* scene, void* models, int integrator, int nee, uint64_t
             const PathResult r = trace_one(*s, m, integrator, nee != 0, seed, pixel[i], sample[i], channel[i]);
             radiance[i] = r.radiance;
             if (segments) segments[i] = r.segments;
+            if (exit_state) {
+                double* e = exit_state + 6 * i;
+                e[0] = r.x.x;
+                e[1] = r.x.y;
+                e[2] = r.x.z;
+                e[3] = r.w.x;
+                e[4] = r.w.y;
+                e[5] = r.w.z;
+            }
             steps += r.sphere_steps;
             events += r.pt_events;
             shadow += r.shadow;

@@ -69,6 +69,7 @@ def _declare(L):
     L.ref_train_model.argtypes = [I, P, U64, U64, P, C.c_char_p, I, P, P, P]
     L.ref_save_dataset.argtypes = [C.c_char_p, U64, D, D, D, D, I, D, D, U64, P]
     L.ref_save_png.argtypes = [C.c_char_p, U32, U32, P]
+    L.ref_trace_paths_ex.argtypes = [P, P, I, I, U64, U64, P, P, P, P, P, P, P]
     L.ref_load_dataset.argtypes = [C.c_char_p, P, P, P, P, U64]
     L.ref_export_dataset_csv.argtypes = [C.c_char_p, U64, P]
     L.ref_make_icosphere.argtypes = [I, D, P, P, P, P]
@@ -227,17 +228,20 @@ class Scene:
             lib().ref_scene_free(self.h)
             self.h = None
 
-    def trace_paths(self, models, integrator, nee, seed, pixel, sample, channel, stats=None):
+    def trace_paths(self, models, integrator, nee, seed, pixel, sample, channel, stats=None, exit_state=False):
+        """(radiance, segments) per path; with exit_state=True also (n, 6) final
+        position and direction."""
         pixel = np.ascontiguousarray(pixel, dtype=np.uint32)
         sample = np.ascontiguousarray(sample, dtype=np.uint32)
         channel = np.ascontiguousarray(channel, dtype=np.uint8)
         n = len(pixel)
         rad = np.empty(n)
         seg = np.empty(n, dtype=np.uint32)
-        check(lib().ref_trace_paths(self.h, models.h if models is not None else None, integrator,
-                                    int(nee), seed, n, ptr(pixel), ptr(sample), ptr(channel), ptr(rad),
-                                    ptr(seg), C.byref(stats) if stats is not None else None))
-        return rad, seg
+        ex = np.empty((n, 6)) if exit_state else None
+        check(lib().ref_trace_paths_ex(self.h, models.h if models is not None else None, integrator,
+                                       int(nee), seed, n, ptr(pixel), ptr(sample), ptr(channel), ptr(rad),
+                                       ptr(seg), ptr(ex), C.byref(stats) if stats is not None else None))
+        return (rad, seg, ex) if exit_state else (rad, seg)
 
 
 # TrainingSample (dataset.hpp:17-27), 52 bytes, no padding.

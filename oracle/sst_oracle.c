@@ -793,7 +793,11 @@ static double nee_term(const so_scene* s, uint32_t obj, int c, v3 p, v3 w, doubl
     return weight * s->power[c] * phase * exp(-1.0 * tau) / d2;
 }
 
-typedef struct { double L; uint32_t seg, steps, events, shadow; int end; int err; } path_res;
+typedef struct { double L; uint32_t seg, steps, events, shadow; int end; int err; v3 x, w; } path_res;
+/* exit state: the path's position and direction when it ends (escape: the last boundary
+ * exit / camera and the escape direction; absorption or cap: the collision point and
+ * the incoming direction) */
+#define SO_END(code) do { r->x = x; r->w = w; r->end = (code); return; } while (0)
 
 static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint64_t seed,
                       uint32_t pixel, uint32_t sample, int c, path_res* r) {
@@ -811,7 +815,7 @@ static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint
     for (;;) {
         double t;
         uint32_t tri;
-        if (!intersect(s, x, w, 1e-9, 1e300, &t, &tri)) { r->L += s->bg[c]; r->end = 0; return; }
+        if (!intersect(s, x, w, 1e-9, 1e300, &t, &tri)) { r->L += s->bg[c]; SO_END(0); }
         const uint32_t obj = s->tobj[tri];
         const sst_medium m = s->media[3 * obj + c];
         const double rmin = r_min_for(s, obj, c);
@@ -824,7 +828,7 @@ static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint
                         r->seg, obj, x.x, x.y, x.z, w.x, w.y, w.z, t_free, hit_, hit_ ? t : 0.0);
             if (hit_) { x = add(x, mul(w, t)); break; }
             x = add(x, mul(w, t_free));
-            if (r->seg >= cap) { r->L = 0.0; r->end = 2; return; }
+            if (r->seg >= cap) { r->L = 0.0; SO_END(2); }
             ++r->seg;
             double rad = 0.0;
             if (integ == SST_INTEGRATOR_ST) {
@@ -835,14 +839,14 @@ static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint
             if (integ == SST_INTEGRATOR_ST && rad > rmin) {
                 ++r->steps;
                 step_out o;
-                if (sphere_step(ms, m.sigma_t, m.g, m.phi, w, x, rad, nee, &rng, &o)) { r->err = 1; r->L = 0.0; return; }
-                if (o.absorbed) { r->end = 1; return; }
+                if (sphere_step(ms, m.sigma_t, m.g, m.phi, w, x, rad, nee, &rng, &o)) { r->err = 1; r->L = 0.0; r->x = x; r->w = w; return; }
+                if (o.absorbed) SO_END(1);
                 if (nee) { r->L += nee_term(s, obj, c, o.rep_pos, o.rep_dir, o.lambda); ++r->shadow; }
                 x = o.exit_pos;
                 w = o.exit_dir;
             } else {
                 ++r->events;
-                if (!(so_uniform(&rng) < m.phi)) { r->end = 1; return; }
+                if (!(so_uniform(&rng) < m.phi)) SO_END(1);
                 if (nee) { r->L += nee_term(s, obj, c, x, w, 1.0); ++r->shadow; }
                 const double u1 = so_uniform(&rng);
                 const double u2 = so_uniform(&rng);
@@ -855,6 +859,12 @@ static void trace_one(const so_scene* s, so_models* ms, int integ, int nee, uint
 int so_trace_paths(const so_scene* s, so_models* m, int integ, int nee, uint64_t seed, uint64_t n,
                    const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
                    double* radiance, uint32_t* segments, sst_path_stats* st) {
+    return so_trace_paths_ex(s, m, integ, nee, seed, n, pixel, sample, channel, radiance, segments, NULL, st);
+}
+
+int so_trace_paths_ex(const so_scene* s, so_models* m, int integ, int nee, uint64_t seed, uint64_t n,
+                      const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                      double* radiance, uint32_t* segments, double* exit_state, sst_path_stats* st) {
     if (integ == SST_INTEGRATOR_ST && !m) return fail(SST_E_INVALID_ARGUMENT, "sphere tracing requires models");
     int err = 0;
     for (uint64_t i = 0; i < n; ++i) {
@@ -862,6 +872,11 @@ int so_trace_paths(const so_scene* s, so_models* m, int integ, int nee, uint64_t
         trace_one(s, m, integ, nee, seed, pixel[i], sample[i], channel[i], &r);
         radiance[i] = r.L;
         if (segments) segments[i] = r.seg;
+        if (exit_state) {
+            double* e = exit_state + 6 * i;
+            e[0] = r.x.x; e[1] = r.x.y; e[2] = r.x.z;
+            e[3] = r.w.x; e[4] = r.w.y; e[5] = r.w.z;
+        }
         if (st) {
             st->paths += 1;
             st->segments += r.seg;

@@ -69,6 +69,10 @@ int so_trace_paths(const so_scene* s, so_models* m, int integrator, int nee, uin
                    uint64_t n, const uint32_t* pixel, const uint32_t* sample,
                    const uint8_t* channel, double* radiance, uint32_t* segments,
                    sst_path_stats* stats);
+/* so_trace_paths plus each path's exit state (double [6 n]: final position, direction). */
+int so_trace_paths_ex(const so_scene* s, so_models* m, int integrator, int nee, uint64_t seed,
+                      uint64_t n, const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
+                      double* radiance, uint32_t* segments, double* exit_state, sst_path_stats* stats);
 
 /* Config 4: training-data generation (dataset.cpp:40-92 generate_dataset,
  * sphere_walk.cpp:22-102). Record layout = TrainingSample (dataset.hpp:17-27). */

@@ -166,7 +166,7 @@ EXPORTED = [
     "sst_gpu_sphere_step_batch", "sst_gpu_upload_scene", "sst_gpu_scene_info", "sst_gpu_get_sdf", "sst_gpu_render",
     "sst_gpu_trace_paths", "sst_gpu_read_stats", "sst_gpu_kernel_timing", "sst_gpu_generate_dataset",
     "sst_train_config_default", "sst_gpu_train_model", "sst_gpu_train_models",
-    "sst_gpu_verify_culling", "sst_gpu_nee_identity",
+    "sst_gpu_verify_culling", "sst_gpu_nee_identity", "sst_gpu_trace_paths_ex",
     # host utilities (no device work): include/sst_host.h
     "sst_mesh_icosphere", "sst_mesh_bumpy_sphere", "sst_mesh_load_obj", "sst_mesh_free",
     "sst_sdf_save", "sst_sdf_load", "sst_sdf_free", "sst_image_save_pfm", "sst_dataset_save",
@@ -231,6 +231,7 @@ def _declare(L):
     L.sst_dataset_load.argtypes = [C.c_char_p, C.POINTER(DatasetHeader), P, U64]
     L.sst_dataset_export_csv.argtypes = [C.c_char_p, U64, P]
     L.sst_gpu_trace_paths.argtypes = [P, I, I, U64, U64, P, P, P, P, P, C.POINTER(PathStats)]
+    L.sst_gpu_trace_paths_ex.argtypes = [P, I, I, U64, U64, P, P, P, P, P, P, C.POINTER(PathStats)]
     L.sst_mesh_icosphere.argtypes = [I, D, P, P, P, P]
     L.sst_mesh_bumpy_sphere.argtypes = [I, D, D, D, P, P, P, P]
     L.sst_mesh_load_obj.argtypes = [C.c_char_p, D, P, P, P, P, P]

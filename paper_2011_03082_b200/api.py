@@ -372,15 +372,18 @@ class Renderer:
                                                  int(seed), C.byref(rep)))
         return rep
 
-    def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None):
+    def trace_paths(self, integrator, nee, seed, pixel, sample, channel, stats=None, exit_state=False):
+        """Per-path parity entry (trace_sphere / trace_bruteforce per key): (radiance,
+        segments), plus the (n, 6) exit state (final position, direction) if asked."""
         pixel = np.ascontiguousarray(pixel, dtype=np.uint32)
         sample = np.ascontiguousarray(sample, dtype=np.uint32)
         channel = np.ascontiguousarray(channel, dtype=np.uint8)
         n = len(pixel)
         rad = np.empty(n)
         seg = np.empty(n, np.uint32)
+        ex = np.empty((n, 6)) if exit_state else None
         stats = stats if stats is not None else abi.PathStats()
-        abi.check(abi.lib().sst_gpu_trace_paths(self.h, integrator, int(nee), seed, n, _p(pixel),
-                                                _p(sample), _p(channel), _p(rad), _p(seg),
-                                                C.byref(stats)))
-        return rad, seg
+        abi.check(abi.lib().sst_gpu_trace_paths_ex(self.h, integrator, int(nee), seed, n, _p(pixel),
+                                                   _p(sample), _p(channel), _p(rad), _p(seg), _p(ex),
+                                                   C.byref(stats)))
+        return (rad, seg, ex) if exit_state else (rad, seg)

@@ -1056,8 +1056,9 @@ void run_trace(sst_gpu_ctx* ctx, const DevScene<R>& sc, bool st, bool explicit_k
                uint64_t seed, uint64_t n_paths, uint32_t n_pix, uint32_t sample_begin,
                const uint32_t* pix, const uint32_t* smp, const uint8_t* ch, R* radiance,
                uint32_t* segments, unsigned long long* work, cudaStream_t stream,
-               sst_gpu_ctx::Slot* wf, std::function<void()> on_finish, bool sync) {
+               sst_gpu_ctx::Slot* wf, std::function<void()> on_finish, bool sync, R* exit_state = nullptr) {
     TraceArgs<R> a{};
+    a.exit_state = exit_state;
     a.sc = sc;
     a.nee = nee;
     a.seed = seed;
@@ -1331,7 +1332,7 @@ void readback_films(sst_gpu_ctx* ctx, const double* dsum, const double* dsq, uin
 template <class R>
 void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
                       const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel,
-                      double* radiance, uint32_t* segments, sst_path_stats* stats) {
+                      double* radiance, uint32_t* segments, double* exit_state, sst_path_stats* stats) {
     const DevScene<R>& sc = scene_of<R>(ctx);
     const uint32_t n_pix = ctx->desc.width * ctx->desc.height;
     for (uint64_t i = 0; i < n; ++i) {
@@ -1346,6 +1347,8 @@ void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, 
     ctx->radiance.reserve(n * sizeof(R));
     ctx->segments.reserve(n * 4);
     ctx->work.reserve(sizeof(unsigned long long));
+    ScopedBuf dexit;
+    if (exit_state) dexit.reserve(6 * n * sizeof(R));
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
     ctx->timing_open = true;
     CK(cudaMemcpyAsync(ctx->keys_pix.p, pixel, n * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -1354,12 +1357,15 @@ void trace_paths_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, 
     run_trace<R>(ctx, sc, integrator == SST_INTEGRATOR_ST, true, nee, seed, n, n_pix, 0,
                  ctx->keys_pix.as<uint32_t>(), ctx->keys_smp.as<uint32_t>(), ctx->keys_ch.as<uint8_t>(),
                  ctx->radiance.as<R>(), ctx->segments.as<uint32_t>(), ctx->work.as<unsigned long long>(),
-                 ctx->stream, &ctx->slots[0], nullptr, true);
+                 ctx->stream, &ctx->slots[0], nullptr, true, exit_state ? dexit.as<R>() : nullptr);
     std::vector<R> rad(n);
     CK(cudaMemcpyAsync(rad.data(), ctx->radiance.p, n * sizeof(R), cudaMemcpyDeviceToHost, ctx->stream));
     if (segments) CK(cudaMemcpyAsync(segments, ctx->segments.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<R> ex(exit_state ? 6 * n : 0);
+    if (exit_state) CK(cudaMemcpyAsync(ex.data(), dexit.p, 6 * n * sizeof(R), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     for (uint64_t i = 0; i < n; ++i) radiance[i] = static_cast<double>(rad[i]);
+    for (uint64_t i = 0; i < ex.size(); ++i) exit_state[i] = static_cast<double>(ex[i]);
     collect_stats(ctx, stats);
 }
 
@@ -1850,15 +1856,24 @@ int sst_gpu_nee_identity(sst_gpu_ctx* ctx, uint64_t walks, uint32_t resamples, d
 int sst_gpu_trace_paths(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
                         const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel, double* radiance,
                         uint32_t* segments, sst_path_stats* stats) {
+    return sst_gpu_trace_paths_ex(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments, nullptr,
+                                  stats);
+}
+
+int sst_gpu_trace_paths_ex(sst_gpu_ctx* ctx, int integrator, int nee, uint64_t seed, uint64_t n,
+                           const uint32_t* pixel, const uint32_t* sample, const uint8_t* channel, double* radiance,
+                           uint32_t* segments, double* exit_state, sst_path_stats* stats) {
     return guarded([&] {
         require_device(ctx);
         check_render_ready(ctx, integrator);
         if (n == 0) return;
         if (!pixel || !sample || !channel || !radiance) throw InvalidArgument("null path key buffers");
         if (ctx->precision == SST_PREC_F64)
-            trace_paths_impl<double>(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments, stats);
+            trace_paths_impl<double>(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments,
+                                     exit_state, stats);
         else
-            trace_paths_impl<float>(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments, stats);
+            trace_paths_impl<float>(ctx, integrator, nee, seed, n, pixel, sample, channel, radiance, segments,
+                                    exit_state, stats);
     });
 }
 

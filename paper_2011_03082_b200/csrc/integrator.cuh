@@ -100,6 +100,18 @@ struct PathLocal {
     R t_pend;
 };
 
+// The path's exit state (trace_paths_ex): position and direction when it ended.
+template <class R>
+SST_D void write_exit_state(R* e, const PathLocal<R>& p) {
+    e += 6 * p.id;
+    e[0] = p.x.x;
+    e[1] = p.x.y;
+    e[2] = p.x.z;
+    e[3] = p.w.x;
+    e[4] = p.w.y;
+    e[5] = p.w.z;
+}
+
 struct LaneStats {
     uint32_t paths = 0, absorbed = 0, escaped = 0, capped = 0, errors = 0;
     uint64_t seg = 0, sphere = 0, events = 0, shadow = 0;
@@ -445,6 +457,7 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
                         if (phase == 4u) {  // kPhEnded: absorbed once those were in
                             a.radiance[p.id] = p.L;
                             if (a.segments) a.segments[p.id] = p.seg;
+                            if (a.exit_state) write_exit_state(a.exit_state, p);
                             ++st.paths;
                             st.seg += p.seg;
                             ++st.absorbed;
@@ -472,6 +485,7 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
         if (alive && end >= 0) {
             a.radiance[p.id] = p.L;
             if (a.segments) a.segments[p.id] = p.seg;
+            if (a.exit_state) write_exit_state(a.exit_state, p);
             ++st.paths;
             st.seg += p.seg;
             st.escaped += end == kEndEscaped;

@@ -195,6 +195,7 @@ struct TraceArgs {
     const uint8_t* channel;
     R* radiance;             // [n_paths]
     uint32_t* segments;      // [n_paths] or null
+    R* exit_state;           // [6 n_paths] final position, direction (trace_paths_ex) or null
     unsigned long long* work;   // path-id counter
     unsigned long long* stats;  // [kStCount]
     int sphere_batch;           // warp regrouping threshold for sphere steps (lanes)

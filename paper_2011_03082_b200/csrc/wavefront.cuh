@@ -237,6 +237,7 @@ template <class R>
 SST_D void finish_path(const TraceArgs<R>& a, const PathLocal<R>& p, int end, LaneStats& st) {
     a.radiance[p.id] = p.L;
     if (a.segments) a.segments[p.id] = p.seg;
+    if (a.exit_state) write_exit_state(a.exit_state, p);
     ++st.paths;
     st.seg += p.seg;
     st.escaped += end == kEndEscaped;

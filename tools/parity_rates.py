@@ -42,6 +42,20 @@ def renderer(precision, **env):
     return r
 
 
+def exit_rates(g_ex, o_ex, same):
+    """Per-path exit state (final position, direction): relative position error
+    |dx| / max(|x|, 1) and direction error |dw|, over paths with equal segment counts."""
+    dx = np.linalg.norm(g_ex[:, :3] - o_ex[:, :3], axis=1) / np.maximum(np.linalg.norm(o_ex[:, :3], axis=1), 1.0)
+    dw = np.linalg.norm(g_ex[:, 3:] - o_ex[:, 3:], axis=1)
+    e = np.maximum(dx, dw)
+    out = {"exit_all_paths": {}, "exit_equal_segments": {}}
+    for rt in (1e-6, 1e-5, 1e-4, 1e-3):
+        out["exit_all_paths"][f"{rt:g}"] = float((e <= rt).mean())
+        out["exit_equal_segments"][f"{rt:g}"] = float((e[same] <= rt).mean()) if same.any() else 1.0
+    out["exit_p999"] = float(np.quantile(e[same], 0.999)) if same.any() else 0.0
+    return out
+
+
 def rates(g_rad, g_seg, o_rad, o_seg):
     same = g_seg == o_seg
     rel = np.abs(g_rad - o_rad) / np.maximum(np.abs(o_rad), 1e-300)
@@ -101,13 +115,14 @@ def main():
         ch = rng.integers(0, 3, n).astype(np.uint8)
         for integ in (sb.ST, sb.PT):
             t0 = time.perf_counter()
-            o_rad, o_seg = rsc.trace_paths(models, integ, 1, 1, pix, smp, ch)
+            o_rad, o_seg, o_ex = rsc.trace_paths(models, integ, 1, 1, pix, smp, ch, exit_state=True)
             t_ref = time.perf_counter() - t0
             for (prec, eng), r in rs.items():
-                g_rad, g_seg = r.trace_paths(integ, 1, 1, pix, smp, ch)
+                g_rad, g_seg, g_ex = r.trace_paths(integ, 1, 1, pix, smp, ch, exit_state=True)
                 row = {"scene": sname, "integrator": "ST" if integ == sb.ST else "PT", "precision": prec,
                        "engine": eng, "ref_s": t_ref}
                 row.update(rates(g_rad, g_seg, o_rad, o_seg))
+                row.update(exit_rates(g_ex, o_ex, g_seg == o_seg))
                 print(json.dumps(row), flush=True)
                 res.append(row)
     for r in rs.values():
