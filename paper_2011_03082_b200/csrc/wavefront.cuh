@@ -892,25 +892,21 @@ template <class R>
 SST_D void wf_shadow(const TraceArgs<R>& a, const WfPool<R>& q, bool with_sphere) {
     uint64_t tris = 0, shadow = 0;
     const uint32_t n = q.counts[kQShadow];
-    uint32_t i_next = warp_fetch(q.counts + kQFetchShadow);  // fetched one batch ahead
     for (;;) {
-        const uint32_t i = i_next;
-        if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
-        i_next = warp_fetch(q.counts + kQFetchShadow);
+        const uint32_t i = warp_fetch(q.counts + kQFetchShadow);
 #ifndef SST_WF_NO_PREFETCH
-        if ((threadIdx.x & 31u) == 0) prefetch_shadow(q, i_next, 32u, n);
+        if ((threadIdx.x & 31u) == 0) prefetch_shadow(q, i, 32u, n);
 #endif
+        if (i - (threadIdx.x & 31u) >= n) break;  // warp-uniform
         if (i >= n) continue;
         shadow_one(a, q, q.q_shadow[i], tris);
         ++shadow;
     }
     if (with_sphere) {
         const uint32_t ns = q.counts[kQShadowS];
-        uint32_t j_next = warp_fetch(q.counts + kQFetchShadowS);
         for (;;) {
-            const uint32_t i = j_next;
+            const uint32_t i = warp_fetch(q.counts + kQFetchShadowS);
             if (i - (threadIdx.x & 31u) >= ns) break;  // warp-uniform
-            j_next = warp_fetch(q.counts + kQFetchShadowS);
             if (i >= ns) continue;
             shadow_one(a, q, q.q_shadow[q.cap * (kNeeChain + 1u) - 1u - i], tris);
             ++shadow;
