@@ -69,3 +69,39 @@ def test_two_contexts_different_models_async_interleaved(models_dir, tmp_path):
     finally:
         A.close()
         B.close()
+
+
+def test_failed_upload_leaves_no_half_moved_scene(models_dir):
+    """A rejected light (checked before anything is touched) keeps the previous scene; a
+    failure after the previous scene's objects were reused (here: a bad triangle index
+    in the second object) leaves NO scene -- never a moved-from one (api.cu upload_scene)."""
+    import numpy as np
+
+    import paper_2011_03082_b200 as sb
+    from paper_2011_03082_b200 import abi
+    mesh = sb.make_icosphere(3, 1.0)
+    r = sb.Renderer(0, "f32")
+    try:
+        r.load_models_dir(models_dir)
+        good = sb.c5_scene(mesh, 32, 18, sdf_resolution=24)
+        r.upload_scene(good)
+        sdf0 = r.get_sdf(0)[3].copy()
+        bad_light = sb.c5_scene(mesh, 32, 18, sdf_resolution=24)
+        bad_light.light_kind = 2
+        with pytest.raises(abi.InvalidArgument):
+            r.upload_scene(bad_light)
+        assert np.array_equal(r.get_sdf(0)[3], sdf0)  # the previous scene is intact
+        img, st = r.render(sb.ST, 2)
+        assert st.paths == 32 * 18 * 3 * 2
+        bad_tri = sb.c5_scene(mesh, 32, 18, sdf_resolution=24)  # object 0 identical: reused
+        P, T = bad_tri.objects[1].positions, bad_tri.objects[1].triangles.copy()
+        T[0, 0] = len(P) + 5
+        bad_tri.objects[1].triangles = T
+        with pytest.raises(abi.InvalidArgument):
+            r.upload_scene(bad_tri)
+        with pytest.raises(abi.InvalidArgument, match="no scene"):
+            r.get_sdf(0)
+        r.upload_scene(good)  # and the context recovers
+        assert np.array_equal(r.get_sdf(0)[3], sdf0)
+    finally:
+        r.close()
