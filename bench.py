@@ -63,10 +63,10 @@ def mlp_flops(dl, dp, de):
 # Algorithmic per-unit work of each wavefront kernel (counted from the
 # device counters of the measured slab):
 #   wf_logic  HBM (layout basis): per slot visit the path state it must read (x,L 16 +
-#             w,r 16 + rng 8 + meta 16 + trace position 4 = 60 B, + flight 4 B while a
-#             traversal is queued), write back and its live-list entry (68 B in all);
-#             per flight it sends to the trace kernel the 36 B ray record + trace position
-#             (4 B) + the 12 B result it reads back next pass; per fresh path the
+#             w,r 16 + rng 8 + meta 16 = 56 B; meta.z holds the trace-queue position while
+#             a traversal is queued), write back and its live-list entry (60 B in all);
+#             per flight it sends to the trace kernel the 36 B ray record + the 12 B
+#             result it reads back next pass; per fresh path the
 #             camera-ray result and direction (28 B); per delta-tracking event its NEE
 #             record + queue entry (36 B); per sphere request a queue entry (4 B).
 #   wf_logic  HBM (SURVEY §8(d) basis, `frac_survey`): 96 B per segment (48 B state read
@@ -76,7 +76,7 @@ def mlp_flops(dl, dp, de):
 #   wf_shadow FP32: 51 FLOP per light-grid triangle test.
 #   wf_sphere FP32: decoder MLP FLOPs 2*(112 nL + 480 nP + 640 nE).
 NODE_FLOP, TRI_FLOP = 36.0, 51.0
-LOGIC_BYTES_PER_SLOT, LOGIC_BYTES_PER_FLIGHT, LOGIC_BYTES_PER_FRESH = 128.0, 52.0, 28.0
+LOGIC_BYTES_PER_SLOT, LOGIC_BYTES_PER_FLIGHT, LOGIC_BYTES_PER_FRESH = 116.0, 48.0, 28.0
 NEE_RECORD_BYTES, SPHERE_QUEUE_BYTES = 36.0, 4.0
 SURVEY_BYTES_PER_SEGMENT = 96.0
 

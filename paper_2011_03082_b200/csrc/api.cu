@@ -821,14 +821,15 @@ void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
 bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
 
 // Sizes of the wavefront pool's arrays for `cap` slots (carve_pool order).
-constexpr int kPoolArrays = 23;
+constexpr int kPoolArrays = 21;
 template <class R>
 size_t pool_layout(uint32_t cap, size_t (&off)[kPoolArrays]) {
     const size_t n = cap, nk = n * kNeeChain;
-    const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R), n * sizeof(R),
-                            n * 8, nk * sizeof(Q4<R>), nk * sizeof(Q4<R>), n * 4, n * 4, (nk + n) * 4, n * 4,
+    const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R),
+                            n * 8, nk * sizeof(Q4<R>), nk * sizeof(Q4<R>), n * 4, (nk + n) * 4, n * 4,
                             kQCount * 4, 8, n * 4, n * 4, n * 4,
                             n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>), nk * sizeof(R)};
+    static_assert(sizeof(sizes) / sizeof(sizes[0]) == kPoolArrays, "pool arrays");
     size_t total = 0;
     int k = 0;
     for (size_t b : sizes) {
@@ -850,25 +851,23 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.wr = reinterpret_cast<Q4<R>*>(base + off[1]);
     q.rng = reinterpret_cast<uint64_t*>(base + off[2]);
     q.meta = reinterpret_cast<uint4*>(base + off[3]);
-    q.tpend = reinterpret_cast<R*>(base + off[4]);
-    q.thit = reinterpret_cast<R*>(base + off[5]);
-    q.hinfo = reinterpret_cast<uint2*>(base + off[6]);
-    q.nee_p = reinterpret_cast<Q4<R>*>(base + off[7]);
-    q.nee_w = reinterpret_cast<Q4<R>*>(base + off[8]);
-    q.tq = reinterpret_cast<uint32_t*>(base + off[9]);
-    q.q_sphere = reinterpret_cast<uint32_t*>(base + off[10]);
-    q.q_shadow = reinterpret_cast<uint32_t*>(base + off[11]);
-    q.q_live = reinterpret_cast<uint32_t*>(base + off[12]);
-    q.counts = reinterpret_cast<uint32_t*>(base + off[13]);
-    q.resume_work = reinterpret_cast<unsigned long long*>(base + off[14]);
-    q.q_la = reinterpret_cast<uint32_t*>(base + off[15]);
-    q.q_lb = reinterpret_cast<uint32_t*>(base + off[16]);
-    q.q_free = reinterpret_cast<uint32_t*>(base + off[17]);
-    q.tr_o = reinterpret_cast<Q4<R>*>(base + off[18]);
-    q.tr_d = reinterpret_cast<Q4<R>*>(base + off[19]);
-    q.tr_f = reinterpret_cast<uint32_t*>(base + off[20]);
-    q.tr_cam = reinterpret_cast<Q4<R>*>(base + off[21]);
-    q.nee_res = reinterpret_cast<R*>(base + off[22]);
+    q.thit = reinterpret_cast<R*>(base + off[4]);
+    q.hinfo = reinterpret_cast<uint2*>(base + off[5]);
+    q.nee_p = reinterpret_cast<Q4<R>*>(base + off[6]);
+    q.nee_w = reinterpret_cast<Q4<R>*>(base + off[7]);
+    q.q_sphere = reinterpret_cast<uint32_t*>(base + off[8]);
+    q.q_shadow = reinterpret_cast<uint32_t*>(base + off[9]);
+    q.q_live = reinterpret_cast<uint32_t*>(base + off[10]);
+    q.counts = reinterpret_cast<uint32_t*>(base + off[11]);
+    q.resume_work = reinterpret_cast<unsigned long long*>(base + off[12]);
+    q.q_la = reinterpret_cast<uint32_t*>(base + off[13]);
+    q.q_lb = reinterpret_cast<uint32_t*>(base + off[14]);
+    q.q_free = reinterpret_cast<uint32_t*>(base + off[15]);
+    q.tr_o = reinterpret_cast<Q4<R>*>(base + off[16]);
+    q.tr_d = reinterpret_cast<Q4<R>*>(base + off[17]);
+    q.tr_f = reinterpret_cast<uint32_t*>(base + off[18]);
+    q.tr_cam = reinterpret_cast<Q4<R>*>(base + off[19]);
+    q.nee_res = reinterpret_cast<R*>(base + off[20]);
     return q;
 }
 
@@ -1141,6 +1140,10 @@ void ensure_pipeline(sst_gpu_ctx* ctx) {
         CK(cudaEventCreateWithFlags(&sl.wf_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sl.wf_join, cudaEventDisableTiming));
         sl.work.reserve(sizeof(unsigned long long));
+        // the wavefront's pinned count buffers: cudaMallocHost on a slot's first job
+        // (mid-pipeline, e.g. inside a timed stretch of asynchronous calls) stalls it
+        CK(cudaMallocHost(&sl.wf_host, 2 * kQCount * sizeof(uint32_t)));
+        for (auto& e : sl.wf_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
     CK(cudaEventCreate(&ctx->ev0));

@@ -152,9 +152,8 @@ struct WfPool {
     Q4<R>* xl;        // position, radiance
     Q4<R>* wr;        // direction, SDF radius at the position
     uint64_t* rng;    // RandomStream state
-    uint4* meta;      // path id, segments, skip triangle, packed obj/channel/flags/phase/cull
-    R* tpend;         // free-flight length of the queued traversal
-    uint32_t* tq;     // trace-queue position of the slot's queued traversal
+    uint4* meta;      // path id, segments, skip triangle (while a traversal is queued: its
+                      // trace-queue position), packed obj/channel/flags/phase/cull
     // Trace queue as contiguous ray records (indexed by queue position, written by
     // the logic / generation kernels, read coalesced by k_wf_trace), and the
     // traversal results at the same positions (read by the next logic pass).

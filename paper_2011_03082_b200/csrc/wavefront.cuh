@@ -106,20 +106,26 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
     p.L = xl.w;
     p.w = mk<R>(wr.x, wr.y, wr.z);
     p.r_here = wr.w;
-    p.t_pend = need_tpend && meta_phase(m.w) == kPhTrace ? q.tpend[s] : Real<R>::kInf;
+    p.t_pend = Real<R>::kInf;
+    // meta.z: the skip triangle, or -- while a traversal is queued -- the record's trace-
+    // queue position (the record carries the skip triangle and the flight length; only
+    // the megakernel hand-off reads them back: a logic visit takes the traversal result)
+    const bool queued = meta_phase(m.w) == kPhTrace;
+    p.skip = queued ? -1 : static_cast<int>(m.z);
+    if (need_tpend && queued && !(m.w & kMetaFresh)) {
+        p.t_pend = q.tr_o[m.z].w;
+        p.skip = bits_int<R>(q.tr_d[m.z].w);
+    }
     if (m.w & kMetaFresh) {  // camera ray: the state is in the trace record
-        const uint32_t j = q.tq[s];
-        const Q4<R> d = q.tr_cam[j];
+        const Q4<R> d = q.tr_cam[m.z];
         p.x = sc_cam_pos;
         p.w = mk<R>(d.x, d.y, d.z);
         p.L = R(0);
         p.r_here = R(0);
-        p.t_pend = Real<R>::kInf;
     }
     p.rng.s = q.rng[s];
     p.id = m.x;
     p.seg = m.y;
-    p.skip = static_cast<int>(m.z);
     p.obj = meta_obj(m.w);
     p.c = static_cast<uint8_t>(meta_c(m.w));
     p.r_valid = (m.w >> 10) & 1u;
@@ -149,16 +155,25 @@ SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* 
     load_slot_from(q, s, q.meta[s], p, phase, cam, need_tpend, fold);
 }
 
-// pending: staged NEE records not yet added to L; flags: kMetaEndAbsorbed.
+// pending: staged NEE records not yet added to L; flags: kMetaEndAbsorbed. A slot that
+// queues a traversal stores its meta after the queue append (slot_meta with z = the
+// record's position; store_state here).
 template <class R>
-SST_D void store_slot(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p, uint32_t phase, uint32_t pending = 0u,
-                      uint32_t flags = 0u) {
+SST_D void store_state(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p) {
     q.xl[s] = Q4<R>{p.x.x, p.x.y, p.x.z, p.L};
     q.wr[s] = Q4<R>{p.w.x, p.w.y, p.w.z, p.r_here};
     q.rng[s] = p.rng.s;
-    q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), p.seg, static_cast<uint32_t>(p.skip),
-                           pack_meta(p.obj, p.c, p.r_valid, phase, p.cull) | (pending << kMetaPendShift) | flags);
-    if (phase == kPhTrace) q.tpend[s] = p.t_pend;
+}
+template <class R>
+SST_D uint4 slot_meta(const PathLocal<R>& p, uint32_t z, uint32_t phase, uint32_t pending = 0u, uint32_t flags = 0u) {
+    return make_uint4(static_cast<uint32_t>(p.id), p.seg, z,
+                      pack_meta(p.obj, p.c, p.r_valid, phase, p.cull) | (pending << kMetaPendShift) | flags);
+}
+template <class R>
+SST_D void store_slot(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p, uint32_t phase, uint32_t pending = 0u,
+                      uint32_t flags = 0u) {
+    store_state(q, s, p);
+    q.meta[s] = slot_meta(p, static_cast<uint32_t>(p.skip), phase, pending, flags);
 }
 
 // Staged NEE record i of slot s.
@@ -394,15 +409,14 @@ enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitFree = 4 };
 // traversal, a sphere step or a shadow ray (at most one per iteration), or its path
 // ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
-SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, unsigned m, LaneStats& st,
-                        bool* live, WfRec<R>& rec, uint32_t* nrec_out) {
+SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, const uint4 mt, unsigned m,
+                        LaneStats& st, bool* live, WfRec<R>& rec, uint32_t* nrec_out, uint4* meta_out) {
     // m: the lanes of this warp calling (converged). The loop below has no break /
     // continue / return inside: every stage is an if-block that all lanes of the warp
     // reach together, so lanes that got to a collision by different routes (after a
     // traversal, or after a flight that needed none) run it in ONE warp pass.
     const DevScene<R>& sc = a.sc;
     PathLocal<R> p;
-    const uint4 mt = q.meta[s];
     const Mailbox<R> mb = load_mailbox(q, s);
     uint32_t phase = meta_phase(mt.w);
     *live = false;
@@ -424,9 +438,8 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
     uint2 hi = make_uint2(0u, 0u);
     R t_hit = R(0);
     if (phase == kPhTrace) {
-        const uint32_t j = q.tq[s];
-        hi = q.hinfo[j];
-        t_hit = q.thit[j];
+        hi = q.hinfo[mt.z];
+        t_hit = q.thit[mt.z];
     }
     load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false, true, &mb);
     ++st.lane_iters;
@@ -586,12 +599,20 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, u
         q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
         return kEmitFree;
     }
-    store_slot(q, s, p, phase, nrec);
     *live = true;
     *nrec_out = nrec;
+    if (emit == kEmitTrace) {  // meta stored by the caller once the record's position is known
+        store_state(q, s, p);
+        *meta_out = slot_meta(p, 0u, kPhTrace, nrec);
+    } else {
+        store_slot(q, s, p, phase, nrec);
+    }
     return emit;
 }
 
+// Processes the input list of live slots (all slots on the first iteration); slots
+// still live afterwards form the output list (stream compaction), so drained slots
+// cost nothing in later iterations.
 // Processes the input list of live slots (all slots on the first iteration); slots
 // still live afterwards form the output list (stream compaction), so drained slots
 // cost nothing in later iterations.
@@ -611,17 +632,16 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
             l2_prefetch(q.xl + nb, cnt * sizeof(Q4<R>));
             l2_prefetch(q.wr + nb, cnt * sizeof(Q4<R>));
             l2_prefetch(q.rng + nb, cnt * sizeof(uint64_t));
-            l2_prefetch(q.tpend + nb, cnt * sizeof(R));
-            l2_prefetch(q.tq + nb, cnt * sizeof(uint32_t));
         }
 #endif
         int emit = kEmitNone;
         bool live = false;
         uint32_t nrec = 0u;
         WfRec<R> rec;
+        uint4 mo;
         const uint32_t s = i < n_in ? (q.q_in ? q.q_in[i] : i) : 0u;
         const unsigned m = __ballot_sync(0xffffffffu, i < n_in);
-        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, m, st, &live, rec, &nrec);
+        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, q.meta[s], m, st, &live, rec, &nrec, &mo);
         const bool want[4] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitFree};
         uint32_t* const ctr[4] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
                                   q.counts + kQFree};
@@ -629,9 +649,9 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
         uint32_t pos[4];
         // the staged NEE records of the visit go onto the shadow queue as record indices
         block_pushn_counted<4>(want, s, ctr, qs, pos, nrec, s * kNeeChain, q.counts + kQShadow, q.q_shadow);
-        if (emit == kEmitTrace) {
+        if (emit == kEmitTrace) {  // the record at its queue position; its position in the meta
             put_trace(q, pos[1], rec);
-            q.tq[s] = pos[1];
+            q.meta[s] = make_uint4(mo.x, mo.y, pos[1], mo.w);
         }
     }
     flush_lane_stats(a.stats, st);
@@ -673,11 +693,10 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
         // only the id/flags and the RNG go to the slot (scattered stores); position and
         // direction stay in the camera-ray record (kMetaFresh, load_slot)
         q.rng[s] = p.rng.s;
-        q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), 0u, static_cast<uint32_t>(-1),
-                               pack_meta(-1, p.c, false, kPhTrace, -1) | kMetaFresh);
         const uint32_t ci = EX ? 0u : (c0 + i) % 3u;
         const uint32_t owner = i >= ci ? i - ci : 0u;
         const uint32_t j = t0 + rank(owner);
+        q.meta[s] = make_uint4(static_cast<uint32_t>(p.id), 0u, j, pack_meta(-1, p.c, false, kPhTrace, -1) | kMetaFresh);
         if (owner == i) {
             WfRec<R> rec;
             rec.a = p.x;
@@ -687,7 +706,6 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
             rec.v = 1u << 9;  // no cull, outside, camera ray
             put_trace(q, j, rec);
         }
-        q.tq[s] = j;
         q.q_out[l0 + i] = s;
     }
     __shared__ bool last;
