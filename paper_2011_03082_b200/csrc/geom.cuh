@@ -39,7 +39,7 @@ SST_D R sdf_raw(const ObjK<R>& o, V3<R> p, bool* inside_grid) {
                    z = static_cast<uint32_t>(rz);
     if (x >= o.dims[0] || y >= o.dims[1] || z >= o.dims[2]) return R(0);
     *inside_grid = true;
-    return static_cast<R>(__ldg(o.sdf + (static_cast<size_t>(z) * o.dims[1] + y) * o.dims[0] + x));
+    return static_cast<R>(ldg_keep(o.sdf + (static_cast<size_t>(z) * o.dims[1] + y) * o.dims[0] + x));
 }
 
 // query_safe_radius: -v inside (v < 0), else 0; 0 outside the grid.
@@ -60,7 +60,7 @@ SST_D R skip_radius(const ObjK<R>& o, V3<R> p) {
     if (rx < R(0) || ry < R(0) || rz < R(0)) return R(0);
     const uint32_t x = static_cast<uint32_t>(rx), y = static_cast<uint32_t>(ry), z = static_cast<uint32_t>(rz);
     if (x >= o.skip_dims[0] || y >= o.skip_dims[1] || z >= o.skip_dims[2]) return R(0);
-    const uint8_t q = __ldg(o.skip + (static_cast<size_t>(z) * o.skip_dims[1] + y) * o.skip_dims[0] + x);
+    const uint8_t q = ldg_keep(o.skip + (static_cast<size_t>(z) * o.skip_dims[1] + y) * o.skip_dims[0] + x);
     return static_cast<R>(q) * o.skip_unit;
 }
 
@@ -178,8 +178,8 @@ SST_D void load_node(const void* nodes, int i, R (&b)[12], int& c0, int& c1, int
 template <>
 SST_D void load_node<float>(const void* nodes, int i, float (&b)[12], int& c0, int& c1, int& o0, int& o1) {
     const NodeF* n = static_cast<const NodeF*>(nodes) + i;
-    const float4 a = __ldg(&n->a), bb = __ldg(&n->b), c = __ldg(&n->c);
-    const int4 d = __ldg(&n->d);
+    const float4 a = ldg_keep(&n->a), bb = ldg_keep(&n->b), c = ldg_keep(&n->c);
+    const int4 d = ldg_keep(&n->d);
     // b = lo0x hi0x lo0y hi0y lo0z hi0z | lo1x hi1x lo1y hi1y lo1z hi1z
     b[0] = a.x; b[1] = a.y; b[2] = a.z; b[3] = a.w; b[4] = c.x; b[5] = c.y;
     b[6] = bb.x; b[7] = bb.y; b[8] = bb.z; b[9] = bb.w; b[10] = c.z; b[11] = c.w;
@@ -206,7 +206,7 @@ template <>
 SST_D void load_tri<float>(const void* tris, uint32_t i, V3<float>& v0, V3<float>& e1,
                            V3<float>& e2, uint32_t& obj, uint32_t& id) {
     const TriF* t = static_cast<const TriF*>(tris) + i;
-    const float4 a = __ldg(&t->v0o), b = __ldg(&t->e1i), c = __ldg(&t->e2);
+    const float4 a = ldg_keep(&t->v0o), b = ldg_keep(&t->e1i), c = ldg_keep(&t->e2);
     v0 = mk(a.x, a.y, a.z);
     e1 = mk(b.x, b.y, b.z);
     e2 = mk(c.x, c.y, c.z);
@@ -428,12 +428,12 @@ template <class R>
 SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int c,
                            uint64_t& n_tris) {
     const uint32_t cell = cube_cell<R>(-ray.d.x, -ray.d.y, -ray.d.z, sc.grid_res);
-    const uint32_t b = __ldg(sc.grid_off + cell), e = __ldg(sc.grid_off + cell + 1);
+    const uint32_t b = ldg_keep(sc.grid_off + cell), e = ldg_keep(sc.grid_off + cell + 1);
     n_tris += e - b;
     R tau = R(0);
     const bool direct = !Real<R>::kIsDouble && sc.grid_tris;  // cell's triangles stored contiguously
     for (uint32_t k = b; k < e; ++k) {
-        const uint32_t i = direct ? k : __ldg(sc.grid_tri + k);
+        const uint32_t i = direct ? k : ldg_keep(sc.grid_tri + k);
         V3<R> v0, e1, e2;
         uint32_t obj, id;
         load_tri<R>(direct ? sc.grid_tris : sc.tris, i, v0, e1, e2, obj, id);
