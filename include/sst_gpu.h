@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SST_GPU_ABI_VERSION 3  /* 3: sst_scene_desc light_kind / light_direction */
+#define SST_GPU_ABI_VERSION 4  /* 3: sst_scene_desc light_kind / light_direction; 4: sst_cull_report planes */
 
 enum {
     SST_OK = 0,
@@ -305,6 +305,8 @@ typedef struct {
     uint64_t violations_sdf, violations_skip, violations_endpoint_convex, violations_endpoint_twoball;
     uint64_t radius_violations;      /* SDF safe radius > exact distance to the surface */
     uint64_t skip_radius_violations; /* skip-grid radius > exact distance */
+    /* (v4) convex end point strictly inside the face planes of its SDF voxel */
+    uint64_t culled_endpoint_planes, violations_endpoint_planes;
 } sst_cull_report;
 int sst_gpu_verify_culling(sst_gpu_ctx* ctx, uint64_t n, uint64_t seed, sst_cull_report* out);
 

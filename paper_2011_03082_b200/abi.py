@@ -106,7 +106,8 @@ class CullReport(C.Structure):
     _fields_ = [(n, U64) for n in ("flights", "culled_sdf", "culled_skip", "culled_endpoint_convex",
                                    "culled_endpoint_twoball", "violations_sdf", "violations_skip",
                                    "violations_endpoint_convex", "violations_endpoint_twoball",
-                                   "radius_violations", "skip_radius_violations")]
+                                   "radius_violations", "skip_radius_violations",
+                                   "culled_endpoint_planes", "violations_endpoint_planes")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -175,7 +176,7 @@ EXPORTED = [
 ]
 
 _lib = None
-ABI_VERSION = 3  # include/sst_gpu.h SST_GPU_ABI_VERSION
+ABI_VERSION = 4  # include/sst_gpu.h SST_GPU_ABI_VERSION
 
 
 def lib():

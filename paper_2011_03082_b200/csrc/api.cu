@@ -109,6 +109,10 @@ struct ObjectHost {
     double skip_voxel = 0.0, skip_unit = 0.0;
     uint32_t skip_dims[3] = {0, 0, 0};
     bool convex = false;
+    // FP32 end-point face-plane lists (types.cuh ObjK::plane_off / planes), convex only
+    std::vector<uint32_t> plane_off;
+    std::vector<float> planes;  // 4 per plane: unit outward normal, offset
+    float plane_eps = 0.0f;
 };
 
 }  // namespace
@@ -151,7 +155,7 @@ struct sst_gpu_ctx {
     DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri;
     DevBuf grid_tris32;  // FP32 triangle records in light-grid list order (grid_tri gathered)
     uint32_t grid_res = 0;
-    std::vector<DevBuf> sdf_dev, skip_dev;
+    std::vector<DevBuf> sdf_dev, skip_dev, plane_off_dev, planes_dev;
     DevScene<float> sc32{};
     DevScene<double> sc64{};
 
@@ -376,6 +380,89 @@ void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, 
     oh.sdf_voxel = a.voxel;
 }
 
+// Face-plane lists of a convex object (integrator.cuh end_inside_planes): for every SDF
+// voxel whose stored value is -0 (centre inside, within half a diagonal of the surface)
+// the planes of the faces that can meet the voxel -- a superset (triangle box overlaps
+// the voxel and the plane passes within half a diagonal of the centre) is enough, since
+// every face plane of a convex object bounds it. tv[first, first + n): the object's
+// outward-wound triangles.
+void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<double, 3>, 3>>& tv, size_t first,
+                       size_t n) {
+    oh.plane_off.clear();
+    oh.planes.clear();
+    if (!oh.convex) return;
+    const uint32_t nx = oh.dims[0], ny = oh.dims[1], nz = oh.dims[2];
+    const size_t nvox = static_cast<size_t>(nx) * ny * nz;
+    const double h = oh.sdf_voxel, hd = 0.5 * std::sqrt(3.0) * h;
+    auto eligible = [&](size_t k) { return oh.sdf[k] == 0.0f && std::signbit(oh.sdf[k]); };
+    struct Pl {
+        double n[3], d;
+    };
+    std::vector<Pl> pl(n);
+    double scale = 0.0;
+    for (size_t t = 0; t < n; ++t) {
+        const auto& c = tv[first + t];
+        const double e1[3] = {c[1][0] - c[0][0], c[1][1] - c[0][1], c[1][2] - c[0][2]};
+        const double e2[3] = {c[2][0] - c[0][0], c[2][1] - c[0][1], c[2][2] - c[0][2]};
+        double nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+        const double l = std::sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+        if (!(l > 0.0)) {  // degenerate: no area, never crossed
+            pl[t] = Pl{{0, 0, 0}, 0};
+            continue;
+        }
+        for (double& v : nn) v /= l;
+        pl[t] = Pl{{nn[0], nn[1], nn[2]}, nn[0] * c[0][0] + nn[1] * c[0][1] + nn[2] * c[0][2]};
+        for (int a = 0; a < 3; ++a)
+            for (int k = 0; k < 3; ++k) scale = std::fmax(scale, std::fabs(c[a][k]));
+    }
+    // candidate (voxel, face) pairs, counted then filled (CSR)
+    std::vector<uint32_t> cnt(nvox + 1, 0);
+    auto for_pairs = [&](auto&& fn) {
+        for (size_t t = 0; t < n; ++t) {
+            const Pl& p = pl[t];
+            if (p.n[0] == 0.0 && p.n[1] == 0.0 && p.n[2] == 0.0) continue;
+            const auto& c = tv[first + t];
+            int lo[3], hi[3];
+            for (int a = 0; a < 3; ++a) {
+                const double mn = std::fmin(c[0][a], std::fmin(c[1][a], c[2][a]));
+                const double mx = std::fmax(c[0][a], std::fmax(c[1][a], c[2][a]));
+                lo[a] = std::max(0, static_cast<int>(std::floor((mn - oh.sdf_origin[a]) / h)) - 1);
+                hi[a] = std::min(static_cast<int>(oh.dims[a]) - 1, static_cast<int>(std::floor((mx - oh.sdf_origin[a]) / h)) + 1);
+            }
+            for (int z = lo[2]; z <= hi[2]; ++z)
+                for (int y = lo[1]; y <= hi[1]; ++y)
+                    for (int x = lo[0]; x <= hi[0]; ++x) {
+                        const size_t k = (static_cast<size_t>(z) * ny + y) * nx + x;
+                        if (!eligible(k)) continue;
+                        const double cc[3] = {oh.sdf_origin[0] + (x + 0.5) * h, oh.sdf_origin[1] + (y + 0.5) * h,
+                                              oh.sdf_origin[2] + (z + 0.5) * h};
+                        // the triangle's box must overlap the voxel (slightly grown) ...
+                        bool overlap = true;
+                        for (int a = 0; a < 3; ++a) {
+                            const double mn = std::fmin(c[0][a], std::fmin(c[1][a], c[2][a]));
+                            const double mx = std::fmax(c[0][a], std::fmax(c[1][a], c[2][a]));
+                            overlap = overlap && mn <= cc[a] + 0.5 * h * (1.0 + 1e-6) && mx >= cc[a] - 0.5 * h * (1.0 + 1e-6);
+                        }
+                        // ... and its plane pass within half a diagonal of the centre
+                        const double dist = p.n[0] * cc[0] + p.n[1] * cc[1] + p.n[2] * cc[2] - p.d;
+                        if (overlap && std::fabs(dist) <= hd * (1.0 + 1e-6)) fn(k, t);
+                    }
+        }
+    };
+    for_pairs([&](size_t k, size_t) { ++cnt[k + 1]; });
+    for (size_t k = 0; k < nvox; ++k) cnt[k + 1] += cnt[k];
+    oh.plane_off = cnt;
+    oh.planes.resize(4 * static_cast<size_t>(cnt[nvox]));
+    std::vector<uint32_t> fill(cnt.begin(), cnt.end() - 1);
+    for_pairs([&](size_t k, size_t t) {
+        float* q = oh.planes.data() + 4 * static_cast<size_t>(fill[k]++);
+        for (int a = 0; a < 3; ++a) q[a] = static_cast<float>(pl[t].n[a]);
+        q[3] = static_cast<float>(pl[t].d);
+    });
+    // margin: far above the FP32 error of n.e - d at this coordinate scale (~1e-7 x scale)
+    oh.plane_eps = static_cast<float>(1e-4 * h + 4e-6 * std::fmax(scale, 1.0));
+}
+
 // Fine skip grid of one object (2x the SDF resolution over the SDF's box).
 void build_skip_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh) {
     SkipBuildArgs a{};
@@ -428,6 +515,13 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
         ok[o].skip_unit = static_cast<R>(oh.skip_unit);
         for (int a = 0; a < 3; ++a) ok[o].skip_dims[a] = oh.skip_dims[a];
         ok[o].convex = oh.convex ? 1u : 0u;
+        {
+            const char* e = std::getenv("SST_NO_PLANES");
+            const bool use = std::is_same<R, float>::value && !oh.plane_off.empty() && !(e && e[0] == '1');
+            ok[o].plane_off = use ? ctx->plane_off_dev[o].as<uint32_t>() : nullptr;
+            ok[o].planes = use ? ctx->planes_dev[o].as<float4>() : nullptr;
+            ok[o].plane_eps = oh.plane_eps;
+        }
         {
             const auto& roots = ctx->scene_cache.bvh.obj_root;
             const char* e = std::getenv("SST_OBJ_ROOT");
@@ -695,6 +789,7 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         }
         build_skip_gpu(ctx, od, objs[o]);
         objs[o].convex = is_convex(od.positions, od.n_vertices, tri);
+        build_plane_lists(objs[o], tv, tv.size() - od.n_triangles, od.n_triangles);
         if (ctx->obj_cache.size() >= 64) ctx->obj_cache.clear();
         ctx->obj_cache[ofp] = objs[o];
     }
@@ -754,6 +849,8 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
     if (ctx->sdf_dev.size() < ctx->objects.size()) {
         ctx->sdf_dev.resize(ctx->objects.size());
         ctx->skip_dev.resize(ctx->objects.size());
+        ctx->plane_off_dev.resize(ctx->objects.size());
+        ctx->planes_dev.resize(ctx->objects.size());
     }
     for (size_t o = 0; o < ctx->objects.size(); ++o) {
         const auto& s = ctx->objects[o].sdf;
@@ -762,9 +859,21 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         const auto& k = ctx->objects[o].skip;
         ctx->skip_dev[o].reserve(std::max<size_t>(k.size(), 1));
         if (!k.empty()) CK(cudaMemcpyAsync(ctx->skip_dev[o].p, k.data(), k.size(), cudaMemcpyHostToDevice, ctx->stream));
+        const auto& po = ctx->objects[o].plane_off;
+        const auto& pp = ctx->objects[o].planes;
+        ctx->plane_off_dev[o].reserve(std::max<size_t>(po.size(), 1) * sizeof(uint32_t));
+        ctx->planes_dev[o].reserve(std::max<size_t>(pp.size(), 4) * sizeof(float));
+        if (!po.empty())
+            CK(cudaMemcpyAsync(ctx->plane_off_dev[o].p, po.data(), po.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               ctx->stream));
+        if (!pp.empty())
+            CK(cudaMemcpyAsync(ctx->planes_dev[o].p, pp.data(), pp.size() * sizeof(float), cudaMemcpyHostToDevice,
+                               ctx->stream));
     }
     uint64_t bytes = bvh.nodes_f32.size() + bvh.tris_f32.size() + bvh.nodes_f64.size() + bvh.tris_f64.size();
-    for (const auto& o : ctx->objects) bytes += o.sdf.size() * sizeof(float) + o.skip.size();
+    for (const auto& o : ctx->objects)
+        bytes += o.sdf.size() * sizeof(float) + o.skip.size() + o.plane_off.size() * sizeof(uint32_t) +
+                 o.planes.size() * sizeof(float);
     bytes += ctx->scene_bytes_grid;
     bytes += ctx->objects.size() * (sizeof(ObjK<float>) + sizeof(ObjK<double>));
     ctx->scene_bytes = bytes;
@@ -1404,6 +1513,8 @@ void verify_culling_impl(sst_gpu_ctx* ctx, uint64_t n, uint64_t seed, sst_cull_r
     out->violations_endpoint_twoball = h[kCvViolTwoBall];
     out->radius_violations = h[kCvRadiusViol];
     out->skip_radius_violations = h[kCvSkipRadiusViol];
+    out->culled_endpoint_planes = h[kCvCullPlanes];
+    out->violations_endpoint_planes = h[kCvViolPlanes];
 }
 }  // namespace
 
@@ -1473,6 +1584,8 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         b->release();
     for (auto& b : ctx->sdf_dev) b.release();
     for (auto& b : ctx->skip_dev) b.release();
+    for (auto& b : ctx->plane_off_dev) b.release();
+    for (auto& b : ctx->planes_dev) b.release();
     for (auto& e : ctx->kt_ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->film_pin_ev)

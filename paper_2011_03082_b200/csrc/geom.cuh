@@ -22,7 +22,7 @@ namespace sstg {
 
 // --------------------------------------------------------------- SDF lookup
 template <class R>
-SST_D R sdf_raw(const ObjK<R>& o, V3<R> p, bool* inside_grid) {
+SST_D R sdf_raw(const ObjK<R>& o, V3<R> p, bool* inside_grid, uint32_t* vox = nullptr) {
     R rx, ry, rz;
     if (Real<R>::kIsDouble) {  // (point - origin) / voxel_size, sdf.cpp:61
         rx = (p.x - o.sdf_origin[0]) / o.sdf_voxel;
@@ -39,7 +39,9 @@ SST_D R sdf_raw(const ObjK<R>& o, V3<R> p, bool* inside_grid) {
                    z = static_cast<uint32_t>(rz);
     if (x >= o.dims[0] || y >= o.dims[1] || z >= o.dims[2]) return R(0);
     *inside_grid = true;
-    return static_cast<R>(ldg_keep(o.sdf + (static_cast<size_t>(z) * o.dims[1] + y) * o.dims[0] + x));
+    const uint32_t k = (z * o.dims[1] + y) * o.dims[0] + x;
+    if (vox) *vox = k;
+    return static_cast<R>(ldg_keep(o.sdf + k));
 }
 
 // query_safe_radius: -v inside (v < 0), else 0; 0 outside the grid.

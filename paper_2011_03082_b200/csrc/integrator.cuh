@@ -171,21 +171,55 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
 // Any object: the safe balls at the two end points (radius r_x at the start -- the
 // larger of the SDF and skip-grid bounds -- and the SDF safe radius at the end) cover the
 // segment when r_x + r_y > t, so it cannot cross the surface either.
+// Exact end-point containment for convex objects (FP32): the end point e lies in an
+// SDF voxel V whose centre c is inside the object and within half a diagonal of the
+// surface; F_V = every face that can meet V. If e is strictly inside every plane of F_V,
+// e is inside the object: otherwise the segment [c, e] (inside V) leaves the object
+// through a face of F_V and e would be beyond that face's plane. A convex object then
+// contains the whole flight [x, e] (x inside), so it cannot cross the surface --
+// exactly the traversal's answer, without the traversal. The margin plane_eps (>> the
+// FP32 error of the plane test) keeps end points on the surface on the traced side.
+template <class R>
+SST_D bool end_inside_planes(const ObjK<R>& ob, uint32_t vox, V3<R> e) {
+    if constexpr (Real<R>::kIsDouble) {
+        return false;
+    } else {
+        if (!ob.plane_off) return false;
+        const uint32_t b = ldg_keep(ob.plane_off + vox), en = ldg_keep(ob.plane_off + vox + 1);
+        if (b == en) return false;
+        for (uint32_t k = b; k < en; ++k) {
+            const float4 pl = ldg_keep(ob.planes + k);
+            if (!(fmaf(pl.x, e.x, fmaf(pl.y, e.y, fmaf(pl.z, e.z, -pl.w))) < -ob.plane_eps)) return false;
+        }
+        return true;
+    }
+}
+
+// Culling rule that decided a contained flight (verification counters).
+enum : int { kContainNone = 0, kContainSdf = 1, kContainPlanes = 2 };
+template <class R>
+SST_D int flight_contained_rule(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
+    if (Real<R>::kIsDouble) return kContainNone;
+    bool in_grid;
+    uint32_t vox = 0;
+    const V3<R> e = x + w * t;
+    const R v = sdf_raw(ob, e, &in_grid, &vox);
+    if (!in_grid) return kContainNone;
+    if (v < R(0) && (ob.convex || t < r_x - v)) return kContainSdf;
+    return ob.convex && end_inside_planes(ob, vox, e) ? kContainPlanes : kContainNone;
+}
 template <class R>
 SST_D bool flight_contained(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
-    if (Real<R>::kIsDouble) return false;
-    bool in_grid;
-    const R v = sdf_raw(ob, x + w * t, &in_grid);
-    if (!in_grid || !(v < R(0))) return false;
-    return ob.convex || t < r_x - v;
+    return flight_contained_rule(ob, x, w, t, r_x) != kContainNone;
 }
 
 // flight_contained with the end point's SDF value already loaded (wavefront logic pass).
 template <class R>
-SST_D bool end_contained(const ObjK<R>& ob, R v_end, bool in_grid, R t, R r_x) {
+SST_D bool end_contained(const ObjK<R>& ob, R v_end, bool in_grid, uint32_t vox, V3<R> e, R t, R r_x) {
     if (Real<R>::kIsDouble) return false;
-    if (!in_grid || !(v_end < R(0))) return false;
-    return ob.convex || t < r_x - v_end;
+    if (!in_grid) return false;
+    if (v_end < R(0) && (ob.convex || t < r_x - v_end)) return true;
+    return ob.convex && end_inside_planes(ob, vox, e);
 }
 
 // FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)

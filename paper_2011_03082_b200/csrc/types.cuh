@@ -65,6 +65,14 @@ struct ObjK {
     R skip_inv_voxel, skip_unit;
     uint32_t skip_dims[3];
     uint32_t convex;  // closed convex mesh: a ray leaving it cannot hit it again
+    // FP32, convex objects: per SDF voxel whose centre is inside and within half a
+    // diagonal of the surface (stored value -0), the planes (unit outward normal, offset)
+    // of every face that can meet the voxel, CSR (plane_off[v] .. plane_off[v + 1]); a
+    // point of such a voxel strictly inside all of them is inside the object
+    // (integrator.cuh end_inside_planes). Null: no lists.
+    const uint32_t* plane_off;
+    const float4* planes;
+    float plane_eps;  // required margin below every plane
     int32_t bvh_root;  // FP32 in-medium traversals start here (host.h FlatBvh::obj_root); 0 = root
 };
 
@@ -247,7 +255,7 @@ struct StepBatchArgs {
 // counters of k_verify_cull (sst_cull_report order)
 enum : int {
     kCvFlights = 0, kCvCullSdf, kCvCullSkip, kCvCullConvex, kCvCullTwoBall, kCvViolSdf, kCvViolSkip,
-    kCvViolConvex, kCvViolTwoBall, kCvRadiusViol, kCvSkipRadiusViol, kCvCount
+    kCvViolConvex, kCvViolTwoBall, kCvRadiusViol, kCvSkipRadiusViol, kCvCullPlanes, kCvViolPlanes, kCvCount
 };
 
 template <class R>

@@ -5,7 +5,8 @@
 //    rule). Random free flights inside the media -- uniform in the SDF box and just
 //    below the surface, where the rules are tight -- go through the PRODUCTION
 //    predicates of the logic pass (same device functions, same precision build):
-//    SDF safe radius, skip-grid radius, convex / two-ball end-point containment. Each
+//    SDF safe radius, skip-grid radius, convex / two-ball end-point containment, the
+//    convex end point's face-plane test (integrator.cuh end_inside_planes). Each
 //    culled flight is checked against the exact FP64 geometry: brute force over every
 //    triangle (Moller-Trumbore without epsilon on (0, t]), and every queried radius
 //    against the exact point-mesh distance. Any hit is a violation.
@@ -136,7 +137,7 @@ SST_D void verify_cull(const CullCheckArgs<R>& a) {
     const ObjK<R>& ob = sc.objs[o];
     V3<R> w = mk<R>(R(0), R(0), R(1));
     R t = R(0);
-    bool cull_sdf = false, cull_skip = false, cull_end = false;
+    bool cull_sdf = false, cull_skip = false, cull_end = false, cull_planes = false;
     R r_here = R(0), rs = R(0);
     if (active) {
         const double cz = 1.0 - 2.0 * rng.template uniform<double>();
@@ -153,7 +154,11 @@ SST_D void verify_cull(const CullCheckArgs<R>& a) {
         if (!cull_sdf) {
             rs = skip_radius(ob, x);
             cull_skip = t < rs;
-            if (!cull_skip && a.convex_end) cull_end = flight_contained(ob, x, w, t, Real<R>::fmax_(r_here, rs));
+            if (!cull_skip && a.convex_end) {
+                const int rule = flight_contained_rule(ob, x, w, t, Real<R>::fmax_(r_here, rs));
+                cull_end = rule == kContainSdf;
+                cull_planes = rule == kContainPlanes;
+            }
         } else {
             rs = skip_radius(ob, x);
         }
@@ -192,6 +197,8 @@ SST_D void verify_cull(const CullCheckArgs<R>& a) {
         c[kCvViolSkip] = cull_skip && hit;
         c[kCvViolConvex] = cull_end && ob.convex && hit;
         c[kCvViolTwoBall] = cull_end && !ob.convex && hit;
+        c[kCvCullPlanes] = cull_planes;
+        c[kCvViolPlanes] = cull_planes && hit;
         c[kCvRadiusViol] = static_cast<double>(r_here) > dist;
         c[kCvSkipRadiusViol] = static_cast<double>(rs) > dist;
     }

@@ -499,10 +499,12 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                 }
                 bool in_grid = true, in_end = false;
                 R v = R(0), v_end = R(1);
+                uint32_t vox_end = 0;
+                const V3<R> x_end = p.x + p.w * t_c;
                 if (!p.r_valid) v = sdf_raw(ob, p.x, &in_grid);
                 const R rs = skip_radius(ob, p.x);
                 if (!Real<R>::kIsDouble && a.convex_end && m.sigma_t > R(0))
-                    v_end = sdf_raw(ob, p.x + p.w * t_c, &in_end);
+                    v_end = sdf_raw(ob, x_end, &in_end, &vox_end);
                 if (!p.r_valid) {
                     p.r_here = v < R(0) ? -v : R(0);
                     p.r_valid = true;
@@ -518,7 +520,8 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                     if (trace) {
                         trace = !(t_free < rs);
                         if (trace && a.convex_end)
-                            trace = !end_contained(ob, v_end, in_end, t_free, Real<R>::fmax_(p.r_here, rs));
+                            trace = !end_contained(ob, v_end, in_end, vox_end, x_end, t_free,
+                                                   Real<R>::fmax_(p.r_here, rs));
                     }
                 }
             }

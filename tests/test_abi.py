@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(abi.EXPORTED)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.sst_gpu_abi_version() == abi.ABI_VERSION == 3
+    assert L.sst_gpu_abi_version() == abi.ABI_VERSION == 4
 
 
 def test_library_is_built_for_sm100a_only():

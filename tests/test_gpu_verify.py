@@ -4,8 +4,8 @@ Conservativeness (acceptance 8 -- "zero sphere-triangle intersectio
 queried radii", extended to every flight-culling rule the wavefront uses): >= 1e6
 random in-medium flights per scene through the production FP32 predicates, every
 culled flight and every queried radius checked against exact FP64 geometry. Zero
-violations allowed. Scenes: the bench's C5 (convex icospheres: SDF, skip grid and
-convex end-point culling) and the C3 bumpy sphere (non-convex: two-ball culling).
+violations allowed. Scenes: the bench's C5 (convex icospheres: SDF, skip grid, convex
+end-point culling and the end voxel's face-plane test) and the C3 bumpy sphere (non-convex: two-ball culling).
 
 NEE estimator identity (acceptance 7): the single-representative
 Lambda-weighted estimate (k ~ phi^k, the dataset generator's sample_representative)
@@ -43,6 +43,7 @@ def test_flight_culling_is_conservative(renderer, scene_name, precision):
     if precision == "f32":
         if scene_name == "c5":
             assert rep["culled_endpoint_convex"] > 0, rep
+            assert rep["culled_endpoint_planes"] > 0, rep  # face-plane test of the end voxel
         else:
             assert rep["culled_endpoint_twoball"] > 0, rep
 
