@@ -113,6 +113,7 @@ struct ObjectHost {
     std::vector<uint32_t> plane_off;
     std::vector<float> planes;  // 4 per plane: unit outward normal, offset
     float plane_eps = 0.0f;
+    double bsphere[4] = {0, 0, 0, 0};  // bounding sphere of the vertices (centre, radius)
 };
 
 }  // namespace
@@ -193,6 +194,7 @@ struct sst_gpu_ctx {
         cudaEvent_t film_done = nullptr;
         // wavefront pool (wavefront.cuh) + pinned queue counters read by the host loop
         DevBuf wf;
+        DevBuf keys;  // camera pre-pass: [count u32, pad] + compacted key list (wf_cam_filter)
         uint32_t* wf_host = nullptr;  // [2][kQCount]
         cudaEvent_t wf_ev[2] = {nullptr, nullptr};
         // concurrent half of a wavefront iteration (sphere + shadow) and its fork/join
@@ -210,6 +212,7 @@ struct sst_gpu_ctx {
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
     bool wf_concurrent = true;  // SST_WF_CONCURRENT=0: one stream per iteration
+    bool cam_filter = true;     // SST_CAM_FILTER=0: every camera ray through the wavefront
     int convex_end = 1;         // SST_CONVEX_END=0: trace every flight the SDF/skip bounds do not cull
     // launches with fewer paths use the megakernel (the wavefront's per-iteration costs
     // dominate below ~3e5 paths: tools/small_render_crossover.py); SST_WF_MIN_PATHS
@@ -515,6 +518,16 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
         ok[o].skip_unit = static_cast<R>(oh.skip_unit);
         for (int a = 0; a < 3; ++a) ok[o].skip_dims[a] = oh.skip_dims[a];
         ok[o].convex = oh.convex ? 1u : 0u;
+        {  // bounding sphere, radius grown past the FP error of camera_ray_may_hit
+            double dc2 = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                const double dk = oh.bsphere[k] - d.cam_position[k];
+                dc2 += dk * dk;
+            }
+            const double r = oh.bsphere[3];
+            for (int k = 0; k < 3; ++k) ok[o].bsphere[k] = static_cast<R>(oh.bsphere[k]);
+            ok[o].bsphere[3] = static_cast<R>(r * (1.0 + 1e-3) + 1e-5 * dc2 / std::fmax(r, 1e-3) + 1e-5);
+        }
         {
             const char* e = std::getenv("SST_NO_PLANES");
             const bool use = std::is_same<R, float>::value && !oh.plane_off.empty() && !(e && e[0] == '1');
@@ -790,6 +803,27 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         build_skip_gpu(ctx, od, objs[o]);
         objs[o].convex = is_convex(od.positions, od.n_vertices, tri);
         build_plane_lists(objs[o], tv, tv.size() - od.n_triangles, od.n_triangles);
+        {  // bounding sphere: box centre, farthest referenced vertex
+            double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+            for (const auto& t : tri)
+                for (uint32_t vi : t)
+                    for (int k = 0; k < 3; ++k) {
+                        lo[k] = std::fmin(lo[k], od.positions[3 * vi + k]);
+                        hi[k] = std::fmax(hi[k], od.positions[3 * vi + k]);
+                    }
+            double r2 = 0.0;
+            for (int k = 0; k < 3; ++k) objs[o].bsphere[k] = 0.5 * (lo[k] + hi[k]);
+            for (const auto& t : tri)
+                for (uint32_t vi : t) {
+                    double d2 = 0.0;
+                    for (int k = 0; k < 3; ++k) {
+                        const double dk = od.positions[3 * vi + k] - objs[o].bsphere[k];
+                        d2 += dk * dk;
+                    }
+                    r2 = std::fmax(r2, d2);
+                }
+            objs[o].bsphere[3] = std::sqrt(r2);
+        }
         if (ctx->obj_cache.size() >= 64) ctx->obj_cache.clear();
         ctx->obj_cache[ofp] = objs[o];
     }
@@ -1132,6 +1166,22 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
     j.stream = stream;
     j.cap = static_cast<uint32_t>(std::max<uint64_t>(32, std::min<uint64_t>(a.n_paths, ctx->wf_pool)));
     a.pool = carve_pool<R>(sl, j.cap);
+    a.keys = nullptr;
+    a.keys_count = nullptr;
+    if (ctx->cam_filter && a.sc.n_objects <= 64 && (explicit_keys || a.n_paths % 3 == 0)) {
+        // camera pre-pass: paths whose camera ray misses every bounding sphere end here
+        const uint64_t n_keys = explicit_keys ? a.n_paths : a.n_paths / 3;
+        sl.keys.reserve(16 + 4 * n_keys);
+        uint32_t* cnt = sl.keys.as<uint32_t>();
+        CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), stream));
+        kt_begin(ctx, stream);  // timed as generation work
+        if constexpr (std::is_same<R, float>::value)
+            CK(f32::launch_wf_cam_filter(a, explicit_keys, static_cast<uint32_t>(n_keys), cnt + 4, cnt, stream));
+        else CK(f64::launch_wf_cam_filter(a, explicit_keys, static_cast<uint32_t>(n_keys), cnt + 4, cnt, stream));
+        kt_end(ctx, stream, SST_KT_WF_GEN);
+        a.keys = cnt + 4;
+        a.keys_count = cnt;
+    }
     j.a = a;
     if (!sl.wf_host) {
         CK(cudaMallocHost(&sl.wf_host, 2 * kQCount * sizeof(uint32_t)));
@@ -1336,16 +1386,19 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         size_t off[kPoolArrays];
         const uint64_t cap = std::max<uint64_t>(32, std::min<uint64_t>(per_sample * chunk, ctx->wf_pool));
         const size_t pool = pool_layout<R>(static_cast<uint32_t>(cap), off);
+        const size_t keys = 16 + 4 * (per_sample * chunk / 3 + 1);  // camera pre-pass list
         bool grow = false;
         for (int k = 0; k < n_slots; ++k) {
             const auto& s2 = ctx->slots[k];
-            grow |= s2.rad.bytes < per_sample * chunk * sizeof(R) || s2.wf.bytes < pool;
+            grow |= s2.rad.bytes < per_sample * chunk * sizeof(R) || s2.wf.bytes < pool ||
+                    (ctx->cam_filter && s2.keys.bytes < keys);
         }
         if (grow) {
             drain_jobs(ctx);
             for (int k = 0; k < n_slots; ++k) {
                 ctx->slots[k].rad.reserve(per_sample * chunk * sizeof(R));
                 ctx->slots[k].wf.reserve(pool);
+                if (ctx->cam_filter) ctx->slots[k].keys.reserve(keys);
             }
         }
     }
@@ -1555,6 +1608,7 @@ int sst_gpu_create(int device, sst_gpu_ctx** out) {
         if (const char* e = std::getenv("SST_WF_TAIL")) ctx->wf_tail = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("SST_WF_BATCH")) ctx->wf_batch = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SST_WF_CONCURRENT")) ctx->wf_concurrent = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SST_CAM_FILTER")) ctx->cam_filter = std::atoi(e) != 0;
         if (const char* e = std::getenv("SST_CONVEX_END")) ctx->convex_end = std::atoi(e) != 0;
         if (const char* e = std::getenv("SST_WF_MIN_PATHS")) ctx->wf_min_paths = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("SST_WF_CHUNK")) ctx->wf_chunk = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
@@ -1599,6 +1653,7 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         sl.rad.release();
         sl.work.release();
         sl.wf.release();
+        sl.keys.release();
         if (sl.wf_host) cudaFreeHost(sl.wf_host);
         for (auto& e : sl.wf_ev)
             if (e) cudaEventDestroy(e);

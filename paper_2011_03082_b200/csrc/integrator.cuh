@@ -119,8 +119,26 @@ struct LaneStats {
     DecodeCount dc;
 };
 
+// Camera ray direction of (pixel, sample): jitter = the first two draws of the pixel
+// stream (DESIGN.md camera model).
+template <class R>
+SST_D V3<R> camera_dir(const TraceArgs<R>& a, uint32_t pixel, uint32_t sample) {
+    const DevScene<R>& sc = a.sc;
+    Rng cam{rng_key(a.seed, 0x06, pixel, sample)};  // kRenderPixel
+    const R jx = cam.uniform<R>();
+    const R jy = cam.uniform<R>();
+    const uint32_t px = pixel % sc.width, py = pixel / sc.width;
+    const R sx = (R(2) * (static_cast<R>(px) + jx) / static_cast<R>(sc.width) - R(1)) * sc.tan_half * sc.aspect;
+    const R sy = (R(1) - R(2) * (static_cast<R>(py) + jy) / static_cast<R>(sc.height)) * sc.tan_half;
+    return normalize(sc.cam_fwd + sc.cam_right * sx + sc.cam_up * sy);
+}
+
 template <class R, bool EXPLICIT>
 SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
+    if (a.keys) {  // camera pre-pass: the id-th path whose camera ray can hit the scene
+        id = EXPLICIT ? static_cast<uint64_t>(a.keys[id])
+                      : static_cast<uint64_t>(a.keys[id / 3]) * 3u + static_cast<uint32_t>(id % 3);
+    }
     uint32_t pixel, sample, c;
     if (EXPLICIT) {
         pixel = a.pixel[id];
@@ -138,14 +156,8 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
         sample = a.sample_begin + static_cast<uint32_t>(rest / a.n_pix);
     }
     const DevScene<R>& sc = a.sc;
-    Rng cam{rng_key(a.seed, 0x06, pixel, sample)};  // kRenderPixel
-    const R jx = cam.uniform<R>();
-    const R jy = cam.uniform<R>();
-    const uint32_t px = pixel % sc.width, py = pixel / sc.width;
-    const R sx = (R(2) * (static_cast<R>(px) + jx) / static_cast<R>(sc.width) - R(1)) * sc.tan_half * sc.aspect;
-    const R sy = (R(1) - R(2) * (static_cast<R>(py) + jy) / static_cast<R>(sc.height)) * sc.tan_half;
     p.x = sc.cam_pos;
-    p.w = normalize(sc.cam_fwd + sc.cam_right * sx + sc.cam_up * sy);
+    p.w = camera_dir(a, pixel, sample);
     p.rng.s = rng_key(a.seed, 0x07, pixel, 3ull * sample + c);  // kRenderChannel
     p.L = R(0);
     p.id = id;

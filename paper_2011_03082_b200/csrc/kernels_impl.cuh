@@ -111,6 +111,11 @@ __global__ void __launch_bounds__(kWfBlock, SST_WF_SHADOW_BLOCKS) k_wf_shadow(Tr
 __global__ void __launch_bounds__(kWfBlock) k_wf_compact(TraceArgs<R> a) { wf_compact<R>(a.pool); }
 __global__ void __launch_bounds__(kWfBlock) k_wf_init(TraceArgs<R> a) { wf_init<R>(a.pool); }
 __global__ void k_wf_reset(TraceArgs<R> a) { wf_reset<R>(a.pool); }
+template <bool EX>
+__global__ void __launch_bounds__(kWfBlock) k_wf_cam_filter(TraceArgs<R> a, uint32_t n_keys, uint32_t* list,
+                                                            uint32_t* count) {
+    wf_cam_filter<R, EX>(a, n_keys, list, count);
+}
 
 // ---------------------------------------------------------------------------
 // Config 4: training-data generation (persistent, one sample per lane).
@@ -190,6 +195,14 @@ static unsigned wf_grid(K kernel, uint32_t items, size_t smem = 0) {
     const uint64_t need = (static_cast<uint64_t>(items) + kWfBlock - 1) / kWfBlock;
     if (g > need) g = need;
     return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_wf_cam_filter(const TraceArgs<R>& a, bool explicit_keys, uint32_t n_keys, uint32_t* list,
+                                 uint32_t* count, cudaStream_t s) {
+    if (n_keys == 0) return cudaSuccess;
+    if (explicit_keys) k_wf_cam_filter<true><<<wf_grid(k_wf_cam_filter<true>, n_keys), kWfBlock, 0, s>>>(a, n_keys, list, count);
+    else k_wf_cam_filter<false><<<wf_grid(k_wf_cam_filter<false>, n_keys), kWfBlock, 0, s>>>(a, n_keys, list, count);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_wf_init(const TraceArgs<R>& a, cudaStream_t s) {

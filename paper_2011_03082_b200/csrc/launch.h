@@ -16,6 +16,8 @@ constexpr int kTraceBlock = 32;  // one warp per block: a long-path tail strands
     cudaError_t launch_trace(const TraceArgs<REAL>& a, bool st, bool explicit_keys,             \
                              cudaStream_t s);                                                   \
     cudaError_t launch_wf_init(const TraceArgs<REAL>& a, cudaStream_t s);                       \
+    cudaError_t launch_wf_cam_filter(const TraceArgs<REAL>& a, bool explicit_keys, uint32_t n_keys, \
+                                     uint32_t* list, uint32_t* count, cudaStream_t s);            \
     cudaError_t launch_wf_iteration(const TraceArgs<REAL>& a, bool st, bool explicit_keys,      \
                                     cudaStream_t s, cudaEvent_t* ev, cudaStream_t side,         \
                                     cudaEvent_t fork, cudaEvent_t join, uint32_t live_hint);    \

@@ -74,6 +74,9 @@ struct ObjK {
     const float4* planes;
     float plane_eps;  // required margin below every plane
     int32_t bvh_root;  // FP32 in-medium traversals start here (host.h FlatBvh::obj_root); 0 = root
+    // Bounding sphere (centre, radius grown by the FP error of the camera-ray test): a
+    // camera ray that misses it misses every triangle of the object (wf_cam_filter).
+    R bsphere[4];
 };
 
 template <class R>
@@ -210,6 +213,11 @@ struct TraceArgs {
     WfPool<R> pool;             // wavefront pool (wavefront.cuh)
     int resume;                 // megakernel resumes the pool's live slots (q_live) instead of new ids
     int convex_end;             // FP32: skip traversals of flights that end inside a convex object
+    // Camera pre-pass (wavefront.cuh wf_cam_filter): the camera keys whose ray can hit an
+    // object's bounding sphere, compacted; path id i maps to key keys[i / 3] (render) or
+    // keys[i] (explicit keys). Null: ids are keys. keys_count: their number (device).
+    const uint32_t* keys;
+    const uint32_t* keys_count;
 };
 
 // TrainingSample (dataset.hpp:17-27): the SSWK record, 52 bytes, no padding.

@@ -404,6 +404,66 @@ SST_D void put_trace(const WfPool<R>& q, uint32_t j, const WfRec<R>& r) {
 
 enum : int { kEmitNone = 0, kEmitTrace = 1, kEmitSphere = 2, kEmitFree = 4 };
 
+// Paths of the launch the wavefront generates (after the camera pre-pass, if any).
+template <class R, bool EX>
+SST_D uint64_t wf_n_paths(const TraceArgs<R>& a) {
+    return a.keys ? static_cast<uint64_t>(*a.keys_count) * (EX ? 1u : 3u) : a.n_paths;
+}
+
+// ------------------------------------------------------------------ k_wf_cam_filter
+// Camera pre-pass: a camera ray that misses every object's (error-grown) bounding sphere
+// misses every triangle, so its paths escape at the camera exactly as a traversal miss
+// ends them (radiance = background, 0 segments, exit state = camera + direction); they
+// are finished here and never occupy a pool slot (C5: ~76% of the frame is background).
+// The other keys are compacted into `list` (block-aggregated, count in *count).
+template <class R>
+SST_D bool camera_ray_may_hit(const DevScene<R>& sc, V3<R> d) {
+    for (uint32_t o = 0; o < sc.n_objects; ++o) {
+        const ObjK<R>& ob = sc.objs[o];
+        const V3<R> oc = mk<R>(ob.bsphere[0], ob.bsphere[1], ob.bsphere[2]) - sc.cam_pos;
+        const R b = dot(oc, d), r = ob.bsphere[3];
+        if (b + r >= R(0) && dot(oc, oc) - b * b <= r * r) return true;
+    }
+    return false;
+}
+
+template <class R, bool EX>
+SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list, uint32_t* count) {
+    const DevScene<R>& sc = a.sc;
+    unsigned long long done = 0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n_keys; base += stride) {  // block-uniform
+        const uint32_t k = base + threadIdx.x;
+        bool keep = false;
+        if (k < n_keys) {
+            const uint32_t pixel = EX ? a.pixel[k] : k % a.n_pix;
+            const uint32_t sample = EX ? a.sample[k] : a.sample_begin + k / a.n_pix;
+            const V3<R> d = camera_dir(a, pixel, sample);
+            keep = camera_ray_may_hit(sc, d);
+            if (!keep) {
+                const uint32_t n_ch = EX ? 1u : 3u;
+                for (uint32_t j = 0; j < n_ch; ++j) {
+                    const uint64_t id = EX ? k : 3ull * k + j;
+                    const uint32_t c = EX ? a.channel[k] : j;
+                    a.radiance[id] = sc.bg[c];
+                    if (a.segments) a.segments[id] = 0u;
+                    if (a.exit_state) {
+                        R* e = a.exit_state + 6 * id;
+                        e[0] = sc.cam_pos.x, e[1] = sc.cam_pos.y, e[2] = sc.cam_pos.z;
+                        e[3] = d.x, e[4] = d.y, e[5] = d.z;
+                    }
+                }
+                done += n_ch;
+            }
+        }
+        block_push(keep, k, count, list);
+    }
+    unsigned long long v[kStCount] = {};
+    v[kStPaths] = done;
+    v[kStEscaped] = done;
+    flush_counts<kStCount>(a.stats, v);
+}
+
 // ------------------------------------------------------------------ k_wf_logic
 // The non-traversal part of path_advance for one slot, run until the slot needs a
 // traversal, a sphere step or a shadow ray (at most one per iteration), or its path
@@ -426,7 +486,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
     m = __ballot_sync(m, phase != kPhEmpty && !ended);
     // ended in k_wf_sphere (which runs concurrently with the generation kernel and so
     // does not touch the free queue): free it now if new paths remain
-    if (phase == kPhEmpty) return *a.work < a.n_paths ? kEmitFree : kEmitNone;
+    if (phase == kPhEmpty) return *a.work < wf_n_paths<R, EX>(a) ? kEmitFree : kEmitNone;
     if (ended) {  // absorbed after staging NEE records: add them, then the path ends
         load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false, true, &mb);
         finish_path(a, p, kEndAbsorbed, st);
@@ -671,7 +731,8 @@ template <class R, bool EX>
 SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     const uint32_t n_free = q.counts[kQFree];
     const uint64_t base = *a.work;
-    const uint64_t left = base < a.n_paths ? a.n_paths - base : 0;
+    const uint64_t n_paths = wf_n_paths<R, EX>(a);
+    const uint64_t left = base < n_paths ? n_paths - base : 0;
     const uint32_t n_new = static_cast<uint32_t>(left < n_free ? left : n_free);
     const uint32_t t0 = q.counts[kQTrace], l0 = q.counts[q.cnt_out];
     // The three channel paths of a (pixel, sample) share one camera ray (the camera
