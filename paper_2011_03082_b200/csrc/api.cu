@@ -518,15 +518,21 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
         ok[o].skip_unit = static_cast<R>(oh.skip_unit);
         for (int a = 0; a < 3; ++a) ok[o].skip_dims[a] = oh.skip_dims[a];
         ok[o].convex = oh.convex ? 1u : 0u;
-        {  // bounding sphere, radius grown past the FP error of camera_ray_may_hit
-            double dc2 = 0.0;
-            for (int k = 0; k < 3; ++k) {
-                const double dk = oh.bsphere[k] - d.cam_position[k];
-                dc2 += dk * dk;
+        {  // bounding sphere, radius grown past the FP error of ray_may_hit (|centre - origin|^2
+           // * 1e-7 for an origin at the camera or anywhere within the objects' span)
+            double span2 = 0.0;
+            for (const ObjectHost& q : ctx->objects) {
+                double dc2 = 0.0, dq2 = 0.0;
+                for (int k = 0; k < 3; ++k) {
+                    dc2 += (oh.bsphere[k] - d.cam_position[k]) * (oh.bsphere[k] - d.cam_position[k]);
+                    dq2 += (oh.bsphere[k] - q.bsphere[k]) * (oh.bsphere[k] - q.bsphere[k]);
+                }
+                const double dq = std::sqrt(dq2) + q.bsphere[3] + oh.bsphere[3];
+                span2 = std::fmax(span2, std::fmax(dc2, dq * dq));
             }
             const double r = oh.bsphere[3];
             for (int k = 0; k < 3; ++k) ok[o].bsphere[k] = static_cast<R>(oh.bsphere[k]);
-            ok[o].bsphere[3] = static_cast<R>(r * (1.0 + 1e-3) + 1e-5 * dc2 / std::fmax(r, 1e-3) + 1e-5);
+            ok[o].bsphere[3] = static_cast<R>(r * (1.0 + 1e-3) + 1e-5 * span2 / std::fmax(r, 1e-3) + 1e-5);
         }
         {
             const char* e = std::getenv("SST_NO_PLANES");

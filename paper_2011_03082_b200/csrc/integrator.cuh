@@ -119,6 +119,22 @@ struct LaneStats {
     DecodeCount dc;
 };
 
+// Can the ray x + t d (t > 0) hit an object other than `skip_obj` (a convex object the
+// ray is leaving)? False only if it misses every object's bounding sphere (radius grown
+// past the test's rounding error): then no triangle can be hit, and a traversal would
+// return a miss -- the test replaces it exactly.
+template <class R>
+SST_D bool ray_may_hit(const DevScene<R>& sc, V3<R> x, V3<R> d, int skip_obj) {
+    for (uint32_t o = 0; o < sc.n_objects; ++o) {
+        if (static_cast<int>(o) == skip_obj) continue;
+        const ObjK<R>& ob = sc.objs[o];
+        const V3<R> oc = mk<R>(ob.bsphere[0], ob.bsphere[1], ob.bsphere[2]) - x;
+        const R b = dot(oc, d), r = ob.bsphere[3];
+        if (b + r >= R(0) && dot(oc, oc) - b * b <= r * r) return true;
+    }
+    return false;
+}
+
 // Camera ray direction of (pixel, sample): jitter = the first two draws of the pixel
 // stream (DESIGN.md camera model).
 template <class R>
@@ -308,7 +324,7 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
                     trace = !flight_contained(*ob, p.x, p.w, t_free, Real<R>::fmax_(p.r_here, rs));
             }
         } else {
-            trace = true;
+            trace = ray_may_hit(sc, p.x, p.w, p.cull);  // else a miss (escape) without traversal
         }
         if (inside) t_max = t_free;
     }

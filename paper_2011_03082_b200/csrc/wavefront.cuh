@@ -418,13 +418,7 @@ SST_D uint64_t wf_n_paths(const TraceArgs<R>& a) {
 // The other keys are compacted into `list` (block-aggregated, count in *count).
 template <class R>
 SST_D bool camera_ray_may_hit(const DevScene<R>& sc, V3<R> d) {
-    for (uint32_t o = 0; o < sc.n_objects; ++o) {
-        const ObjK<R>& ob = sc.objs[o];
-        const V3<R> oc = mk<R>(ob.bsphere[0], ob.bsphere[1], ob.bsphere[2]) - sc.cam_pos;
-        const R b = dot(oc, d), r = ob.bsphere[3];
-        if (b + r >= R(0) && dot(oc, oc) - b * b <= r * r) return true;
-    }
-    return false;
+    return ray_may_hit(sc, sc.cam_pos, d, -1);
 }
 
 template <class R, bool EX>
@@ -585,6 +579,13 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                     }
                 }
             }
+            if (!inside && !ray_may_hit(sc, p.x, p.w, p.cull)) {
+                // an outside ray that misses every bounding sphere escapes (a traversal
+                // miss): the path ends in this visit, without a trace round trip
+                p.L += sc.bg[p.c];
+                end = kEndEscaped;
+                trace = false;
+            }
             if (trace) {
                 p.t_pend = t_free;
                 phase = kPhTrace;
@@ -596,7 +597,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                 rec.v = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8) |
                         (inside ? static_cast<uint32_t>(p.obj + 1) << 16 : 0u);
                 run = false;
-            } else {
+            } else if (end < 0) {
                 collide = true;  // the flight stays inside: collision without traversal
             }
         }
