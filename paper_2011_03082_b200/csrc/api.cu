@@ -205,10 +205,13 @@ struct sst_gpu_ctx {
     // tracer only, 2 (default) also for the delta-tracking path tracer (C5 PT+NEE 1.42x,
     // C3 sigma_t=160 1.44x the megakernel since the session-3 wavefront work; the long-path
     // tail still goes to the megakernel). Pool slots per launch, hand-off when live slots
-    // <= min(pool / 8, wf_tail), iterations per host check.
+    // <= min(pool / 8, wf_tail), iterations per host check. wf_tail: with the flight and
+    // camera culling the drain iterations stay cheaper than the megakernel down to ~16K
+    // live paths (C5, 10-slab runs: 512K 5.94, 128K 6.03, 32K 6.13, 16K 6.15, 2K 6.14
+    // Gseg/s; synchronous calls unchanged).
     int wavefront = 2;
     uint32_t wf_pool = 1u << 23;
-    uint32_t wf_tail = 1u << 19;
+    uint32_t wf_tail = 1u << 14;
     uint64_t wf_chunk = 1ull << 28;  // paths per render launch (radiance scratch)
     int wf_batch = 4;
     bool wf_concurrent = true;  // SST_WF_CONCURRENT=0: one stream per iteration
