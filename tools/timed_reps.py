@@ -18,7 +18,7 @@ be = bench._CudaBackend(0, r.stream)
 with be.stream_ctx():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 class A: pass
-a = A(); a.warmup = 3; a.steps = steps
+a = A(); a.warmup = int(os.environ.get("REPS_WARMUP", "3")); a.steps = steps
 out = []
 for k in range(reps):
     ms, stats, _ = bench.timed_slabs(r, be, None, 1, 0, a, 3 * 1920 * 1080, 32, 5000, flush)
