@@ -153,7 +153,7 @@ struct sst_gpu_ctx {
     std::vector<ObjectHost> objects;
     std::vector<uint64_t> object_fp;  // fingerprint of objects[o] (re-upload of the same object: no copy)
     sst_scene_desc desc{};
-    DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri;
+    DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri, grid_split;
     DevBuf grid_tris32;  // FP32 triangle records in light-grid list order (grid_tri gathered)
     uint32_t grid_res = 0;
     std::vector<DevBuf> sdf_dev, skip_dev, plane_off_dev, planes_dev;
@@ -180,7 +180,7 @@ struct sst_gpu_ctx {
         uint64_t geo_fp = 0, grid_fp = 0;
         bool have_bvh = false;
         FlatBvh bvh;
-        std::vector<uint32_t> grid_off, grid_tri;
+        std::vector<uint32_t> grid_off, grid_tri, grid_split;
         uint32_t grid_res = 0;
     } scene_cache;
 
@@ -606,6 +606,11 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     sc.grid_off = use_grid ? ctx->grid_off.as<uint32_t>() : nullptr;
     sc.grid_tri = use_grid ? ctx->grid_tri.as<uint32_t>() : nullptr;
     sc.grid_tris = use_grid && std::is_same<R, float>::value ? ctx->grid_tris32.p : nullptr;
+    {
+        const char* e = std::getenv("SST_NO_GRID_SPLIT");
+        sc.grid_split = use_grid && std::is_same<R, float>::value && !(e && e[0] == '1') ? ctx->grid_split.as<uint32_t>()
+                                                                                          : nullptr;
+    }
     sc.grid_res = ctx->grid_res;
 }
 
@@ -614,7 +619,8 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
 // direction, half angle = max vertex angle + padding); cells overlap-tested on the
 // GPU in FP64 (count pass, host prefix sum, fill pass).
 void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
-                      const std::vector<std::array<std::array<double, 3>, 3>>& tv, const FlatBvh& bvh) {
+                      const std::vector<std::array<std::array<double, 3>, 3>>& tv, const std::vector<uint32_t>& tobj,
+                      const FlatBvh& bvh) {
     const uint32_t n = bvh.n_tris;
     uint32_t res = n <= 4096 ? 256u : 512u;
     if (const char* e = std::getenv("SST_LIGHT_GRID_RES")) res = static_cast<uint32_t>(std::max(8, std::atoi(e)));
@@ -692,6 +698,56 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
     if (total) CK(cudaMemcpyAsync(ctx->scene_cache.grid_tri.data(), ctx->grid_tri.p, total * sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    {
+        // Each cell's list: faces whose normal points toward the light first (list order
+        // kept), then the faces pointing away, grouped by object (stable). grid_split =
+        // front count | (the one object owning every back face, else 0xff) << 24.
+        std::vector<int8_t> back(n, 0);
+        for (uint32_t k = 0; k < n; ++k) {
+            const auto& t = tv[bvh.order[k]];
+            double e1[3], e2[3], to_l[3];
+            for (int a = 0; a < 3; ++a) {
+                e1[a] = t[1][a] - t[0][a];
+                e2[a] = t[2][a] - t[0][a];
+                to_l[a] = d->light_position[a] - t[0][a];
+            }
+            const double nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                                  e1[0] * e2[1] - e1[1] * e2[0]};
+            const double f = nn[0] * to_l[0] + nn[1] * to_l[1] + nn[2] * to_l[2];
+            const double scale = std::sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]) *
+                                 std::sqrt(to_l[0] * to_l[0] + to_l[1] * to_l[1] + to_l[2] * to_l[2]);
+            back[k] = f < -1e-9 * scale ? 1 : 0;  // clearly facing away (the light is behind its plane)
+        }
+        auto& lst = ctx->scene_cache.grid_tri;
+        std::vector<uint32_t> split(ncell, 0xffu << 24), tmp, bk;
+        for (uint32_t c = 0; c < ncell; ++c) {
+            const uint32_t b = offsets[c], e = offsets[c + 1];
+            tmp.clear();
+            bk.clear();
+            for (uint32_t k = b; k < e; ++k)
+                if (!back[lst[k]]) tmp.push_back(lst[k]);
+            const uint32_t nf = static_cast<uint32_t>(tmp.size());
+            for (uint32_t k = b; k < e; ++k)
+                if (back[lst[k]]) bk.push_back(lst[k]);
+            std::stable_sort(bk.begin(), bk.end(), [&](uint32_t x, uint32_t y) {
+                return tobj[bvh.order[x]] < tobj[bvh.order[y]];
+            });
+            uint32_t owner = 0xffu;
+            if (!bk.empty() && tobj[bvh.order[bk.front()]] == tobj[bvh.order[bk.back()]] &&
+                tobj[bvh.order[bk.front()]] < 0xffu)
+                owner = tobj[bvh.order[bk.front()]];
+            tmp.insert(tmp.end(), bk.begin(), bk.end());
+            std::copy(tmp.begin(), tmp.end(), lst.begin() + b);
+            split[c] = (nf < (1u << 24) ? nf : 0xffffffu) | (nf < (1u << 24) ? owner << 24 : 0xffu << 24);
+        }
+        if (total) CK(cudaMemcpyAsync(ctx->grid_tri.p, lst.data(), total * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                      ctx->stream));
+        ctx->scene_cache.grid_split = split;
+        ctx->grid_split.reserve(split.size() * sizeof(uint32_t));
+        CK(cudaMemcpyAsync(ctx->grid_split.p, split.data(), split.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     ctx->scene_cache.grid_res = res;
     ctx->grid_res = res;
     ctx->scene_bytes_grid = offsets.size() * sizeof(uint32_t) + total * sizeof(uint32_t);
@@ -858,7 +914,7 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         ctx->grid_list_n = 0;
     } else if (!cached) {
         cache.grid_fp = 0;
-        build_light_grid(ctx, d, tv, cache.bvh);
+        build_light_grid(ctx, d, tv, tobj, cache.bvh);
         cache.grid_fp = lfp;
     } else {  // copy the cached light grid to the device (inputs travel every upload)
         const auto& sc = ctx->scene_cache;
@@ -866,6 +922,10 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         ctx->grid_tri.reserve(std::max<size_t>(sc.grid_tri.size(), 1) * sizeof(uint32_t));
         CK(cudaMemcpyAsync(ctx->grid_off.p, sc.grid_off.data(), sc.grid_off.size() * sizeof(uint32_t),
                            cudaMemcpyHostToDevice, ctx->stream));
+        ctx->grid_split.reserve(std::max<size_t>(sc.grid_split.size(), 1) * sizeof(uint32_t));
+        if (!sc.grid_split.empty())
+            CK(cudaMemcpyAsync(ctx->grid_split.p, sc.grid_split.data(), sc.grid_split.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
         if (!sc.grid_tri.empty())
             CK(cudaMemcpyAsync(ctx->grid_tri.p, sc.grid_tri.data(), sc.grid_tri.size() * sizeof(uint32_t),
                                cudaMemcpyHostToDevice, ctx->stream));
@@ -1641,7 +1701,7 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         auto it = g_const_owner.find(ctx->device);
         if (it != g_const_owner.end() && it->second.ctx == ctx) it->second.ctx = nullptr;
     }
-    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri, &ctx->grid_tris32,
+    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri, &ctx->grid_split, &ctx->grid_tris32,
                       &ctx->radiance, &ctx->segments, &ctx->work, &ctx->stats, &ctx->error, &ctx->film_sum,
                       &ctx->film_sq, &ctx->keys_pix, &ctx->keys_smp, &ctx->keys_ch, &ctx->step_in, &ctx->step_out})
         b->release();

@@ -426,11 +426,17 @@ SST_HD uint32_t cube_cell(R x, R y, R z, uint32_t res) {
 // grid: the same Moller-Trumbore tests as the BVH path on a conservative
 // candidate set (every triangle whose footprint seen from the light overlaps the
 // cell of this direction), so the hit set is identical -- without pointer chasing.
+// own: the convex object the ray starts in (-1: none / unknown).
 template <class R>
 SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_max, int c,
-                           uint64_t& n_tris) {
+                           uint64_t& n_tris, int own = -1) {
     const uint32_t cell = cube_cell<R>(-ray.d.x, -ray.d.y, -ray.d.z, sc.grid_res);
-    const uint32_t b = ldg_keep(sc.grid_off + cell), e = ldg_keep(sc.grid_off + cell + 1);
+    const uint32_t b = ldg_keep(sc.grid_off + cell);
+    uint32_t e = ldg_keep(sc.grid_off + cell + 1);
+    if (!Real<R>::kIsDouble && sc.grid_split && own >= 0) {
+        const uint32_t sp = ldg_keep(sc.grid_split + cell);
+        if (static_cast<int>(sp >> 24) == own) e = b + (sp & 0xffffffu);  // skip own back faces
+    }
     n_tris += e - b;
     R tau = R(0);
     const bool direct = !Real<R>::kIsDouble && sc.grid_tris;  // cell's triangles stored contiguously

@@ -54,7 +54,7 @@ constexpr double kFarLight = 1e30;
 // weight * Phi * hg(g, w.wl) * exp(-tau) / d^2.
 template <class R>
 SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<R> w, R weight,
-                 uint64_t& tri_tests) {
+                 uint64_t& tri_tests, int own = -1) {
     if (sc.directional) {
         // E * hg(g, w.wl) * exp(-tau), tau over the in-medium part of the ray out to the
         // last boundary exit (closed meshes: every hit beyond it is an entry/exit pair).
@@ -74,7 +74,7 @@ SST_D R nee_term(const DevScene<R>& sc, const MediumK<R>& m, int c, V3<R> p, V3<
     } else {
         ray = make_ray(p, wl);
     }
-    const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c, tri_tests)
+    const R tau = sc.grid_off ? optical_depth_grid(sc, ray, sc.t_min, d, c, tri_tests, own)
                               : optical_depth(sc, ray, sc.t_min, d, c);
     const R phase = hg_eval(m.g, dot(w, wl));
     if (Real<R>::kIsDouble) return weight * sc.power[c] * phase * Real<R>::exp_(R(-1) * tau) / d2;
@@ -478,7 +478,8 @@ SST_D int path_advance(const TraceArgs<R>& a, PathLocal<R>& p, LaneStats& st, bo
     // ---- 5. NEE
     if (nee) {
         const uint64_t t0 = st.tris;
-        p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt, st.tris);
+        p.L += nee_term(sc, ob->med[p.c], p.c, nee_p, nee_w, nee_wt, st.tris,
+                        ob->convex ? static_cast<int>(ob - sc.objs) : -1);
         st.shadow_tris += st.tris - t0;
         ++st.shadow;
     }

@@ -100,6 +100,12 @@ struct DevScene {
     const uint32_t* grid_off;
     const uint32_t* grid_tri;
     const void* grid_tris;  // FP32: TriF records in list order (grid_tri gathered); null in FP64
+    // Per cell: the list holds the faces that face the light first, then the ones facing
+    // away grouped by object; grid_split[c] = count of the former | (the single object
+    // owning all of the latter, 0xff if mixed) << 24. A shadow ray from inside a convex
+    // object never crosses that object's faces that face away from the light (FP32: those
+    // tests are skipped when they are the whole back part). Null: test the whole list.
+    const uint32_t* grid_split;
     uint32_t grid_res;
     uint32_t bvh_depth;  // FlatBvh::max_depth (traversal stack bound)
 };

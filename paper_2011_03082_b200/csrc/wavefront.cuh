@@ -963,7 +963,8 @@ SST_D void shadow_rec(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t idx, c
     const int oc = bits_int<R>(nw.w);
     const int obj = oc & 0xff, c = oc >> 8;
     q.nee_res[idx] =
-        nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w, tris);
+        nee_term(sc, sc.objs[obj].med[c], c, mk<R>(np.x, np.y, np.z), mk<R>(nw.x, nw.y, nw.z), np.w, tris,
+                 sc.objs[obj].convex ? obj : -1);
 }
 
 // Records [0, n) of one shadow range (queue position pos(i)) by work stealing in grabs
