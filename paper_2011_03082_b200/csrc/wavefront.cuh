@@ -556,8 +556,11 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                 uint32_t vox_end = 0;
                 const V3<R> x_end = p.x + p.w * t_c;
                 if (!p.r_valid) v = sdf_raw(ob, p.x, &in_grid);
-                const R rs = skip_radius(ob, p.x);
-                if (!Real<R>::kIsDouble && a.convex_end && m.sigma_t > R(0))
+                // with the safe radius known, a flight inside it needs neither culling gather
+                const bool gather = !p.r_valid || !(t_c < p.r_here);
+                R rs = R(0);
+                if (gather) rs = skip_radius(ob, p.x);
+                if (gather && !Real<R>::kIsDouble && a.convex_end && m.sigma_t > R(0))
                     v_end = sdf_raw(ob, x_end, &in_end, &vox_end);
                 if (!p.r_valid) {
                     p.r_here = v < R(0) ? -v : R(0);
