@@ -326,9 +326,14 @@ SST_D void block_pushn(const bool (&want)[N], uint32_t value, uint32_t* const (&
 template <int N>
 SST_D void block_pushn_counted(const bool (&want)[N], uint32_t value, uint32_t* const (&counter)[N],
                                uint32_t* const (&queue)[N], uint32_t (&pos)[N], uint32_t cnt, uint32_t first,
-                               uint32_t* ccounter, uint32_t* cqueue) {
-    __shared__ uint32_t wc[8][33];
-    __shared__ uint32_t qbase[8];
+                               uint32_t* ccounter, uint32_t* cqueue, uint32_t parity) {
+    // double-buffered by call parity: a call's writes never meet the previous call's
+    // reads, so no trailing barrier (every thread passed this call's two barriers before
+    // the buffer comes round again)
+    __shared__ uint32_t wcb[2][8][33];
+    __shared__ uint32_t qbaseb[2][8];
+    uint32_t(&wc)[8][33] = wcb[parity & 1u];
+    uint32_t(&qbase)[8] = qbaseb[parity & 1u];
     static_assert(N + 1 <= 8, "queues");
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const unsigned nw = (blockDim.x + 31u) >> 5;
@@ -364,7 +369,6 @@ SST_D void block_pushn_counted(const bool (&want)[N], uint32_t value, uint32_t* 
     }
     const uint32_t at = qbase[N] + wc[N][warp] + incl - cnt;
     for (uint32_t i = 0; i < cnt; ++i) cqueue[at + i] = first + i;
-    __syncthreads();
 }
 
 // Warp-granular work stealing over a queue of n items: returns the next item index
@@ -715,7 +719,8 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
         uint32_t* const qs[4] = {q.q_out, nullptr, q.q_sphere, q.q_free};
         uint32_t pos[4];
         // the staged NEE records of the visit go onto the shadow queue as record indices
-        block_pushn_counted<4>(want, s, ctr, qs, pos, nrec, s * kNeeChain, q.counts + kQShadow, q.q_shadow);
+        block_pushn_counted<4>(want, s, ctr, qs, pos, nrec, s * kNeeChain, q.counts + kQShadow, q.q_shadow,
+                               base / stride);
         if (emit == kEmitTrace) {  // the record at its queue position; its position in the meta
             put_trace(q, pos[1], rec);
             q.meta[s] = make_uint4(mo.x, mo.y, pos[1], mo.w);
