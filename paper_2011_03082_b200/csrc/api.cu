@@ -387,8 +387,9 @@ void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, 
 }
 
 // Face-plane lists of a convex object (integrator.cuh end_inside_planes): for every SDF
-// voxel whose stored value is -0 (centre inside, within half a diagonal of the surface)
-// the planes of the faces that can meet the voxel -- a superset (triangle box overlaps
+// voxel whose stored value is -0 (centre inside, within half a diagonal of the surface),
+// or +0 with a corner strictly inside the object, the planes of the faces that can meet
+// the voxel -- a superset (triangle box overlaps
 // the voxel and the plane passes within half a diagonal of the centre) is enough, since
 // every face plane of a convex object bounds it. tv[first, first + n): the object's
 // outward-wound triangles.
@@ -400,7 +401,11 @@ void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<d
     const uint32_t nx = oh.dims[0], ny = oh.dims[1], nz = oh.dims[2];
     const size_t nvox = static_cast<size_t>(nx) * ny * nz;
     const double h = oh.sdf_voxel, hd = 0.5 * std::sqrt(3.0) * h;
-    auto eligible = [&](size_t k) { return oh.sdf[k] == 0.0f && std::signbit(oh.sdf[k]); };
+    // eligible voxels: centre inside (stored -0), or centre outside (+0) with a corner
+    // strictly inside the object (decided below) -- either gives a point of V inside it
+    std::vector<uint8_t> elig(nvox, 0);
+    for (size_t k = 0; k < nvox; ++k) elig[k] = oh.sdf[k] == 0.0f ? (std::signbit(oh.sdf[k]) ? 1 : 2) : 0;
+    auto eligible = [&](size_t k) { return elig[k] != 0; };
     struct Pl {
         double n[3], d;
     };
@@ -455,6 +460,39 @@ void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<d
                     }
         }
     };
+    {  // +0 voxels: keep those with a corner strictly inside every face plane
+        for_pairs([&](size_t k, size_t) { ++cnt[k + 1]; });
+        for (size_t k = 0; k < nvox; ++k) cnt[k + 1] += cnt[k];
+        std::vector<uint32_t> cand(cnt[nvox]), fill(cnt.begin(), cnt.end() - 1);
+        for_pairs([&](size_t k, size_t t) { cand[fill[k]++] = static_cast<uint32_t>(t); });
+        const double m = 1e-9 * std::fmax(scale, 1.0);
+        auto inside = [&](const double* q, const uint32_t* b, const uint32_t* e) {
+            for (const uint32_t* t = b; t != e; ++t) {
+                const Pl& p = pl[*t];
+                if (!(p.n[0] * q[0] + p.n[1] * q[1] + p.n[2] * q[2] - p.d < -m)) return false;
+            }
+            return true;
+        };
+        std::vector<uint32_t> all;
+        for (size_t t = 0; t < n; ++t)
+            if (pl[t].n[0] != 0.0 || pl[t].n[1] != 0.0 || pl[t].n[2] != 0.0) all.push_back(static_cast<uint32_t>(t));
+        for (uint32_t z = 0; z < nz; ++z)
+            for (uint32_t y = 0; y < ny; ++y)
+                for (uint32_t x = 0; x < nx; ++x) {
+                    const size_t k = (static_cast<size_t>(z) * ny + y) * nx + x;
+                    if (elig[k] != 2) continue;
+                    bool ok = false;
+                    for (int c = 0; c < 8 && !ok; ++c) {
+                        const double q[3] = {oh.sdf_origin[0] + (x + (c & 1)) * h, oh.sdf_origin[1] + (y + ((c >> 1) & 1)) * h,
+                                             oh.sdf_origin[2] + (z + ((c >> 2) & 1)) * h};
+                        // nearby planes first (cheap rejection), then every face plane
+                        ok = inside(q, cand.data() + cnt[k], cand.data() + cnt[k + 1]) &&
+                             inside(q, all.data(), all.data() + all.size());
+                    }
+                    elig[k] = ok ? 1 : 0;
+                }
+        std::fill(cnt.begin(), cnt.end(), 0u);
+    }
     for_pairs([&](size_t k, size_t) { ++cnt[k + 1]; });
     for (size_t k = 0; k < nvox; ++k) cnt[k + 1] += cnt[k];
     oh.plane_off = cnt;

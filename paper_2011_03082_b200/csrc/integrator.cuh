@@ -199,11 +199,12 @@ SST_D void path_init(const TraceArgs<R>& a, uint64_t id, PathLocal<R>& p) {
 // Any object: the safe balls at the two end points (radius r_x at the start -- the
 // larger of the SDF and skip-grid bounds -- and the SDF safe radius at the end) cover the
 // segment when r_x + r_y > t, so it cannot cross the surface either.
-// Exact end-point containment for convex objects (FP32): the end point e lies in an
-// SDF voxel V whose centre c is inside the object and within half a diagonal of the
-// surface; F_V = every face that can meet V. If e is strictly inside every plane of F_V,
-// e is inside the object: otherwise the segment [c, e] (inside V) leaves the object
-// through a face of F_V and e would be beyond that face's plane. A convex object then
+// Exact end-point containment for convex objects (FP32): the end point e lies in a
+// boundary SDF voxel V that holds a point q inside the object (its centre, stored -0, or
+// a corner -- checked against every face plane at upload); F_V = every face that can
+// meet V. If e is strictly inside every plane of F_V, e is inside the object: otherwise
+// the segment [q, e] (inside V) leaves the object through a face of F_V and e would be
+// beyond that face's plane. A convex object then
 // contains the whole flight [x, e] (x inside), so it cannot cross the surface --
 // exactly the traversal's answer, without the traversal. The margin plane_eps (>> the
 // FP32 error of the plane test) keeps end points on the surface on the traced side.

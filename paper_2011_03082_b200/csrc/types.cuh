@@ -65,10 +65,10 @@ struct ObjK {
     R skip_inv_voxel, skip_unit;
     uint32_t skip_dims[3];
     uint32_t convex;  // closed convex mesh: a ray leaving it cannot hit it again
-    // FP32, convex objects: per SDF voxel whose centre is inside and within half a
-    // diagonal of the surface (stored value -0), the planes (unit outward normal, offset)
-    // of every face that can meet the voxel, CSR (plane_off[v] .. plane_off[v + 1]); a
-    // point of such a voxel strictly inside all of them is inside the object
+    // FP32, convex objects: per boundary SDF voxel (stored value +-0) that holds a point
+    // inside the object (the centre, or a corner), the planes (unit outward normal,
+    // offset) of every face that can meet the voxel, CSR (plane_off[v] .. plane_off[v +
+    // 1]); a point of such a voxel strictly inside all of them is inside the object
     // (integrator.cuh end_inside_planes). Null: no lists.
     const uint32_t* plane_off;
     const float4* planes;
