@@ -155,10 +155,13 @@ enum : int {
 // NEE mailbox (wavefront.cuh): a logic visit chains up to kNeeChain delta-tracking
 // events; their NEE records are staged per slot at s * kNeeChain + i, the shadow kernel
 // writes each contribution to nee_res at the same index, and the slot's next visit adds
-// them to its radiance in event order. 2 measured best on C5 (logic 93.7 -> 87 ms per
-// 32-spp slab; 3: 92, 4: 96, 8: 131 -- a warp runs as long as its longest chain).
+// them to its radiance in event order. With traversals frequent (round 2 start) 2
+// measured best on C5 (3: +6%, 4: +10% logic time -- a warp runs as long as its longest
+// chain, and traversals cut chains anyway); once the exact flight culling removed 85% of
+// the traversals, the mailbox became what ends most visits: 2 / 3 / 4 / 5 / 6 give
+// 6.86 / 7.06 / 7.20 / 7.07 / 6.93 Gseg/s.
 #ifndef SST_NEE_CHAIN
-#define SST_NEE_CHAIN 2
+#define SST_NEE_CHAIN 4
 #endif
 constexpr uint32_t kNeeChain = SST_NEE_CHAIN;
 static_assert(kNeeChain >= 1 && kNeeChain <= 15, "pending count lives in 4 meta bits");
