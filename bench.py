@@ -409,6 +409,10 @@ def timed_slabs(r, be, dist, world, rank, args, n_values, S, spp_total, flush=No
         one(i)
     r.read_stats()
     with be.stream_ctx():
+        # one untimed reduce first: its output buffers come from the caching allocator
+        # afterwards (a first-time cudaMalloc inside the timed region cost up to ~10% of a
+        # 10-slab measurement)
+        ordered_film_sum({rank: (fsum, fsq)}, list(range(world)))
         fsum.zero_()
         fsq.zero_()
     if dist:
@@ -435,6 +439,8 @@ def timed_frame(r, be, dist, world, rank, n_values, spp):
     from paper_2011_03082_b200.dist import group_owners, group_slab, groups_of_rank, ordered_film_sum
     mine = list(groups_of_rank(rank, world))
     films = {g: (be.zeros(n_values), be.zeros(n_values)) for g in mine}
+    with be.stream_ctx():  # untimed reduce first: its buffers come from the allocator cache
+        ordered_film_sum(films, group_owners(world))
     if dist:
         dist.barrier()
     be.sync()
