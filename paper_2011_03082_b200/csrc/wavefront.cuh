@@ -510,6 +510,11 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
         if (!__any_sync(m, run)) break;
         bool collide = false;
         R t_free = Real<R>::kInf;
+        // FP32: a flight that collides without a traversal hands its end point and the SDF
+        // value there (gathered for the culling tests) to the collision stage
+        bool have_end = false, in_end = false;
+        R v_end = R(1);
+        V3<R> x_end = p.x;
         if (run && phase == kPhTrace) {
             // ---- resolve (path_advance phase 2) with the traversal result
             const bool hit = (hi.y >> 31) != 0u;
@@ -555,17 +560,19 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                     if (Real<R>::kIsDouble) t_c = -Real<R>::log1p_(-u) / m.sigma_t;
                     else t_c = -Real<R>::div_(Real<R>::log_(R(1) - u), m.sigma_t);
                 }
-                bool in_grid = true, in_end = false;
-                R v = R(0), v_end = R(1);
+                bool in_grid = true;
+                R v = R(0);
                 uint32_t vox_end = 0;
-                const V3<R> x_end = p.x + p.w * t_c;
+                x_end = p.x + p.w * t_c;
                 if (!p.r_valid) v = sdf_raw(ob, p.x, &in_grid);
-                // with the safe radius known, a flight inside it needs neither culling gather
+                // with the safe radius known, a flight inside it needs no skip-grid gather
                 const bool gather = !p.r_valid || !(t_c < p.r_here);
                 R rs = R(0);
                 if (gather) rs = skip_radius(ob, p.x);
-                if (gather && !Real<R>::kIsDouble && a.convex_end && m.sigma_t > R(0))
+                if (!Real<R>::kIsDouble && m.sigma_t > R(0)) {
                     v_end = sdf_raw(ob, x_end, &in_end, &vox_end);
+                    have_end = true;
+                }
                 if (!p.r_valid) {
                     p.r_here = v < R(0) ? -v : R(0);
                     p.r_valid = true;
@@ -613,7 +620,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
             // ---- collision (path_advance phases 2-3)
             const ObjK<R>& ob = sc.objs[p.obj];
             p.skip = -1;
-            p.x = p.x + p.w * t_free;
+            p.x = have_end ? x_end : p.x + p.w * t_free;
             p.r_valid = false;
             if (p.seg >= (ST ? sc.cap_st : sc.cap_pt)) {
                 p.L = R(0);  // dropped
@@ -623,8 +630,8 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                 bool event = true;
                 phase = kPhFlight;
                 if (ST) {
-                    bool in_grid;
-                    const R v = sdf_raw(ob, p.x, &in_grid);
+                    bool in_grid = in_end;
+                    const R v = have_end ? v_end : sdf_raw(ob, p.x, &in_grid);
                     p.r_here = v < R(0) ? -v : R(0);
                     p.r_valid = true;
                     if (leaked(ob, v, in_grid)) {  // not in the medium: next pass flies from here
