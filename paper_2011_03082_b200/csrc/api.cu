@@ -386,7 +386,7 @@ void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, 
     oh.sdf_voxel = a.voxel;
 }
 
-// Face-plane lists of a convex object (integrator.cuh end_inside_planes): for every SDF
+// Face-plane lists of an object (integrator.cuh end_inside_planes): for every SDF
 // voxel whose stored value is -0 (centre inside, within half a diagonal of the surface),
 // or +0 with a corner strictly inside the object, the planes of the faces that can meet
 // the voxel -- a superset (triangle box overlaps
@@ -397,14 +397,16 @@ void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<d
                        size_t n) {
     oh.plane_off.clear();
     oh.planes.clear();
-    if (!oh.convex) return;
     const uint32_t nx = oh.dims[0], ny = oh.dims[1], nz = oh.dims[2];
     const size_t nvox = static_cast<size_t>(nx) * ny * nz;
     const double h = oh.sdf_voxel, hd = 0.5 * std::sqrt(3.0) * h;
     // eligible voxels: centre inside (stored -0), or centre outside (+0) with a corner
     // strictly inside the object (decided below) -- either gives a point of V inside it
     std::vector<uint8_t> elig(nvox, 0);
-    for (size_t k = 0; k < nvox; ++k) elig[k] = oh.sdf[k] == 0.0f ? (std::signbit(oh.sdf[k]) ? 1 : 2) : 0;
+    // (non-convex objects: centre-inside voxels only -- "inside every face plane" is the
+    // inside test of a convex object alone)
+    for (size_t k = 0; k < nvox; ++k)
+        elig[k] = oh.sdf[k] == 0.0f ? (std::signbit(oh.sdf[k]) ? 1 : (oh.convex ? 2 : 0)) : 0;
     auto eligible = [&](size_t k) { return elig[k] != 0; };
     struct Pl {
         double n[3], d;

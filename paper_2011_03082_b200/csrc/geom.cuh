@@ -44,6 +44,19 @@ SST_D R sdf_raw(const ObjK<R>& o, V3<R> p, bool* inside_grid, uint32_t* vox = nu
     return static_cast<R>(ldg_keep(o.sdf + k));
 }
 
+// The SDF voxel of p (sdf_raw's index arithmetic, no load); false off the grid.
+template <class R>
+SST_D bool sdf_voxel(const ObjK<R>& o, V3<R> p, uint32_t* vox) {
+    const R rx = (p.x - o.sdf_origin[0]) * o.sdf_inv_voxel;
+    const R ry = (p.y - o.sdf_origin[1]) * o.sdf_inv_voxel;
+    const R rz = (p.z - o.sdf_origin[2]) * o.sdf_inv_voxel;
+    if (rx < R(0) || ry < R(0) || rz < R(0)) return false;
+    const uint32_t x = static_cast<uint32_t>(rx), y = static_cast<uint32_t>(ry), z = static_cast<uint32_t>(rz);
+    if (x >= o.dims[0] || y >= o.dims[1] || z >= o.dims[2]) return false;
+    *vox = (z * o.dims[1] + y) * o.dims[0] + x;
+    return true;
+}
+
 // query_safe_radius: -v inside (v < 0), else 0; 0 outside the grid.
 template <class R>
 SST_D R sdf_radius(const ObjK<R>& o, V3<R> p) {

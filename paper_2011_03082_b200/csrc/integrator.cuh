@@ -224,6 +224,30 @@ SST_D bool end_inside_planes(const ObjK<R>& ob, uint32_t vox, V3<R> e) {
     }
 }
 
+// Any closed object: a flight whose both ends lie in the same listed voxel V and strictly
+// inside all of V's planes stays in the medium. Every point of the segment is then
+// strictly inside those planes (an intersection of half-spaces is convex) and in V, so
+// -- by the argument above, which needs no convexity: a point of V outside the object
+// lies beyond the plane of the face through which [q, point] leaves last -- every point
+// is interior: the segment meets no face.
+template <class R>
+SST_D bool seg_inside_planes(const ObjK<R>& ob, uint32_t vox, V3<R> x, V3<R> e) {
+    if constexpr (Real<R>::kIsDouble) {
+        return false;
+    } else {
+        if (!ob.plane_off) return false;
+        const uint32_t b = ldg_keep(ob.plane_off + vox), en = ldg_keep(ob.plane_off + vox + 1);
+        if (b == en) return false;
+        for (uint32_t k = b; k < en; ++k) {
+            const float4 pl = ldg_keep(ob.planes + k);
+            if (!(fmaf(pl.x, e.x, fmaf(pl.y, e.y, fmaf(pl.z, e.z, -pl.w))) < -ob.plane_eps) ||
+                !(fmaf(pl.x, x.x, fmaf(pl.y, x.y, fmaf(pl.z, x.z, -pl.w))) < -ob.plane_eps))
+                return false;
+        }
+        return true;
+    }
+}
+
 // Culling rule that decided a contained flight (verification counters).
 enum : int { kContainNone = 0, kContainSdf = 1, kContainPlanes = 2 };
 template <class R>
@@ -235,7 +259,10 @@ SST_D int flight_contained_rule(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x)
     const R v = sdf_raw(ob, e, &in_grid, &vox);
     if (!in_grid) return kContainNone;
     if (v < R(0) && (ob.convex || t < r_x - v)) return kContainSdf;
-    return ob.convex && end_inside_planes(ob, vox, e) ? kContainPlanes : kContainNone;
+    if (ob.convex) return end_inside_planes(ob, vox, e) ? kContainPlanes : kContainNone;
+    uint32_t vox_x;
+    return sdf_voxel(ob, x, &vox_x) && vox_x == vox && seg_inside_planes(ob, vox, x, e) ? kContainPlanes
+                                                                                        : kContainNone;
 }
 template <class R>
 SST_D bool flight_contained(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
@@ -244,11 +271,13 @@ SST_D bool flight_contained(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
 
 // flight_contained with the end point's SDF value already loaded (wavefront logic pass).
 template <class R>
-SST_D bool end_contained(const ObjK<R>& ob, R v_end, bool in_grid, uint32_t vox, V3<R> e, R t, R r_x) {
+SST_D bool end_contained(const ObjK<R>& ob, R v_end, bool in_grid, uint32_t vox, V3<R> x, V3<R> e, R t, R r_x) {
     if (Real<R>::kIsDouble) return false;
     if (!in_grid) return false;
     if (v_end < R(0) && (ob.convex || t < r_x - v_end)) return true;
-    return ob.convex && end_inside_planes(ob, vox, e);
+    if (ob.convex) return end_inside_planes(ob, vox, e);
+    uint32_t vox_x;
+    return sdf_voxel(ob, x, &vox_x) && vox_x == vox && seg_inside_planes(ob, vox, x, e);
 }
 
 // FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)

@@ -588,7 +588,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                     if (trace) {
                         trace = !(t_free < rs);
                         if (trace && a.convex_end)
-                            trace = !end_contained(ob, v_end, in_end, vox_end, x_end, t_free,
+                            trace = !end_contained(ob, v_end, in_end, vox_end, p.x, x_end, t_free,
                                                    Real<R>::fmax_(p.r_here, rs));
                     }
                 }

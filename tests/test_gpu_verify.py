@@ -46,6 +46,7 @@ def test_flight_culling_is_conservative(renderer, scene_name, precision):
             assert rep["culled_endpoint_planes"] > 0, rep  # face-plane test of the end voxel
         else:
             assert rep["culled_endpoint_twoball"] > 0, rep
+            assert rep["culled_endpoint_planes"] > 0, rep  # same-voxel face-plane test
 
 
 @pytest.mark.parametrize("sigma_t,g,phi", [(10.0, 0.8, 0.9), (20.0, 0.3, 0.95), (5.0, -0.5, 1.0)])
