@@ -194,7 +194,7 @@ struct sst_gpu_ctx {
         cudaEvent_t film_done = nullptr;
         // wavefront pool (wavefront.cuh) + pinned queue counters read by the host loop
         DevBuf wf;
-        DevBuf keys;  // camera pre-pass: [count u32, pad] + compacted key list (wf_cam_filter)
+        DevBuf keys;  // camera pre-pass: [16 u32 header] + compacted key list (wf_cam_filter)
         uint32_t* wf_host = nullptr;  // [2][kQCount]
         cudaEvent_t wf_ev[2] = {nullptr, nullptr};
         // concurrent half of a wavefront iteration (sphere + shadow) and its fork/join
@@ -561,6 +561,14 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
         ok[o].skip_unit = static_cast<R>(oh.skip_unit);
         for (int a = 0; a < 3; ++a) ok[o].skip_dims[a] = oh.skip_dims[a];
         ok[o].convex = oh.convex ? 1u : 0u;
+        {  // density rank (camera pre-pass ordering)
+            auto dens = [](const ObjectHost& q) {
+                return std::fmax(q.media[0].sigma_t, std::fmax(q.media[1].sigma_t, q.media[2].sigma_t));
+            };
+            uint32_t rank = 0;
+            for (const ObjectHost& q : ctx->objects) rank += dens(q) > dens(oh);
+            ok[o].cost_class = std::min<uint32_t>(rank, 3u);
+        }
         {  // bounding sphere, radius grown past the FP error of ray_may_hit (|centre - origin|^2
            // * 1e-7 for an origin at the camera or anywhere within the objects' span)
             double span2 = 0.0;
@@ -1280,15 +1288,15 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
     if (ctx->cam_filter && a.sc.n_objects <= 64 && (explicit_keys || a.n_paths % 3 == 0)) {
         // camera pre-pass: paths whose camera ray misses every bounding sphere end here
         const uint64_t n_keys = explicit_keys ? a.n_paths : a.n_paths / 3;
-        sl.keys.reserve(16 + 4 * n_keys);
-        uint32_t* cnt = sl.keys.as<uint32_t>();
-        CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), stream));
+        sl.keys.reserve(64 + 4 * n_keys);
+        uint32_t* cnt = sl.keys.as<uint32_t>();  // header: total, class counts, class cursors
+        CK(cudaMemsetAsync(cnt, 0, 64, stream));
         kt_begin(ctx, stream);  // timed as generation work
         if constexpr (std::is_same<R, float>::value)
-            CK(f32::launch_wf_cam_filter(a, explicit_keys, static_cast<uint32_t>(n_keys), cnt + 4, cnt, stream));
-        else CK(f64::launch_wf_cam_filter(a, explicit_keys, static_cast<uint32_t>(n_keys), cnt + 4, cnt, stream));
+            CK(f32::launch_wf_cam_filter(a, explicit_keys, static_cast<uint32_t>(n_keys), cnt + 16, cnt, stream));
+        else CK(f64::launch_wf_cam_filter(a, explicit_keys, static_cast<uint32_t>(n_keys), cnt + 16, cnt, stream));
         kt_end(ctx, stream, SST_KT_WF_GEN);
-        a.keys = cnt + 4;
+        a.keys = cnt + 16;
         a.keys_count = cnt;
     }
     j.a = a;
@@ -1495,7 +1503,7 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         size_t off[kPoolArrays];
         const uint64_t cap = std::max<uint64_t>(32, std::min<uint64_t>(per_sample * chunk, ctx->wf_pool));
         const size_t pool = pool_layout<R>(static_cast<uint32_t>(cap), off);
-        const size_t keys = 16 + 4 * (per_sample * chunk / 3 + 1);  // camera pre-pass list
+        const size_t keys = 64 + 4 * (per_sample * chunk / 3 + 1);  // camera pre-pass list
         bool grow = false;
         for (int k = 0; k < n_slots; ++k) {
             const auto& s2 = ctx->slots[k];

@@ -77,6 +77,9 @@ struct ObjK {
     // Bounding sphere (centre, radius grown by the FP error of the camera-ray test): a
     // camera ray that misses it misses every triangle of the object (wf_cam_filter).
     R bsphere[4];
+    // Rank of the object's medium density among the scene's objects (0 = densest, capped
+    // at kCostClasses - 1): the camera pre-pass generates paths into dense media first.
+    uint32_t cost_class;
 };
 
 template <class R>

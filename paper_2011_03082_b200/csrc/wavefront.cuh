@@ -425,20 +425,48 @@ SST_D bool camera_ray_may_hit(const DevScene<R>& sc, V3<R> d) {
     return ray_may_hit(sc, sc.cam_pos, d, -1);
 }
 
+// Keys are grouped by the cost class of the costliest object their ray may enter
+// (ObjK::cost_class, 0 = densest medium first): expensive paths are generated first, so
+// the pool's drain -- exposed at the end of a launch -- holds the cheap ones. Two passes:
+// pass 0 finishes the misses and counts the classes (hdr[1 + c]); pass 1 scatters each
+// kept key behind the classes before it (cursors hdr[1 + kCostClasses + c]). hdr[0] =
+// the total.
+constexpr uint32_t kCostClasses = 4;
+template <class R>
+SST_D uint32_t camera_ray_class(const DevScene<R>& sc, V3<R> d) {
+    uint32_t cls = kCostClasses;  // none: the ray misses every bounding sphere
+    for (uint32_t o = 0; o < sc.n_objects; ++o) {
+        const ObjK<R>& ob = sc.objs[o];
+        const V3<R> oc = mk<R>(ob.bsphere[0], ob.bsphere[1], ob.bsphere[2]) - sc.cam_pos;
+        const R b = dot(oc, d), r = ob.bsphere[3];
+        if (b + r >= R(0) && dot(oc, oc) - b * b <= r * r) cls = min(cls, ob.cost_class);
+    }
+    return cls;
+}
+
 template <class R, bool EX>
-SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list, uint32_t* count) {
+SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list, uint32_t* hdr, int pass) {
     const DevScene<R>& sc = a.sc;
     unsigned long long done = 0;
+    __shared__ uint32_t base_cls[kCostClasses];
+    if (pass == 1 && threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t c = 0; c < kCostClasses; ++c) {
+            base_cls[c] = acc;
+            acc += hdr[1 + c];
+        }
+    }
+    __syncthreads();
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t base = blockIdx.x * blockDim.x; base < n_keys; base += stride) {  // block-uniform
         const uint32_t k = base + threadIdx.x;
-        bool keep = false;
+        uint32_t cls = kCostClasses;
         if (k < n_keys) {
             const uint32_t pixel = EX ? a.pixel[k] : k % a.n_pix;
             const uint32_t sample = EX ? a.sample[k] : a.sample_begin + k / a.n_pix;
             const V3<R> d = camera_dir(a, pixel, sample);
-            keep = camera_ray_may_hit(sc, d);
-            if (!keep) {
+            cls = camera_ray_class(sc, d);
+            if (cls == kCostClasses && pass == 0) {
                 const uint32_t n_ch = EX ? 1u : 3u;
                 for (uint32_t j = 0; j < n_ch; ++j) {
                     const uint64_t id = EX ? k : 3ull * k + j;
@@ -454,12 +482,29 @@ SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list,
                 done += n_ch;
             }
         }
-        block_push(keep, k, count, list);
+        const bool want[kCostClasses] = {cls == 0u, cls == 1u, cls == 2u, cls == 3u};
+        uint32_t pos[kCostClasses];
+        if (pass == 0) {
+            uint32_t* const ctr[kCostClasses] = {hdr + 1, hdr + 2, hdr + 3, hdr + 4};
+            uint32_t* const qs[kCostClasses] = {nullptr, nullptr, nullptr, nullptr};
+            block_pushn<kCostClasses>(want, k, ctr, qs, pos);
+        } else {
+            uint32_t* const ctr[kCostClasses] = {hdr + 5, hdr + 6, hdr + 7, hdr + 8};
+            uint32_t* const qs[kCostClasses] = {nullptr, nullptr, nullptr, nullptr};
+            block_pushn<kCostClasses>(want, k, ctr, qs, pos);
+            if (cls < kCostClasses) list[base_cls[cls] + pos[cls]] = k;
+        }
     }
-    unsigned long long v[kStCount] = {};
-    v[kStPaths] = done;
-    v[kStEscaped] = done;
-    flush_counts<kStCount>(a.stats, v);
+    if (pass == 0) {
+        unsigned long long v[kStCount] = {};
+        v[kStPaths] = done;
+        v[kStEscaped] = done;
+        flush_counts<kStCount>(a.stats, v);
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (uint32_t c = 0; c < kCostClasses; ++c) tot += hdr[1 + c];
+        hdr[0] = tot;
+    }
 }
 
 // ------------------------------------------------------------------ k_wf_logic
