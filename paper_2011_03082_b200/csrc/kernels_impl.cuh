@@ -158,6 +158,28 @@ cudaError_t upload_constants(const double* weights1332, const double* norms6, cu
     if (e != cudaSuccess) return e;
     e = cudaMemcpyToSymbolAsync(c_norm, n, sizeof n, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
+#ifdef SST_DECODER_PAIRS
+    float2 wp[kTotalWeights / 2];
+    auto pack = [&](auto shape) {
+        using S = decltype(shape);
+        auto layer = [&](int rows, int cols, int off_w, int off_b, int p_w, int p_b) {
+            for (int rp = 0; rp < rows / 2; ++rp) {
+                for (int c = 0; c < cols; ++c)
+                    wp[p_w + rp * cols + c] = make_float2(static_cast<float>(w[off_w + 2 * rp * cols + c]),
+                                                          static_cast<float>(w[off_w + (2 * rp + 1) * cols + c]));
+                wp[p_b + rp] = make_float2(static_cast<float>(w[off_b + 2 * rp]), static_cast<float>(w[off_b + 2 * rp + 1]));
+            }
+        };
+        layer(S::W, S::IN, S::OFF_W0, S::OFF_B0, S::P_W0, S::P_B0);
+        layer(S::W, S::W, S::OFF_W1, S::OFF_B1, S::P_W1, S::P_B1);
+        layer(S::OUT, S::W, S::OFF_W2, S::OFF_B2, S::P_W2, S::P_B2);
+    };
+    pack(LengthShape{});
+    pack(PathShape{});
+    pack(EventShape{});
+    e = cudaMemcpyToSymbolAsync(c_wpair, wp, sizeof wp, 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+#endif
     return cudaStreamSynchronize(s);  // the host staging arrays live on this stack
 }
 
