@@ -40,7 +40,17 @@ def main():
                 if v > 0.05:
                     stalls[h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = v
         d["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda x: -x[1]))
-        out[name[:80]] = d
+        # several launches of one kernel: keep the longest (the bulk, not a drain tail)
+        key = name[:80]
+        def dur(x):
+            try:
+                v, u = (x.get("gpu__time_duration.sum", "0 ns").split() + ["ns"])[:2]
+                return float(v) * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
+                                   "s": 1.0, "second": 1.0, "nsecond": 1e-9}.get(u, 1e-9)
+            except ValueError:
+                return 0.0
+        if key not in out or dur(d) > dur(out[key]):
+            out[key] = d
     print(json.dumps(out, indent=1))
     if "--json" in sys.argv:
         json.dump(out, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)

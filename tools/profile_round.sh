@@ -19,6 +19,6 @@ $W > gpurun_out/wfprof_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file gpurun_out/launches_wf16.csv $W > gpurun_out/ncu_b.log 2>&1
 echo "ncu traffic rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_wf_(logic|trace|sphere|shadow)" -s 300 -c 4 \
+ncu --set full --clock-control none --import-source on -k regex:"k_wf_(logic|trace|sphere|shadow)" -s 40 -c 5 \
     -o gpurun_out/prof_wf $W > gpurun_out/ncu_c.log 2>&1
 echo "ncu full rc=$?"
