@@ -386,20 +386,58 @@ void build_sdf_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh, 
     oh.sdf_voxel = a.voxel;
 }
 
+// Triangle / axis-aligned box overlap (separating axes: the box normals, the triangle
+// normal, the 9 edge cross products; Akenine-Moller), box centre c and half size e.
+bool tri_box_overlap(const std::array<std::array<double, 3>, 3>& t, const double (&c)[3], double e) {
+    double v[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int a = 0; a < 3; ++a) v[i][a] = t[i][a] - c[a];
+    auto sep = [&](const double (&ax)[3]) {
+        const double r = e * (std::fabs(ax[0]) + std::fabs(ax[1]) + std::fabs(ax[2]));
+        double lo = 1e300, hi = -1e300;
+        for (int i = 0; i < 3; ++i) {
+            const double p = v[i][0] * ax[0] + v[i][1] * ax[1] + v[i][2] * ax[2];
+            lo = std::fmin(lo, p);
+            hi = std::fmax(hi, p);
+        }
+        return lo > r || hi < -r;
+    };
+    for (int a = 0; a < 3; ++a) {
+        double ax[3] = {0, 0, 0};
+        ax[a] = 1.0;
+        if (sep(ax)) return false;
+    }
+    double ed[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int a = 0; a < 3; ++a) ed[i][a] = v[(i + 1) % 3][a] - v[i][a];
+    const double nn[3] = {ed[0][1] * ed[1][2] - ed[0][2] * ed[1][1], ed[0][2] * ed[1][0] - ed[0][0] * ed[1][2],
+                          ed[0][0] * ed[1][1] - ed[0][1] * ed[1][0]};
+    if (sep(nn)) return false;
+    for (int i = 0; i < 3; ++i)
+        for (int a = 0; a < 3; ++a) {
+            double u[3] = {0, 0, 0};
+            u[a] = 1.0;
+            const double ax[3] = {u[1] * ed[i][2] - u[2] * ed[i][1], u[2] * ed[i][0] - u[0] * ed[i][2],
+                                  u[0] * ed[i][1] - u[1] * ed[i][0]};
+            if (sep(ax)) return false;
+        }
+    return true;
+}
+
 // Face-plane lists of an object (integrator.cuh end_inside_planes): for every SDF
 // voxel whose stored value is -0 (centre inside, within half a diagonal of the surface),
-// or +0 with a corner strictly inside the object, the planes of the faces that can meet
-// the voxel -- a superset (triangle box overlaps
-// the voxel and the plane passes within half a diagonal of the centre) is enough, since
-// every face plane of a convex object bounds it. tv[first, first + n): the object's
-// outward-wound triangles.
+// or +0 with a corner strictly inside the (convex) object, the planes of the faces that
+// meet the voxel (separating-axis test on the voxel grown by 1e-6: a superset of the
+// faces crossing it is all the containment argument needs); a listed voxel no face
+// meets is wholly inside and gets one always-satisfied plane. tv[first, first + n): the
+// object's outward-wound triangles.
 void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<double, 3>, 3>>& tv, size_t first,
                        size_t n) {
     oh.plane_off.clear();
     oh.planes.clear();
     const uint32_t nx = oh.dims[0], ny = oh.dims[1], nz = oh.dims[2];
     const size_t nvox = static_cast<size_t>(nx) * ny * nz;
-    const double h = oh.sdf_voxel, hd = 0.5 * std::sqrt(3.0) * h;
+    const double h = oh.sdf_voxel;
     // eligible voxels: centre inside (stored -0), or centre outside (+0) with a corner
     // strictly inside the object (decided below) -- either gives a point of V inside it
     std::vector<uint8_t> elig(nvox, 0);
@@ -449,16 +487,8 @@ void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<d
                         if (!eligible(k)) continue;
                         const double cc[3] = {oh.sdf_origin[0] + (x + 0.5) * h, oh.sdf_origin[1] + (y + 0.5) * h,
                                               oh.sdf_origin[2] + (z + 0.5) * h};
-                        // the triangle's box must overlap the voxel (slightly grown) ...
-                        bool overlap = true;
-                        for (int a = 0; a < 3; ++a) {
-                            const double mn = std::fmin(c[0][a], std::fmin(c[1][a], c[2][a]));
-                            const double mx = std::fmax(c[0][a], std::fmax(c[1][a], c[2][a]));
-                            overlap = overlap && mn <= cc[a] + 0.5 * h * (1.0 + 1e-6) && mx >= cc[a] - 0.5 * h * (1.0 + 1e-6);
-                        }
-                        // ... and its plane pass within half a diagonal of the centre
-                        const double dist = p.n[0] * cc[0] + p.n[1] * cc[1] + p.n[2] * cc[2] - p.d;
-                        if (overlap && std::fabs(dist) <= hd * (1.0 + 1e-6)) fn(k, t);
+                        // the triangle meets the voxel (slightly grown): separating-axis test
+                        if (tri_box_overlap(c, cc, 0.5 * h * (1.0 + 1e-6) + 1e-12 * scale)) fn(k, t);
                     }
         }
     };
@@ -496,6 +526,11 @@ void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<d
         std::fill(cnt.begin(), cnt.end(), 0u);
     }
     for_pairs([&](size_t k, size_t) { ++cnt[k + 1]; });
+    // an eligible voxel that no face meets lies wholly inside (it holds an interior point
+    // and the surface does not enter it): one always-satisfied plane (0, 0, 0, 1)
+    std::vector<uint8_t> inner(nvox, 0);
+    for (size_t k = 0; k < nvox; ++k)
+        if (elig[k] && cnt[k + 1] == 0) inner[k] = 1, cnt[k + 1] = 1;
     for (size_t k = 0; k < nvox; ++k) cnt[k + 1] += cnt[k];
     oh.plane_off = cnt;
     oh.planes.resize(4 * static_cast<size_t>(cnt[nvox]));
@@ -505,6 +540,12 @@ void build_plane_lists(ObjectHost& oh, const std::vector<std::array<std::array<d
         for (int a = 0; a < 3; ++a) q[a] = static_cast<float>(pl[t].n[a]);
         q[3] = static_cast<float>(pl[t].d);
     });
+    for (size_t k = 0; k < nvox; ++k)
+        if (inner[k]) {
+            float* q = oh.planes.data() + 4 * static_cast<size_t>(fill[k]++);
+            q[0] = q[1] = q[2] = 0.0f;
+            q[3] = 1.0f;
+        }
     // margin: far above the FP32 error of n.e - d at this coordinate scale (~1e-7 x scale)
     oh.plane_eps = static_cast<float>(1e-4 * h + 4e-6 * std::fmax(scale, 1.0));
 }
