@@ -269,15 +269,40 @@ SST_D bool flight_contained(const ObjK<R>& ob, V3<R> x, V3<R> w, R t, R r_x) {
     return flight_contained_rule(ob, x, w, t, r_x) != kContainNone;
 }
 
-// flight_contained with the end point's SDF value already loaded (wavefront logic pass).
+// A convex object's end point e strictly beyond one of its voxel's face planes (margin
+// plane_eps) is outside the object: a convex object lies inside every face plane.
 template <class R>
-SST_D bool end_contained(const ObjK<R>& ob, R v_end, bool in_grid, uint32_t vox, V3<R> x, V3<R> e, R t, R r_x) {
-    if (Real<R>::kIsDouble) return false;
-    if (!in_grid) return false;
-    if (v_end < R(0) && (ob.convex || t < r_x - v_end)) return true;
-    if (ob.convex) return end_inside_planes(ob, vox, e);
+SST_D bool end_beyond_a_plane(const ObjK<R>& ob, uint32_t vox, V3<R> e) {
+    if constexpr (Real<R>::kIsDouble) {
+        return false;
+    } else {
+        if (!ob.plane_off) return false;
+        const uint32_t b = ldg_keep(ob.plane_off + vox), en = ldg_keep(ob.plane_off + vox + 1);
+        for (uint32_t k = b; k < en; ++k) {
+            const float4 pl = ldg_keep(ob.planes + k);
+            if (fmaf(pl.x, e.x, fmaf(pl.y, e.y, fmaf(pl.z, e.z, -pl.w))) > ob.plane_eps) return true;
+        }
+        return false;
+    }
+}
+
+// Where a flight ends relative to its medium (wavefront logic pass, the end point's SDF
+// value already loaded): kEndIn -- provably inside, no traversal (flight_contained);
+// kEndOut -- a convex object's end point provably outside (off the grid, a voxel wholly
+// outside, or beyond a face plane): the flight leaves the object; kEndUnknown.
+enum : int { kEndUnknown = 0, kEndIn = 1, kEndOut = 2 };
+template <class R>
+SST_D int end_where(const ObjK<R>& ob, R v_end, bool in_grid, uint32_t vox, V3<R> x, V3<R> e, R t, R r_x) {
+    if (Real<R>::kIsDouble) return kEndUnknown;
+    if (!in_grid) return ob.convex ? kEndOut : kEndUnknown;  // the grid covers the mesh box
+    if (v_end < R(0) && (ob.convex || t < r_x - v_end)) return kEndIn;
+    if (ob.convex) {
+        if (v_end > R(0)) return kEndOut;  // conservative SDF: the whole voxel is outside
+        if (end_inside_planes(ob, vox, e)) return kEndIn;
+        return end_beyond_a_plane(ob, vox, e) ? kEndOut : kEndUnknown;
+    }
     uint32_t vox_x;
-    return sdf_voxel(ob, x, &vox_x) && vox_x == vox && seg_inside_planes(ob, vox, x, e);
+    return sdf_voxel(ob, x, &vox_x) && vox_x == vox && seg_inside_planes(ob, vox, x, e) ? kEndIn : kEndUnknown;
 }
 
 // FP32 leak detection: the conservative SDF value at x is > 0 (or x is off the grid)
@@ -547,13 +572,15 @@ SST_D void trace_persistent(const TraceArgs<R>& a) {
                     if (my < a.pool.counts[kQResume]) {
                         uint32_t phase;  // the slot's staged NEE contributions are added here
                         load_slot(a.pool, a.pool.q_live[my], p, &phase, a.sc.cam_pos, true, true);
-                        if (phase == 4u) {  // kPhEnded: absorbed once those were in
+                        if (phase >= 4u) {  // kPhEnded(Escaped): absorbed / escaped once those were in
+                            if (phase == 5u) p.L += a.sc.bg[p.c];
                             a.radiance[p.id] = p.L;
                             if (a.segments) a.segments[p.id] = p.seg;
                             if (a.exit_state) write_exit_state(a.exit_state, p);
                             ++st.paths;
                             st.seg += p.seg;
-                            ++st.absorbed;
+                            st.absorbed += phase == 4u;
+                            st.escaped += phase == 5u;
                         } else {
                             alive = true;
                         }

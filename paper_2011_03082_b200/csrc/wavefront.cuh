@@ -45,13 +45,17 @@ SST_D uint32_t meta_phase(uint32_t m) { return (m >> 11) & 3u; }
 // live only in its camera-ray trace record (xl / wr were not written; L = 0).
 constexpr uint32_t kMetaFresh = 1u << 13;
 // NEE mailbox (types.cuh kNeeChain): meta.w bits 24-27 = number of staged NEE records
-// whose contributions the slot's next logic visit adds to L (in event order); bit 14 =
-// the path was absorbed after staging some: the next visit adds them, then ends it.
+// whose contributions the slot's next logic visit adds to L (in event order); bit 14 /
+// bit 15 = the path was absorbed / escaped after staging some: the next visit adds them,
+// then ends it.
 constexpr uint32_t kMetaEndAbsorbed = 1u << 14;
+constexpr uint32_t kMetaEndEscaped = 1u << 15;
+constexpr uint32_t kMetaEnded = kMetaEndAbsorbed | kMetaEndEscaped;
 constexpr int kMetaPendShift = 24;
 SST_D uint32_t meta_pending(uint32_t m) { return (m >> kMetaPendShift) & 0xfu; }
-// Transient phase returned by load_slot for a slot whose path already ended (absorbed).
-constexpr uint32_t kPhEnded = 4;
+// Transient phases returned by load_slot for a slot whose path already ended (absorbed /
+// escaped) once its staged contributions are in.
+constexpr uint32_t kPhEnded = 4, kPhEndedEscaped = 5;
 // Integer payloads carried in the spare lane of a record vector.
 template <class R>
 SST_D R int_bits(int v) {
@@ -145,7 +149,7 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
         } else {
             for (uint32_t i = 0; i < k; ++i) p.L += q.nee_res[s * kNeeChain + i];
         }
-        if (m.w & kMetaEndAbsorbed) *phase = kPhEnded;
+        if (m.w & kMetaEnded) *phase = (m.w & kMetaEndEscaped) ? kPhEndedEscaped : kPhEnded;
     }
 }
 
@@ -525,14 +529,15 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
     *live = false;
     *nrec_out = 0u;
     ++st.wf_slots;
-    const bool ended = (mt.w & kMetaEndAbsorbed) != 0u;
+    const bool ended = (mt.w & kMetaEnded) != 0u;
     m = __ballot_sync(m, phase != kPhEmpty && !ended);
     // ended in k_wf_sphere (which runs concurrently with the generation kernel and so
     // does not touch the free queue): free it now if new paths remain
     if (phase == kPhEmpty) return *a.work < wf_n_paths<R, EX>(a) ? kEmitFree : kEmitNone;
-    if (ended) {  // absorbed after staging NEE records: add them, then the path ends
+    if (ended) {  // absorbed / escaped after staging NEE records: add them, then it ends
         load_slot_from(q, s, mt, p, &phase, sc.cam_pos, false, true, &mb);
-        finish_path(a, p, kEndAbsorbed, st);
+        if (mt.w & kMetaEndEscaped) p.L += sc.bg[p.c];
+        finish_path(a, p, (mt.w & kMetaEndEscaped) ? kEndEscaped : kEndAbsorbed, st);
         q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
         return kEmitFree;
     }
@@ -549,6 +554,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
     int emit = kEmitNone;
     int end = -1;
     bool run = true;
+    bool bg_pending = false;  // an escape decided without its exit: background not yet added
     uint32_t nrec = 0u;  // NEE records staged by this visit (the mailbox)
 #pragma unroll 1
     for (int guard = 0; guard < 4 + 2 * static_cast<int>(kNeeChain); ++guard) {
@@ -632,9 +638,22 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                     trace = !(t_free < p.r_here);
                     if (trace) {
                         trace = !(t_free < rs);
-                        if (trace && a.convex_end)
-                            trace = !end_contained(ob, v_end, in_end, vox_end, p.x, x_end, t_free,
-                                                   Real<R>::fmax_(p.r_here, rs));
+                        if (trace && a.convex_end) {
+                            const int where = end_where(ob, v_end, in_end, vox_end, p.x, x_end, t_free,
+                                                        Real<R>::fmax_(p.r_here, rs));
+                            trace = where != kEndIn;
+                            // The flight certainly leaves the convex object; if its ray misses
+                            // every other object's bounding sphere, so does the ray continuing
+                            // from the exit point (a sub-ray): the path escapes. Without an
+                            // exit-state output the exit point itself is never needed.
+                            // (The background is added once the visit's staged NEE
+                            // contributions are in: the reference's order of additions.)
+                            if (where == kEndOut && !a.exit_state && !ray_may_hit(sc, p.x, p.w, p.obj)) {
+                                end = kEndEscaped;
+                                bg_pending = true;
+                                trace = false;
+                            }
+                        }
                     }
                 }
             }
@@ -712,12 +731,14 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
         if (end >= 0) run = false;
     }
     if (end >= 0) {
-        if (end == kEndAbsorbed && nrec > 0u) {  // its staged contributions arrive next pass
-            store_slot(q, s, p, kPhFlight, nrec, kMetaEndAbsorbed);
+        if ((end == kEndAbsorbed || end == kEndEscaped) && nrec > 0u) {
+            // its staged contributions arrive next pass (then an escape adds the background)
+            store_slot(q, s, p, kPhFlight, nrec, end == kEndAbsorbed ? kMetaEndAbsorbed : kMetaEndEscaped);
             *live = true;
             *nrec_out = nrec;
             return kEmitNone;
         }
+        if (bg_pending) p.L += sc.bg[p.c];
         finish_path(a, p, end, st);  // capped: L = 0, the staged records do not matter
         q.meta[s] = make_uint4(0u, 0u, 0u, pack_meta(-1, 0, false, kPhEmpty, -1));
         return kEmitFree;
