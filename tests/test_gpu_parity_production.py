@@ -145,6 +145,26 @@ def test_wavefront_fp32_paths_match_reference_at_bench_config(wf32, bench_scene,
 
 
 @pytest.mark.parametrize("integ", [1, 0], ids=["ST", "PT"])
+def test_wavefront_fp32_render_semantics_match_reference(wf32, bench_scene, integ):
+    """Without an exit-state output (the render path the bench times) a flight that
+    provably leaves its convex object and whose ray misses every other bounding sphere
+    escapes without the exit traversal (DESIGN.md §5 rule 5). Same gates against the
+    reference, and the same radiance / segments as the exit-state run on all but rare
+    FP32 edge cases (an exit the BVH's Moller-Trumbore misses at an edge)."""
+    sc, ref = bench_scene
+    pix, smp, ch = _keys(sc.n_pixels, 100_000, 31 + integ)
+    g_rad, g_seg = wf32.trace_paths(integ, 1, 1, pix, smp, ch)
+    x_rad, x_seg, _ = wf32.trace_paths(integ, 1, 1, pix, smp, ch, exit_state=True)
+    same = (g_rad == x_rad) & (g_seg == x_seg)
+    assert same.mean() >= 0.99995, same.mean()
+    o_rad, o_seg = ref.trace(integ, 1, 1, pix, smp, ch)
+    r = _rates(g_rad, g_seg, o_rad, o_seg)
+    assert r["seg"] >= 0.9999, (ref.kind, r)
+    assert r[1e-3] >= 0.998, (ref.kind, r)
+    assert r[1e-4] >= 0.95, (ref.kind, r)
+
+
+@pytest.mark.parametrize("integ", [1, 0], ids=["ST", "PT"])
 def test_wavefront_fp64_paths_match_reference_at_bench_config(wf64, bench_scene, integ):
     sc, ref = bench_scene
     pix, smp, ch = _keys(sc.n_pixels, 30_000, 21 + integ)
