@@ -155,6 +155,9 @@ struct sst_gpu_ctx {
     sst_scene_desc desc{};
     DevBuf nodes32, tris32, nodes64, tris64, objs32, objs64, grid_off, grid_tri, grid_split;
     DevBuf grid_tris32;  // FP32 triangle records in light-grid list order (grid_tri gathered)
+    DevBuf cam_off, cam_idx, cam_tris32;  // camera tiles (types.cuh DevScene::cam_off)
+    uint32_t cam_tiles_x = 0, cam_tiles_y = 0;
+    uint64_t cam_list_n = 0;
     uint32_t grid_res = 0;
     std::vector<DevBuf> sdf_dev, skip_dev, plane_off_dev, planes_dev;
     DevScene<float> sc32{};
@@ -581,6 +584,8 @@ void build_skip_gpu(sst_gpu_ctx* ctx, const sst_object_desc& od, ObjectHost& oh)
     for (int k = 0; k < 3; ++k) oh.skip_dims[k] = a.dims[k];
 }
 
+constexpr uint32_t kCamTile = 8;  // camera tile size in pixels (build_camera_tiles)
+
 template <class R>
 void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const DevBuf& tris, DevBuf& objs) {
     const sst_scene_desc& d = ctx->desc;
@@ -696,6 +701,15 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
     sc.grid_tri = use_grid ? ctx->grid_tri.as<uint32_t>() : nullptr;
     sc.grid_tris = use_grid && std::is_same<R, float>::value ? ctx->grid_tris32.p : nullptr;
     {
+        const char* e = std::getenv("SST_NO_CAM_TILES");
+        const bool use = std::is_same<R, float>::value && ctx->cam_off.p && !(e && e[0] == '1');
+        sc.cam_off = use ? ctx->cam_off.as<uint32_t>() : nullptr;
+        sc.cam_tris = use ? ctx->cam_tris32.p : nullptr;
+        sc.cam_tile = kCamTile;
+        sc.cam_tiles_x = ctx->cam_tiles_x;
+        sc.cam_tiles_y = ctx->cam_tiles_y;
+    }
+    {
         const char* e = std::getenv("SST_NO_GRID_SPLIT");
         sc.grid_split = use_grid && std::is_same<R, float>::value && !(e && e[0] == '1') ? ctx->grid_split.as<uint32_t>()
                                                                                           : nullptr;
@@ -707,6 +721,80 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
 // Per triangle: the cone from the light that contains it (axis = mean vertex
 // direction, half angle = max vertex angle + padding); cells overlap-tested on the
 // GPU in FP64 (count pass, host prefix sum, fill pass).
+// Camera tiles (types.cuh DevScene::cam_off): per kCamTile x kCamTile pixel tile, the
+// leaf-order triangles that face the camera (a camera ray can only enter them: FP32 outside
+// rays accept entering crossings only) whose projected bounding box, grown by one pixel,
+// meets the tile. A triangle reaching behind the camera goes into every tile.
+void build_camera_tiles(sst_gpu_ctx* ctx, const sst_scene_desc* d,
+                        const std::vector<std::array<std::array<double, 3>, 3>>& tv, const FlatBvh& bvh) {
+    auto sub = [](const double* a, const double* b) { return std::array<double, 3>{a[0] - b[0], a[1] - b[1], a[2] - b[2]}; };
+    auto cross = [](std::array<double, 3> a, std::array<double, 3> b) {
+        return std::array<double, 3>{a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    };
+    auto dot = [](std::array<double, 3> a, std::array<double, 3> b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
+    auto norm = [&](std::array<double, 3> a) {
+        const double l = std::sqrt(dot(a, a));
+        return std::array<double, 3>{a[0] / l, a[1] / l, a[2] / l};
+    };
+    const auto fwd = norm(sub(d->cam_look_at, d->cam_position));
+    const auto right = norm(cross(fwd, std::array<double, 3>{d->cam_up[0], d->cam_up[1], d->cam_up[2]}));
+    const auto up = cross(right, fwd);
+    const double tan_half = std::tan(d->cam_vfov_deg * 3.14159265358979323846 / 360.0);
+    const double aspect = static_cast<double>(d->width) / static_cast<double>(d->height);
+    const uint32_t nx = (d->width + kCamTile - 1) / kCamTile, ny = (d->height + kCamTile - 1) / kCamTile;
+    const uint32_t n = bvh.n_tris;
+    std::vector<std::vector<uint32_t>> tiles(static_cast<size_t>(nx) * ny);
+    for (uint32_t k = 0; k < n; ++k) {
+        const auto& t = tv[bvh.order[k]];
+        std::array<double, 3> c[3];
+        for (int i = 0; i < 3; ++i) c[i] = {t[i][0], t[i][1], t[i][2]};
+        const auto nn = cross(std::array<double, 3>{c[1][0] - c[0][0], c[1][1] - c[0][1], c[1][2] - c[0][2]},
+                              std::array<double, 3>{c[2][0] - c[0][0], c[2][1] - c[0][1], c[2][2] - c[0][2]});
+        const auto to_cam = sub(d->cam_position, c[0].data());
+        const double f = dot(nn, to_cam);
+        if (f < -1e-9 * std::sqrt(dot(nn, nn) * dot(to_cam, to_cam))) continue;  // clearly faces away
+        double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+        bool behind = false;
+        for (int i = 0; i < 3; ++i) {
+            const auto q = sub(c[i].data(), d->cam_position);
+            const double z = dot(q, fwd);
+            if (!(z > 1e-9)) {
+                behind = true;
+                break;
+            }
+            const double px = (dot(q, right) / z / (tan_half * aspect) + 1.0) * 0.5 * d->width;
+            const double py = (1.0 - dot(q, up) / z / tan_half) * 0.5 * d->height;
+            x0 = std::fmin(x0, px), x1 = std::fmax(x1, px), y0 = std::fmin(y0, py), y1 = std::fmax(y1, py);
+        }
+        int tx0 = 0, tx1 = static_cast<int>(nx) - 1, ty0 = 0, ty1 = static_cast<int>(ny) - 1;
+        if (!behind) {
+            tx0 = std::max(tx0, static_cast<int>(std::floor((x0 - 1.0) / kCamTile)));
+            tx1 = std::min(tx1, static_cast<int>(std::floor((x1 + 1.0) / kCamTile)));
+            ty0 = std::max(ty0, static_cast<int>(std::floor((y0 - 1.0) / kCamTile)));
+            ty1 = std::min(ty1, static_cast<int>(std::floor((y1 + 1.0) / kCamTile)));
+        }
+        for (int y = ty0; y <= ty1; ++y)
+            for (int x = tx0; x <= tx1; ++x) tiles[static_cast<size_t>(y) * nx + x].push_back(k);
+    }
+    std::vector<uint32_t> off(tiles.size() + 1, 0), idx;
+    for (size_t i = 0; i < tiles.size(); ++i) {
+        off[i] = static_cast<uint32_t>(idx.size());
+        idx.insert(idx.end(), tiles[i].begin(), tiles[i].end());
+    }
+    off[tiles.size()] = static_cast<uint32_t>(idx.size());
+    ctx->cam_off.reserve(off.size() * sizeof(uint32_t));
+    ctx->cam_idx.reserve(std::max<size_t>(idx.size(), 1) * sizeof(uint32_t));
+    ctx->cam_tris32.reserve(std::max<size_t>(idx.size(), 1) * sizeof(TriF));
+    CK(cudaMemcpyAsync(ctx->cam_off.p, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (!idx.empty())
+        CK(cudaMemcpyAsync(ctx->cam_idx.p, idx.data(), idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+    ctx->cam_tiles_x = nx;
+    ctx->cam_tiles_y = ny;
+    ctx->cam_list_n = idx.size();
+    CK(cudaStreamSynchronize(ctx->stream));  // the host vectors die here
+}
+
 void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
                       const std::vector<std::array<std::array<double, 3>, 3>>& tv, const std::vector<uint32_t>& tobj,
                       const FlatBvh& bvh) {
@@ -1079,6 +1167,11 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
             CK(launch_gather_tris(ctx->grid_tri.as<uint32_t>(), ctx->tris32.as<TriF>(), n_list,
                                   ctx->grid_tris32.as<TriF>(), ctx->stream));
         bytes += n_list * sizeof(TriF);
+        build_camera_tiles(ctx, d, tv, bvh);
+        if (ctx->cam_list_n)
+            CK(launch_gather_tris(ctx->cam_idx.as<uint32_t>(), ctx->tris32.as<TriF>(), ctx->cam_list_n,
+                                  ctx->cam_tris32.as<TriF>(), ctx->stream));
+        bytes += ctx->cam_list_n * sizeof(TriF) + (static_cast<uint64_t>(ctx->cam_tiles_x) * ctx->cam_tiles_y + 1) * 4;
         ctx->scene_bytes = bytes;
     }
     fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
@@ -1790,7 +1883,7 @@ void sst_gpu_destroy(sst_gpu_ctx* ctx) {
         auto it = g_const_owner.find(ctx->device);
         if (it != g_const_owner.end() && it->second.ctx == ctx) it->second.ctx = nullptr;
     }
-    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri, &ctx->grid_split, &ctx->grid_tris32,
+    for (DevBuf* b : {&ctx->nodes32, &ctx->tris32, &ctx->nodes64, &ctx->tris64, &ctx->objs32, &ctx->objs64, &ctx->grid_off, &ctx->grid_tri, &ctx->grid_split, &ctx->grid_tris32, &ctx->cam_off, &ctx->cam_idx, &ctx->cam_tris32,
                       &ctx->radiance, &ctx->segments, &ctx->work, &ctx->stats, &ctx->error, &ctx->film_sum,
                       &ctx->film_sq, &ctx->keys_pix, &ctx->keys_smp, &ctx->keys_ch, &ctx->step_in, &ctx->step_out})
         b->release();

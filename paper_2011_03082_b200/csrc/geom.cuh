@@ -409,6 +409,39 @@ SST_D R optical_depth(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R t_ma
     }
 }
 
+// ---------------------------------------------------------------- camera tiles
+// Nearest entering hit of a camera ray from its pixel tile's triangle list (FP32;
+// DevScene::cam_off): the same Moller-Trumbore test and acceptance as the BVH leaves.
+template <class R>
+SST_D bool camera_tile_hit(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R* t_best, uint32_t* tri,
+                           uint32_t* obj, uint64_t& n_tris) {
+    const R z = dot(ray.d, sc.cam_fwd);
+    const R px = (Real<R>::div_(dot(ray.d, sc.cam_right), z) / (sc.tan_half * sc.aspect) + R(1)) * R(0.5) *
+                 static_cast<R>(sc.width);
+    const R py = (R(1) - Real<R>::div_(dot(ray.d, sc.cam_up), z) / sc.tan_half) * R(0.5) * static_cast<R>(sc.height);
+    int tx = static_cast<int>(px) / static_cast<int>(sc.cam_tile), ty = static_cast<int>(py) / static_cast<int>(sc.cam_tile);
+    tx = tx < 0 ? 0 : (tx >= static_cast<int>(sc.cam_tiles_x) ? static_cast<int>(sc.cam_tiles_x) - 1 : tx);
+    ty = ty < 0 ? 0 : (ty >= static_cast<int>(sc.cam_tiles_y) ? static_cast<int>(sc.cam_tiles_y) - 1 : ty);
+    const uint32_t tile = static_cast<uint32_t>(ty) * sc.cam_tiles_x + static_cast<uint32_t>(tx);
+    const uint32_t b = ldg_keep(sc.cam_off + tile), e = ldg_keep(sc.cam_off + tile + 1);
+    n_tris += e - b;
+    bool found = false;
+    for (uint32_t k = b; k < e; ++k) {
+        V3<R> v0, e1, e2;
+        uint32_t o, id;
+        load_tri<R>(sc.cam_tris, k, v0, e1, e2, o, id);
+        R det;
+        const R t = ray_tri(ray, v0, e1, e2, t_min, *t_best, &det);
+        if (t >= R(0) && det > R(0)) {
+            *t_best = t;
+            *tri = id;
+            *obj = o;
+            found = true;
+        }
+    }
+    return found;
+}
+
 // ---------------------------------------------------------------- light grid
 // Cube-map cell of a direction (faces +x,-x,+y,-y,+z,-z; (s,t) = minor/|major|).
 // Shared by the device lookup and the build kernel (cell centres).

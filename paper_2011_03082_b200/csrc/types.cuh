@@ -109,6 +109,14 @@ struct DevScene {
     // object never crosses that object's faces that face away from the light (FP32: those
     // tests are skipped when they are the whole back part). Null: test the whole list.
     const uint32_t* grid_split;
+    // FP32 camera tiles (cam_tile x cam_tile pixels): per tile the triangles facing the
+    // camera whose projection (grown by a pixel) meets it, as contiguous TriF records
+    // (CSR cam_off over cam_tiles_x * cam_tiles_y tiles). A camera ray's nearest entering
+    // hit is among its tile's list: the trace kernel answers camera rays from it instead
+    // of the BVH. Null: BVH.
+    const uint32_t* cam_off;
+    const void* cam_tris;
+    uint32_t cam_tile, cam_tiles_x, cam_tiles_y;
     uint32_t grid_res;
     uint32_t bvh_depth;  // FlatBvh::max_depth (traversal stack bound)
 };

@@ -950,9 +950,19 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
                     ray = make_ray(mk<R>(o.x, o.y, o.z), mk<R>(d.x, d.y, d.z));
                     want = Real<R>::kIsDouble ? 0 : (inside ? -1 : 1);
                     t_min = skip >= 0 ? sc.surf_eps : sc.t_min;
-                    // an in-medium flight starts at its object's subtree (disjoint objects, FP32)
-                    tr.init(o.w, inside ? sc.objs[static_cast<int>(f >> 16) - 1].bvh_root : 0);
-                    have = true;
+                    if (cam && sc.cam_off) {  // camera ray: its pixel tile's list, no traversal
+                        R t_best = o.w;
+                        uint32_t tri = 0u, obj = 0u;
+                        const bool found = camera_tile_hit(sc, ray, t_min, &t_best, &tri, &obj, tris);
+                        q.tr_cam[s] = Q4<R>{ray.d.x, ray.d.y, ray.d.z, R(0)};
+                        q.thit[s] = t_best;
+                        q.hinfo[s] = make_uint2(found ? tri : 0u, (found ? obj : 0u) | (found ? 0x80000000u : 0u));
+                        ++trav;
+                    } else {
+                        // an in-medium flight starts at its object's subtree (disjoint objects, FP32)
+                        tr.init(o.w, inside ? sc.objs[static_cast<int>(f >> 16) - 1].bvh_root : 0);
+                        have = true;
+                    }
                 }
             }
         }
