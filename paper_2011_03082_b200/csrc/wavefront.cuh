@@ -1059,13 +1059,14 @@ SST_D void shadow_rec(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t idx, c
 }
 
 // Records [0, n) of one shadow range (queue position pos(i)) by work stealing in grabs
-// of 32 * kShadowGrab items per warp: the grab's queue entries are loaded together and
-// each lane's next record is loaded while its current shadow ray is traced. Measured on
-// C5 (ms per 32-spp slab): grab 1 (no pipelining) 41.4, 2 at 8 blocks/SM 41.7, 4 at 10
-// blocks/SM 41.3 (spills), 4 at 8: 44.2, 4 at 6: 50.7 -- the chain is not what limits
-// the kernel (the cells' triangle loads and per-lane list lengths are); default 1.
+// of 32 * kShadowGrab items per warp, processed one after another: the grab's single
+// atomic on the shared cursor is what matters (950M shadow rays per C5 slab -- at one
+// same-address atomic per 32 rays the cursor's L2 atomic throughput showed as 16% of the
+// kernel's stall samples). Measured (Gseg/s): grab 1: 7.79, 2: 8.00, 4: 8.03, 8: 8.01;
+// loading each lane's next record while its current ray is traced cost more registers
+// than it saved (grab 2: 7.95, grab 4: 7.87).
 #ifndef SST_SHADOW_GRAB
-#define SST_SHADOW_GRAB 1
+#define SST_SHADOW_GRAB 4
 #endif
 constexpr uint32_t kShadowGrab = SST_SHADOW_GRAB;
 constexpr uint32_t kNoRec = 0xffffffffu;
@@ -1083,22 +1084,15 @@ SST_D void shadow_range(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t* cur
         }
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= n) break;  // warp-uniform
-        uint32_t idx[kShadowGrab];
-#pragma unroll
+#pragma unroll 1
         for (uint32_t j = 0; j < kShadowGrab; ++j) {
             const uint32_t i = base + 32u * j + lane;
-            idx[j] = i < n ? q.q_shadow[pos(i)] : kNoRec;
-        }
-        Q4<R> np{}, nw{};
-        if (idx[0] != kNoRec) np = q.nee_p[idx[0]], nw = q.nee_w[idx[0]];
-#pragma unroll
-        for (uint32_t j = 0; j < kShadowGrab; ++j) {
-            const Q4<R> cp = np, cw = nw;
-            if (j + 1 < kShadowGrab && idx[j + 1] != kNoRec) np = q.nee_p[idx[j + 1]], nw = q.nee_w[idx[j + 1]];
-            if (idx[j] != kNoRec) {
-                shadow_rec(a, q, idx[j], cp, cw, tris);
-                ++shadow;
-            }
+            if (i - lane >= n) break;  // warp-uniform
+            if (i >= n) continue;
+            const uint32_t idx = q.q_shadow[pos(i)];
+            if (idx == kNoRec) continue;
+            shadow_rec(a, q, idx, q.nee_p[idx], q.nee_w[idx], tris);
+            ++shadow;
         }
     }
 }
