@@ -1042,8 +1042,11 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         } else {
             build_sdf_gpu(ctx, od, objs[o], is_watertight(tri));
         }
-        build_skip_gpu(ctx, od, objs[o]);
         objs[o].convex = is_convex(od.positions, od.n_vertices, tri);
+        // the fine skip grid only pays for non-convex objects: a convex object's face-plane
+        // lists decide the flights it would cull exactly (C5: 8.04 -> 8.33 Gseg/s without
+        // it; C3 bumpy sphere sigma_t = 160: 4.27 vs 4.44 ms/spp with it)
+        if (!objs[o].convex) build_skip_gpu(ctx, od, objs[o]);
         build_plane_lists(objs[o], tv, tv.size() - od.n_triangles, od.n_triangles);
         {  // bounding sphere: box centre, farthest referenced vertex
             double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
