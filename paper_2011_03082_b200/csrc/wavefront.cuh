@@ -243,6 +243,31 @@ SST_D void flush_counts(unsigned long long* stats, const unsigned long long (&v)
         if (sh[k]) atomicAdd(dst + k, sh[k]);
 }
 
+// Per-thread counters of one wavefront launch: a thread handles tens of slots per launch,
+// so 32 bits suffice (the logic pass is register-bound; 64-bit counters cost it ~9 more).
+struct WfStats {
+    uint32_t paths = 0, absorbed = 0, escaped = 0, capped = 0, errors = 0;
+    uint32_t seg = 0, sphere = 0, events = 0, lane_iters = 0, wf_slots = 0;
+    DecodeCount dc;
+};
+SST_D void flush_lane_stats(unsigned long long* stats, const WfStats& st) {
+    unsigned long long v[kStCount] = {};
+    v[kStPaths] = st.paths;
+    v[kStSegments] = st.seg;
+    v[kStSphere] = st.sphere;
+    v[kStEvents] = st.events;
+    v[kStDecL] = st.dc.l;
+    v[kStDecP] = st.dc.p;
+    v[kStDecE] = st.dc.e;
+    v[kStAbsorbed] = st.absorbed;
+    v[kStEscaped] = st.escaped;
+    v[kStCapped] = st.capped;
+    v[kStErrors] = st.errors;
+    v[kStLaneIters] = st.lane_iters;
+    v[kStWfSlots] = st.wf_slots;
+    flush_counts<kStCount>(stats, v);
+}
+
 SST_D void flush_lane_stats(unsigned long long* stats, const LaneStats& st) {
     const unsigned long long v[kStCount] = {st.paths, st.seg, st.sphere, st.events, st.dc.l, st.dc.p,
                                             st.dc.e, st.absorbed, st.escaped, st.capped, st.errors, st.shadow,
@@ -252,8 +277,8 @@ SST_D void flush_lane_stats(unsigned long long* stats, const LaneStats& st) {
 }
 
 // Path end: the radiance (and segment count) of path p.id, end statistics.
-template <class R>
-SST_D void finish_path(const TraceArgs<R>& a, const PathLocal<R>& p, int end, LaneStats& st) {
+template <class R, class Stats>
+SST_D void finish_path(const TraceArgs<R>& a, const PathLocal<R>& p, int end, Stats& st) {
     a.radiance[p.id] = p.L;
     if (a.segments) a.segments[p.id] = p.seg;
     if (a.exit_state) write_exit_state(a.exit_state, p);
@@ -517,7 +542,7 @@ SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list,
 // ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
 SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, const uint4 mt, unsigned m,
-                        LaneStats& st, bool* live, WfRec<R>& rec, uint32_t* nrec_out, uint4* meta_out) {
+                        WfStats& st, bool* live, WfRec<R>& rec, uint32_t* nrec_out, uint4* meta_out) {
     // m: the lanes of this warp calling (converged). The loop below has no break /
     // continue / return inside: every stage is an if-block that all lanes of the warp
     // reach together, so lanes that got to a collision by different routes (after a
@@ -762,7 +787,7 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
 // cost nothing in later iterations.
 template <class R, bool ST, bool EX>
 SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
-    LaneStats st;
+    WfStats st;
     // q_in == null: every slot in slot order (while the pool is full: coalesced SoA
     // accesses); otherwise the compacted list of the previous iteration (drain)
     const uint32_t n_in = q.q_in ? q.counts[q.cnt_in] : q.cap;
@@ -993,7 +1018,7 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
 template <class R>
 SST_D void wf_sphere(const TraceArgs<R>& a, const WfPool<R>& q) {
     const DevScene<R>& sc = a.sc;
-    LaneStats st;
+    WfStats st;
     const uint32_t n = q.counts[kQSphere];
     for (;;) {
         const uint32_t i = warp_fetch(q.counts + kQFetchSphere);
