@@ -1218,14 +1218,15 @@ void kt_end(sst_gpu_ctx* ctx, cudaStream_t s, int kind) {
 bool use_wavefront(const sst_gpu_ctx* ctx, bool st) { return ctx->wavefront >= 2 || (ctx->wavefront == 1 && st); }
 
 // Sizes of the wavefront pool's arrays for `cap` slots (carve_pool order).
-constexpr int kPoolArrays = 21;
+constexpr int kPoolArrays = 25;
 template <class R>
 size_t pool_layout(uint32_t cap, size_t (&off)[kPoolArrays]) {
     const size_t n = cap, nk = n * kNeeChain;
     const size_t sizes[] = {n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 8, n * 16, n * sizeof(R),
                             n * 8, nk * sizeof(Q4<R>), nk * sizeof(Q4<R>), n * 4, (nk + n) * 4, n * 4,
                             kQCount * 4, 8, n * 4, n * 4, n * 4,
-                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>), nk * sizeof(R)};
+                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * sizeof(Q4<R>), nk * sizeof(R),
+                            n * sizeof(Q4<R>), n * sizeof(Q4<R>), n * 4, n * 4};
     static_assert(sizeof(sizes) / sizeof(sizes[0]) == kPoolArrays, "pool arrays");
     size_t total = 0;
     int k = 0;
@@ -1265,6 +1266,10 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.tr_f = reinterpret_cast<uint32_t*>(base + off[18]);
     q.tr_cam = reinterpret_cast<Q4<R>*>(base + off[19]);
     q.nee_res = reinterpret_cast<R*>(base + off[20]);
+    q.trs_o = reinterpret_cast<Q4<R>*>(base + off[21]);
+    q.trs_d = reinterpret_cast<Q4<R>*>(base + off[22]);
+    q.trs_f = reinterpret_cast<uint32_t*>(base + off[23]);
+    q.q_trace = reinterpret_cast<uint32_t*>(base + off[24]);
     return q;
 }
 

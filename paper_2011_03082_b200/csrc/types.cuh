@@ -161,6 +161,7 @@ enum : int {
     kQTicket = 10,  // last-block detection of the generation kernel
     kQShadowS = 11,       // sphere-step NEE records (stored from the back of the shadow arrays)
     kQFetchShadowS = 12,  // their work-stealing cursor
+    kQTraceLogic = 13,    // trace entries [0, n) are the logic pass's (slot records), the rest camera records
     kQCount = 14
 };
 // NEE mailbox (wavefront.cuh): a logic visit chains up to kNeeChain delta-tracking
@@ -191,6 +192,14 @@ struct WfPool {
     Q4<R>* tr_o;      // origin, t_max
     Q4<R>* tr_d;      // direction, skip triangle (int bits)
     uint32_t* tr_f;   // (cull + 1) | inside << 8 | camera ray << 9
+    // A flight the logic pass queues is written to its slot's record (trs_*, slot-indexed)
+    // the moment it is decided -- no record held in registers until the queue append --
+    // and the trace queue entry q_trace[j] names the slot; positions [counts[kQTraceLogic],
+    // counts[kQTrace]) hold the generation kernel's camera records (tr_*, position-indexed).
+    Q4<R>* trs_o;
+    Q4<R>* trs_d;
+    uint32_t* trs_f;
+    uint32_t* q_trace;
     // Direction of a camera ray, copied by the trace kernel next to its result (a fresh
     // path reads it there in the next logic pass, which overwrites the records).
     Q4<R>* tr_cam;

@@ -116,9 +116,9 @@ SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLoc
     // the megakernel hand-off reads them back: a logic visit takes the traversal result)
     const bool queued = meta_phase(m.w) == kPhTrace;
     p.skip = queued ? -1 : static_cast<int>(m.z);
-    if (need_tpend && queued && !(m.w & kMetaFresh)) {
-        p.t_pend = q.tr_o[m.z].w;
-        p.skip = bits_int<R>(q.tr_d[m.z].w);
+    if (need_tpend && queued && !(m.w & kMetaFresh)) {  // the slot's own trace record
+        p.t_pend = q.trs_o[s].w;
+        p.skip = bits_int<R>(q.trs_d[s].w);
     }
     if (m.w & kMetaFresh) {  // camera ray: the state is in the trace record
         const Q4<R> d = q.tr_cam[m.z];
@@ -213,7 +213,8 @@ SST_D void prefetch_trace(const WfPool<R>& q, uint32_t j, uint32_t n, uint32_t l
     j += SST_WF_PREFETCH_AHEAD;
     if (j >= len) return;
     if (n > len - j) n = len - j;
-    l2_prefetch(q.tr_o + j, n * sizeof(Q4<R>));
+    l2_prefetch(q.q_trace + j, n * sizeof(uint32_t));  // logic entries (their records are gathered)
+    l2_prefetch(q.tr_o + j, n * sizeof(Q4<R>));         // camera records
     l2_prefetch(q.tr_d + j, n * sizeof(Q4<R>));
     l2_prefetch(q.tr_f + j, n * sizeof(uint32_t));
 }
@@ -542,7 +543,7 @@ SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list,
 // ends. Operation order per path is path_advance's.
 template <class R, bool ST, bool EX>
 SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, const uint4 mt, unsigned m,
-                        WfStats& st, bool* live, WfRec<R>& rec, uint32_t* nrec_out, uint4* meta_out) {
+                        WfStats& st, bool* live, uint32_t* nrec_out) {
     // m: the lanes of this warp calling (converged). The loop below has no break /
     // continue / return inside: every stage is an if-block that all lanes of the warp
     // reach together, so lanes that got to a collision by different routes (after a
@@ -693,11 +694,9 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
                 p.t_pend = t_free;
                 phase = kPhTrace;
                 emit = kEmitTrace;
-                rec.a = p.x;
-                rec.b = p.w;
-                rec.t = t_free;
-                rec.u = p.skip;
-                rec.v = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8) |
+                q.trs_o[s] = Q4<R>{p.x.x, p.x.y, p.x.z, t_free};
+                q.trs_d[s] = Q4<R>{p.w.x, p.w.y, p.w.z, int_bits<R>(p.skip)};
+                q.trs_f[s] = static_cast<uint32_t>(p.cull + 1) | (static_cast<uint32_t>(inside) << 8) |
                         (inside ? static_cast<uint32_t>(p.obj + 1) << 16 : 0u);
                 run = false;
             } else if (end < 0) {
@@ -770,12 +769,8 @@ SST_D int wf_logic_slot(const TraceArgs<R>& a, const WfPool<R>& q, uint32_t s, c
     }
     *live = true;
     *nrec_out = nrec;
-    if (emit == kEmitTrace) {  // meta stored by the caller once the record's position is known
-        store_state(q, s, p);
-        *meta_out = slot_meta(p, 0u, kPhTrace, nrec);
-    } else {
-        store_slot(q, s, p, phase, nrec);
-    }
+    // a queued traversal's meta.z (its queue position) is patched after the append
+    store_slot(q, s, p, phase, nrec);
     return emit;
 }
 
@@ -806,23 +801,18 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
         int emit = kEmitNone;
         bool live = false;
         uint32_t nrec = 0u;
-        WfRec<R> rec;
-        uint4 mo;
         const uint32_t s = i < n_in ? (q.q_in ? q.q_in[i] : i) : 0u;
         const unsigned m = __ballot_sync(0xffffffffu, i < n_in);
-        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, q.meta[s], m, st, &live, rec, &nrec, &mo);
+        if (i < n_in) emit = wf_logic_slot<R, ST, EX>(a, q, s, q.meta[s], m, st, &live, &nrec);
         const bool want[4] = {live, emit == kEmitTrace, emit == kEmitSphere, emit == kEmitFree};
         uint32_t* const ctr[4] = {q.counts + q.cnt_out, q.counts + kQTrace, ST ? q.counts + kQSphere : nullptr,
                                   q.counts + kQFree};
-        uint32_t* const qs[4] = {q.q_out, nullptr, q.q_sphere, q.q_free};
+        uint32_t* const qs[4] = {q.q_out, q.q_trace, q.q_sphere, q.q_free};
         uint32_t pos[4];
         // the staged NEE records of the visit go onto the shadow queue as record indices
         block_pushn_counted<4>(want, s, ctr, qs, pos, nrec, s * kNeeChain, q.counts + kQShadow, q.q_shadow,
                                base / stride);
-        if (emit == kEmitTrace) {  // the record at its queue position; its position in the meta
-            put_trace(q, pos[1], rec);
-            q.meta[s] = make_uint4(mo.x, mo.y, pos[1], mo.w);
-        }
+        if (emit == kEmitTrace) q.meta[s].z = pos[1];  // the traversal's queue position
     }
     flush_lane_stats(a.stats, st);
 }
@@ -888,6 +878,7 @@ SST_D void wf_gen(const TraceArgs<R>& a, const WfPool<R>& q) {
     __syncthreads();
     if (last && threadIdx.x == 0) {
         *a.work = base + n_new;
+        q.counts[kQTraceLogic] = t0;
         q.counts[kQTrace] = t0 + n_own;
         q.counts[q.cnt_out] = l0 + n_new;
         q.counts[kQFree] = 0u;
@@ -938,7 +929,7 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
 #define SST_TRACE_REFILL 16
 #endif
     constexpr int kTraceRefill = SST_TRACE_REFILL;
-    const uint32_t n = q.counts[kQTrace];
+    const uint32_t n = q.counts[kQTrace], n_logic = q.counts[kQTraceLogic];
     const unsigned lane = threadIdx.x & 31u;
     bool have = false, exhausted = false;
     uint32_t s = 0;
@@ -966,8 +957,14 @@ SST_D void wf_trace(const TraceArgs<R>& a, const WfPool<R>& q) {
                 const uint32_t i = base + __popc(idle & ((1u << lane) - 1u));
                 if (i < n) {
                     s = i;  // results go to the record's queue position
-                    const Q4<R> o = q.tr_o[i], d = q.tr_d[i];
-                    const uint32_t f = q.tr_f[i];
+                    Q4<R> o, d;
+                    uint32_t f;
+                    if (i < n_logic) {  // a logic flight: its slot's record
+                        const uint32_t sl = q.q_trace[i];
+                        o = q.trs_o[sl], d = q.trs_d[sl], f = q.trs_f[sl];
+                    } else {  // a camera ray: the generation kernel's record
+                        o = q.tr_o[i], d = q.tr_d[i], f = q.tr_f[i];
+                    }
                     skip = bits_int<R>(d.w);
                     cull = static_cast<int>(f & 0xffu) - 1;
                     const bool inside = (f >> 8) & 1u;
