@@ -927,7 +927,7 @@ void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
     }
     ctx->scene_cache.grid_res = res;
     ctx->grid_res = res;
-    ctx->scene_bytes_grid = offsets.size() * sizeof(uint32_t) + total * sizeof(uint32_t);
+    ctx->scene_bytes_grid = (offsets.size() + total + ncell) * sizeof(uint32_t);  // offsets, lists, split
     ctx->grid_list_n = total;
 }
 
@@ -1110,7 +1110,7 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
             CK(cudaMemcpyAsync(ctx->grid_tri.p, sc.grid_tri.data(), sc.grid_tri.size() * sizeof(uint32_t),
                                cudaMemcpyHostToDevice, ctx->stream));
         ctx->grid_res = sc.grid_res;
-        ctx->scene_bytes_grid = (sc.grid_off.size() + sc.grid_tri.size()) * sizeof(uint32_t);
+        ctx->scene_bytes_grid = (sc.grid_off.size() + sc.grid_tri.size() + sc.grid_split.size()) * sizeof(uint32_t);
         ctx->grid_list_n = sc.grid_tri.size();
     }
     const FlatBvh& bvh = ctx->scene_cache.bvh;
@@ -1169,12 +1169,12 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         if (n_list)
             CK(launch_gather_tris(ctx->grid_tri.as<uint32_t>(), ctx->tris32.as<TriF>(), n_list,
                                   ctx->grid_tris32.as<TriF>(), ctx->stream));
-        bytes += n_list * sizeof(TriF);
+        // (h2d bytes: the gathered records are built on the device from uploaded data)
         build_camera_tiles(ctx, d, tv, bvh);
         if (ctx->cam_list_n)
             CK(launch_gather_tris(ctx->cam_idx.as<uint32_t>(), ctx->tris32.as<TriF>(), ctx->cam_list_n,
                                   ctx->cam_tris32.as<TriF>(), ctx->stream));
-        bytes += ctx->cam_list_n * sizeof(TriF) + (static_cast<uint64_t>(ctx->cam_tiles_x) * ctx->cam_tiles_y + 1) * 4;
+        bytes += (ctx->cam_list_n + static_cast<uint64_t>(ctx->cam_tiles_x) * ctx->cam_tiles_y + 1) * 4;
         ctx->scene_bytes = bytes;
     }
     fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
