@@ -185,6 +185,9 @@ struct sst_gpu_ctx {
         FlatBvh bvh;
         std::vector<uint32_t> grid_off, grid_tri, grid_split;
         uint32_t grid_res = 0;
+        uint64_t cam_fp = 0;  // camera tiles of (geometry, camera): lists kept for re-uploads
+        std::vector<uint32_t> cam_off, cam_idx;
+        uint32_t cam_tiles_x = 0, cam_tiles_y = 0;
     } scene_cache;
 
     // Render pipeline: chunks of a render call rotate over kSlots streams so the
@@ -721,12 +724,45 @@ void fill_devscene(sst_gpu_ctx* ctx, DevScene<R>& sc, const DevBuf& nodes, const
 // Per triangle: the cone from the light that contains it (axis = mean vertex
 // direction, half angle = max vertex angle + padding); cells overlap-tested on the
 // GPU in FP64 (count pass, host prefix sum, fill pass).
+void build_camera_tile_lists(const sst_scene_desc* d, const std::vector<std::array<std::array<double, 3>, 3>>& tv,
+                             const FlatBvh& bvh, std::vector<uint32_t>& off, std::vector<uint32_t>& idx,
+                             uint32_t& tiles_x, uint32_t& tiles_y);
+
 // Camera tiles (types.cuh DevScene::cam_off): per kCamTile x kCamTile pixel tile, the
 // leaf-order triangles that face the camera (a camera ray can only enter them: FP32 outside
 // rays accept entering crossings only) whose projected bounding box, grown by one pixel,
 // meets the tile. A triangle reaching behind the camera goes into every tile.
 void build_camera_tiles(sst_gpu_ctx* ctx, const sst_scene_desc* d,
                         const std::vector<std::array<std::array<double, 3>, 3>>& tv, const FlatBvh& bvh) {
+    auto& cache = ctx->scene_cache;
+    uint64_t fp = fnv(d->cam_position, sizeof d->cam_position, cache.geo_fp);
+    fp = fnv(d->cam_look_at, sizeof d->cam_look_at, fp);
+    fp = fnv(d->cam_up, sizeof d->cam_up, fp);
+    fp = fnv(&d->cam_vfov_deg, sizeof d->cam_vfov_deg, fp);
+    fp = fnv(&d->width, sizeof d->width, fp);
+    fp = fnv(&d->height, sizeof d->height, fp);
+    if (cache.cam_fp != fp || cache.cam_off.empty()) {
+        cache.cam_fp = 0;
+        build_camera_tile_lists(d, tv, bvh, cache.cam_off, cache.cam_idx, cache.cam_tiles_x, cache.cam_tiles_y);
+        cache.cam_fp = fp;
+    }
+    const auto& off = cache.cam_off;
+    const auto& idx = cache.cam_idx;
+    ctx->cam_off.reserve(off.size() * sizeof(uint32_t));
+    ctx->cam_idx.reserve(std::max<size_t>(idx.size(), 1) * sizeof(uint32_t));
+    ctx->cam_tris32.reserve(std::max<size_t>(idx.size(), 1) * sizeof(TriF));
+    CK(cudaMemcpyAsync(ctx->cam_off.p, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (!idx.empty())
+        CK(cudaMemcpyAsync(ctx->cam_idx.p, idx.data(), idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+    ctx->cam_tiles_x = cache.cam_tiles_x;
+    ctx->cam_tiles_y = cache.cam_tiles_y;
+    ctx->cam_list_n = idx.size();
+}
+
+void build_camera_tile_lists(const sst_scene_desc* d, const std::vector<std::array<std::array<double, 3>, 3>>& tv,
+                             const FlatBvh& bvh, std::vector<uint32_t>& off, std::vector<uint32_t>& idx,
+                             uint32_t& tiles_x, uint32_t& tiles_y) {
     auto sub = [](const double* a, const double* b) { return std::array<double, 3>{a[0] - b[0], a[1] - b[1], a[2] - b[2]}; };
     auto cross = [](std::array<double, 3> a, std::array<double, 3> b) {
         return std::array<double, 3>{a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
@@ -776,23 +812,15 @@ void build_camera_tiles(sst_gpu_ctx* ctx, const sst_scene_desc* d,
         for (int y = ty0; y <= ty1; ++y)
             for (int x = tx0; x <= tx1; ++x) tiles[static_cast<size_t>(y) * nx + x].push_back(k);
     }
-    std::vector<uint32_t> off(tiles.size() + 1, 0), idx;
+    off.assign(tiles.size() + 1, 0);
+    idx.clear();
     for (size_t i = 0; i < tiles.size(); ++i) {
         off[i] = static_cast<uint32_t>(idx.size());
         idx.insert(idx.end(), tiles[i].begin(), tiles[i].end());
     }
     off[tiles.size()] = static_cast<uint32_t>(idx.size());
-    ctx->cam_off.reserve(off.size() * sizeof(uint32_t));
-    ctx->cam_idx.reserve(std::max<size_t>(idx.size(), 1) * sizeof(uint32_t));
-    ctx->cam_tris32.reserve(std::max<size_t>(idx.size(), 1) * sizeof(TriF));
-    CK(cudaMemcpyAsync(ctx->cam_off.p, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
-    if (!idx.empty())
-        CK(cudaMemcpyAsync(ctx->cam_idx.p, idx.data(), idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                           ctx->stream));
-    ctx->cam_tiles_x = nx;
-    ctx->cam_tiles_y = ny;
-    ctx->cam_list_n = idx.size();
-    CK(cudaStreamSynchronize(ctx->stream));  // the host vectors die here
+    tiles_x = nx;
+    tiles_y = ny;
 }
 
 void build_light_grid(sst_gpu_ctx* ctx, const sst_scene_desc* d,
