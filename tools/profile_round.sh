@@ -24,7 +24,8 @@ ncu --set full --clock-control none --import-source on -k regex:"k_wf_(logic|tra
 echo "ncu full rc=$?"
 # per-line stalls: ncu attributes the production build's inline-PTX evict_last loads to the
 # asm lines, so the line view comes from a plain-__ldg build of the same sources
-# (tools/build_variant.sh nokeep -DSST_L2_KEEP=0, built before the gpurun call)
+# (tools/build_variant.sh nokeep -DSST_L2_KEEP=0, built here from the current sources)
+tools/build_variant.sh nokeep -DSST_L2_KEEP=0 > gpurun_out/build_nokeep.log 2>&1
 if [ -f build_var/nokeep/libsst_gpu.so ]; then
   SST_GPU_LIB=build_var/nokeep/libsst_gpu.so ncu --set full --clock-control none --import-source on \
       -k regex:"k_wf_(logic|trace|sphere|shadow)" -s 40 -c 5 -o gpurun_out/prof_wf_lines $W > gpurun_out/ncu_d.log 2>&1
