@@ -1458,7 +1458,7 @@ void run_wavefront(sst_gpu_ctx* ctx, TraceArgs<R>& a, bool st, bool explicit_key
     if (ctx->cam_filter && a.sc.n_objects <= 64 && (explicit_keys || a.n_paths % 3 == 0)) {
         // camera pre-pass: paths whose camera ray misses every bounding sphere end here
         const uint64_t n_keys = explicit_keys ? a.n_paths : a.n_paths / 3;
-        sl.keys.reserve(64 + 4 * n_keys);
+        sl.keys.reserve(64 + 5 * n_keys);  // header, list, per-key class byte
         uint32_t* cnt = sl.keys.as<uint32_t>();  // header: total, class counts, class cursors
         CK(cudaMemsetAsync(cnt, 0, 64, stream));
         kt_begin(ctx, stream);  // timed as generation work
@@ -1673,7 +1673,7 @@ void render_impl(sst_gpu_ctx* ctx, int integrator, int nee, uint32_t spp_total, 
         size_t off[kPoolArrays];
         const uint64_t cap = std::max<uint64_t>(32, std::min<uint64_t>(per_sample * chunk, ctx->wf_pool));
         const size_t pool = pool_layout<R>(static_cast<uint32_t>(cap), off);
-        const size_t keys = 64 + 4 * (per_sample * chunk / 3 + 1);  // camera pre-pass list
+        const size_t keys = 64 + 5 * (per_sample * chunk / 3 + 1);  // camera pre-pass list + classes
         bool grow = false;
         for (int k = 0; k < n_slots; ++k) {
             const auto& s2 = ctx->slots[k];

@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(kWfBlock) k_wf_init(TraceArgs<R> a) { wf_init<
 __global__ void k_wf_reset(TraceArgs<R> a) { wf_reset<R>(a.pool); }
 template <bool EX>
 __global__ void __launch_bounds__(kWfBlock) k_wf_cam_filter(TraceArgs<R> a, uint32_t n_keys, uint32_t* list,
-                                                            uint32_t* hdr, int pass) {
-    wf_cam_filter<R, EX>(a, n_keys, list, hdr, pass);
+                                                            uint32_t* hdr, uint8_t* cls_of, int pass) {
+    wf_cam_filter<R, EX>(a, n_keys, list, hdr, cls_of, pass);
 }
 
 // ---------------------------------------------------------------------------
@@ -222,11 +222,14 @@ static unsigned wf_grid(K kernel, uint32_t items, size_t smem = 0) {
 cudaError_t launch_wf_cam_filter(const TraceArgs<R>& a, bool explicit_keys, uint32_t n_keys, uint32_t* list,
                                  uint32_t* count, cudaStream_t s) {
     if (n_keys == 0) return cudaSuccess;
-    for (int pass = 0; pass < 2; ++pass) {  // count per cost class, then scatter
+    uint8_t* cls_of = reinterpret_cast<uint8_t*>(list + n_keys);  // per-key class, after the list
+    for (int pass = 0; pass < 2; ++pass) {  // classify + count, then scatter
         if (explicit_keys)
-            k_wf_cam_filter<true><<<wf_grid(k_wf_cam_filter<true>, n_keys), kWfBlock, 0, s>>>(a, n_keys, list, count, pass);
+            k_wf_cam_filter<true><<<wf_grid(k_wf_cam_filter<true>, n_keys), kWfBlock, 0, s>>>(a, n_keys, list, count,
+                                                                                              cls_of, pass);
         else
-            k_wf_cam_filter<false><<<wf_grid(k_wf_cam_filter<false>, n_keys), kWfBlock, 0, s>>>(a, n_keys, list, count, pass);
+            k_wf_cam_filter<false><<<wf_grid(k_wf_cam_filter<false>, n_keys), kWfBlock, 0, s>>>(a, n_keys, list, count,
+                                                                                                cls_of, pass);
     }
     return cudaGetLastError();
 }

@@ -459,8 +459,8 @@ SST_D bool camera_ray_may_hit(const DevScene<R>& sc, V3<R> d) {
 // (ObjK::cost_class, 0 = densest medium first): expensive paths are generated first, so
 // the pool's drain -- exposed at the end of a launch -- holds the cheap ones. Two passes:
 // pass 0 finishes the misses and counts the classes (hdr[1 + c]); pass 1 scatters each
-// kept key behind the classes before it (cursors hdr[1 + kCostClasses + c]). hdr[0] =
-// the total.
+// kept key behind the classes before it (cursors hdr[1 + kCostClasses + c]), reading the
+// class pass 0 stored per key (cls_of). hdr[0] = the total.
 constexpr uint32_t kCostClasses = 4;
 template <class R>
 SST_D uint32_t camera_ray_class(const DevScene<R>& sc, V3<R> d) {
@@ -475,7 +475,8 @@ SST_D uint32_t camera_ray_class(const DevScene<R>& sc, V3<R> d) {
 }
 
 template <class R, bool EX>
-SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list, uint32_t* hdr, int pass) {
+SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list, uint32_t* hdr, uint8_t* cls_of,
+                         int pass) {
     const DevScene<R>& sc = a.sc;
     unsigned long long done = 0;
     __shared__ uint32_t base_cls[kCostClasses];
@@ -491,12 +492,14 @@ SST_D void wf_cam_filter(const TraceArgs<R>& a, uint32_t n_keys, uint32_t* list,
     for (uint32_t base = blockIdx.x * blockDim.x; base < n_keys; base += stride) {  // block-uniform
         const uint32_t k = base + threadIdx.x;
         uint32_t cls = kCostClasses;
-        if (k < n_keys) {
+        if (k < n_keys && pass == 1) cls = cls_of[k];  // pass 0's class of this key
+        if (k < n_keys && pass == 0) {
             const uint32_t pixel = EX ? a.pixel[k] : k % a.n_pix;
             const uint32_t sample = EX ? a.sample[k] : a.sample_begin + k / a.n_pix;
             const V3<R> d = camera_dir(a, pixel, sample);
             cls = camera_ray_class(sc, d);
-            if (cls == kCostClasses && pass == 0) {
+            cls_of[k] = static_cast<uint8_t>(cls);
+            if (cls == kCostClasses) {
                 const uint32_t n_ch = EX ? 1u : 3u;
                 for (uint32_t j = 0; j < n_ch; ++j) {
                     const uint64_t id = EX ? k : 3ull * k + j;
