@@ -1280,7 +1280,8 @@ WfPool<R> carve_pool(sst_gpu_ctx::Slot& sl, uint32_t cap) {
     q.thit = reinterpret_cast<R*>(base + off[4]);
     q.hinfo = reinterpret_cast<uint2*>(base + off[5]);
     q.nee_p = reinterpret_cast<Q4<R>*>(base + off[6]);
-    q.nee_w = reinterpret_cast<Q4<R>*>(base + off[7]);
+    q.nee_w = reinterpret_cast<Q4<R>*>(base + off[7]);  // contiguous with nee_p: the paired layout
+                                                        // (SST_NEE_PAIR) uses both as one array
     q.q_sphere = reinterpret_cast<uint32_t*>(base + off[8]);
     q.q_shadow = reinterpret_cast<uint32_t*>(base + off[9]);
     q.q_live = reinterpret_cast<uint32_t*>(base + off[10]);
