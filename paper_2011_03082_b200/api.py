@@ -177,7 +177,10 @@ class Renderer:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except (TypeError, AttributeError):  # interpreter shutdown: the ctypes module is gone
+            pass
 
     def __enter__(self):
         return self
