@@ -97,6 +97,20 @@ SST_D Mailbox<R> load_mailbox(const WfPool<R>& q, uint32_t s) {
     return mb;
 }
 
+// A slot's position + radiance and direction + safe radius; SST_SLOT_PAIR keeps both in
+// one 32-byte sector (the sphere kernel's slots are scattered: ~11% of the pool per pass).
+#ifndef SST_SLOT_PAIR
+#define SST_SLOT_PAIR 1
+#endif
+template <class R>
+SST_D Q4<R>& slot_xl(const WfPool<R>& q, uint32_t s) {
+    return SST_SLOT_PAIR ? q.xl[2u * s] : q.xl[s];
+}
+template <class R>
+SST_D Q4<R>& slot_wr(const WfPool<R>& q, uint32_t s) {
+    return SST_SLOT_PAIR ? q.xl[2u * s + 1u] : q.wr[s];
+}
+
 // need_tpend: the queued flight length is only stored while a traversal is queued and
 // only the megakernel hand-off reads it from the slot (the logic pass takes it from the
 // traversal result: a miss leaves t_hit = t_max = the flight length).
@@ -105,7 +119,7 @@ SST_D Mailbox<R> load_mailbox(const WfPool<R>& q, uint32_t s) {
 template <class R>
 SST_D void load_slot_from(const WfPool<R>& q, uint32_t s, const uint4 m, PathLocal<R>& p, uint32_t* phase,
                           const V3<R>& sc_cam_pos, bool need_tpend, bool fold, const Mailbox<R>* mb = nullptr) {
-    const Q4<R> xl = q.xl[s], wr = q.wr[s];
+    const Q4<R> xl = slot_xl(q, s), wr = slot_wr(q, s);
     p.x = mk<R>(xl.x, xl.y, xl.z);
     p.L = xl.w;
     p.w = mk<R>(wr.x, wr.y, wr.z);
@@ -164,8 +178,8 @@ SST_D void load_slot(const WfPool<R>& q, uint32_t s, PathLocal<R>& p, uint32_t* 
 // record's position; store_state here).
 template <class R>
 SST_D void store_state(const WfPool<R>& q, uint32_t s, const PathLocal<R>& p) {
-    q.xl[s] = Q4<R>{p.x.x, p.x.y, p.x.z, p.L};
-    q.wr[s] = Q4<R>{p.w.x, p.w.y, p.w.z, p.r_here};
+    slot_xl(q, s) = Q4<R>{p.x.x, p.x.y, p.x.z, p.L};
+    slot_wr(q, s) = Q4<R>{p.w.x, p.w.y, p.w.z, p.r_here};
     q.rng[s] = p.rng.s;
 }
 template <class R>
@@ -814,8 +828,12 @@ SST_D void wf_logic(const TraceArgs<R>& a, const WfPool<R>& q) {
         if (!q.q_in && threadIdx.x == 0 && base + stride < n_in) {  // slot order: this block's next chunk
             const uint32_t nb = base + stride, cnt = min(blockDim.x, n_in - nb);
             l2_prefetch(q.meta + nb, cnt * sizeof(uint4));
-            l2_prefetch(q.xl + nb, cnt * sizeof(Q4<R>));
-            l2_prefetch(q.wr + nb, cnt * sizeof(Q4<R>));
+            if (SST_SLOT_PAIR) {
+                l2_prefetch(&slot_xl(q, nb), 2u * cnt * sizeof(Q4<R>));
+            } else {
+                l2_prefetch(q.xl + nb, cnt * sizeof(Q4<R>));
+                l2_prefetch(q.wr + nb, cnt * sizeof(Q4<R>));
+            }
             l2_prefetch(q.rng + nb, cnt * sizeof(uint64_t));
         }
 #endif
