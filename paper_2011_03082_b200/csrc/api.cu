@@ -1206,6 +1206,9 @@ void upload_scene_body(sst_gpu_ctx* ctx, const sst_scene_desc* d, bool direction
         ctx->scene_bytes = bytes;
     }
     fill_devscene<float>(ctx, ctx->sc32, ctx->nodes32, ctx->tris32, ctx->objs32);
+    if (ctx->grid_res && ctx->grid_list_n)  // after the FP32 ObjK upload (same stream)
+        CK(launch_grid_sigma(ctx->grid_tris32.as<TriF>(), ctx->grid_list_n, ctx->objs32.as<ObjK<float>>(),
+                             ctx->stream));
     fill_devscene<double>(ctx, ctx->sc64, ctx->nodes64, ctx->tris64, ctx->objs64);
     CK(cudaStreamSynchronize(ctx->stream));
     lap("done");

@@ -487,16 +487,26 @@ SST_D R optical_depth_grid(const DevScene<R>& sc, const RayK<R>& ray, R t_min, R
     R tau = R(0);
     const bool direct = !Real<R>::kIsDouble && sc.grid_tris;  // cell's triangles stored contiguously
     for (uint32_t k = b; k < e; ++k) {
-        const uint32_t i = direct ? k : ldg_keep(sc.grid_tri + k);
         V3<R> v0, e1, e2;
-        uint32_t obj, id;
-        load_tri<R>(direct ? sc.grid_tris : sc.tris, i, v0, e1, e2, obj, id);
+        R sig;
+        if constexpr (!Real<R>::kIsDouble) {
+            if (direct) {  // the copy carries sigma_t per channel in its .w words (k_grid_sigma)
+                const TriF* tr = static_cast<const TriF*>(sc.grid_tris) + k;
+                const float4 p = ldg_keep(&tr->v0o), q = ldg_keep(&tr->e1i), r = ldg_keep(&tr->e2);
+                v0 = mk(p.x, p.y, p.z);
+                e1 = mk(q.x, q.y, q.z);
+                e2 = mk(r.x, r.y, r.z);
+                sig = c == 0 ? p.w : (c == 1 ? q.w : r.w);
+            }
+        }
+        if (!direct) {
+            uint32_t obj, id;
+            load_tri<R>(sc.tris, ldg_keep(sc.grid_tri + k), v0, e1, e2, obj, id);
+            sig = sc.objs[obj].med[c].sigma_t;
+        }
         R det;
         const R t = ray_tri(ray, v0, e1, e2, t_min, t_max, &det);
-        if (t >= R(0)) {
-            const R sig = sc.objs[obj].med[c].sigma_t;
-            tau += det < R(0) ? sig * t : -(sig * t);
-        }
+        if (t >= R(0)) tau += det < R(0) ? sig * t : -(sig * t);
     }
     return tau;
 }

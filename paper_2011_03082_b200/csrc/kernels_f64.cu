@@ -278,7 +278,27 @@ __global__ void k_gather_tris(const uint32_t* __restrict__ idx, const TriF* __re
         out[k] = tris[idx[k]];
 }
 
+// The light grid's FP32 triangle copies carry their object's extinction per channel in
+// the three .w words (v0.w, e1.w, e2.w) instead of object / triangle ids: a shadow ray's
+// hit needs sigma_t and nothing else, and reading it from the record saves the dependent
+// ObjK load (geom.cuh optical_depth_grid).
+__global__ void k_grid_sigma(TriF* __restrict__ t, uint64_t n, const ObjK<float>* __restrict__ objs) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const ObjK<float>& o = objs[__float_as_uint(t[k].v0o.w)];
+        t[k].v0o.w = o.med[0].sigma_t;
+        t[k].e1i.w = o.med[1].sigma_t;
+        t[k].e2.w = o.med[2].sigma_t;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_grid_sigma(TriF* tris, uint64_t n, const ObjK<float>* objs, cudaStream_t s) {
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_grid_sigma<<<static_cast<unsigned>(blocks), 256, 0, s>>>(tris, n, objs);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gather_tris(const uint32_t* idx, const TriF* tris, uint64_t n, TriF* out, cudaStream_t s) {
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);

@@ -77,5 +77,6 @@ struct LightGridArgs {
 cudaError_t launch_light_grid(const LightGridArgs& a, cudaStream_t s);
 // out[k] = tris[idx[k]]: FP32 triangle records in light-grid list order (kernels_f64.cu).
 cudaError_t launch_gather_tris(const uint32_t* idx, const TriF* tris, uint64_t n, TriF* out, cudaStream_t s);
+cudaError_t launch_grid_sigma(TriF* tris, uint64_t n, const ObjK<float>* objs, cudaStream_t s);
 
 }  // namespace sstg
